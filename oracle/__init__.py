@@ -1,0 +1,290 @@
+"""CPU oracle for the LMS hot path (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package.  The product path
+(paper_1606_00803_b200) never imports it and shares no code with it.
+
+Thin ctypes wrapper over oracle/oracle.c (plain C, fp64, -ffp-contract=off).
+Each wrapper cites the passage of PAPER.md (P:<line>) that the C function
+follows; see the header of oracle.c.  Functions with no independent pin are
+listed as "parity unpinned" in DESIGN.md (currently: none).
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-shared", "-fPIC", "-std=c99"]
+
+O_OK, O_E_ARG, O_E_INDEX, O_E_ISOLATED, O_E_PERM, O_E_DEGENERATE, O_E_NOMEM = 0, -1, -2, -3, -4, -5, -6
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: oracle status {status}")
+        self.status = status
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc; no GPU needed)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ct.CDLL(build())
+        P = ct.c_void_p
+        i64, i32, u64 = ct.c_int64, ct.c_int32, ct.c_uint64
+        L.o_build_csr.argtypes = [i64, i32, i64, P, P, ct.POINTER(P), ct.POINTER(i64)]
+        L.o_boundary.argtypes = [i64, i32, i64, P, P]
+        L.o_quality.argtypes = [i32, i64, P, i32, i64, P, P, P]
+        L.o_global_quality.argtypes = [i64, P]
+        L.o_global_quality.restype = ct.c_double
+        L.o_colour.argtypes = [i64, P, P, P, P, P]
+        L.o_colour.restype = i32
+        L.o_hash.argtypes = [u64, u64, u64]
+        L.o_hash.restype = u64
+        L.o_order_original.argtypes = [i64, P]
+        L.o_order_random.argtypes = [i64, u64, P]
+        L.o_order_bfs.argtypes = [i64, P, P, i64, P]
+        L.o_order_rdr.argtypes = [i64, P, P, P, P, P, ct.POINTER(i64), ct.POINTER(i64)]
+        L.o_inverse_perm.argtypes = [i64, P, P]
+        L.o_permute_elems.argtypes = [i64, i32, P, P, P]
+        L.o_permute_csr.argtypes = [i64, P, P, P, P, P, P]
+        L.o_smooth.argtypes = [i32, i64, P, P, P, P, i32, i32]
+        L.o_smooth_omp.argtypes = [i32, i64, P, P, P, P, i32, i32, i32]
+        L.o_smooth_partitioned.argtypes = [i32, i64, P, P, P, P, i32, i32, i32, P]
+        L.o_free.argtypes = [P]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ct.c_void_p)
+
+
+def _ptrs(arrs):
+    arr = (ct.c_void_p * 3)(*[a.ctypes.data for a in arrs] + [0] * (3 - len(arrs)))
+    return arr
+
+
+def _chk(st, what):
+    if st != O_OK:
+        raise OracleError(st, what)
+
+
+# --------------------------------------------------------------------------- O1
+def build_csr(V: int, elems: np.ndarray):
+    """O1 -- vertex adjacency rows (P:244-251 'N neighbored vertices'); int64 row_ptr."""
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    k = elems.shape[1] if elems.ndim == 2 else 3
+    n_el = elems.shape[0] if elems.ndim == 2 else 0
+    row_ptr = np.zeros(V + 1, dtype=np.int64)
+    colp = ct.c_void_p()
+    nnz = ct.c_int64()
+    st = lib().o_build_csr(V, k, n_el, _p(elems), _p(row_ptr), ct.byref(colp), ct.byref(nnz))
+    _chk(st, "o_build_csr")
+    n = nnz.value
+    col = np.ctypeslib.as_array(ct.cast(colp, ct.POINTER(ct.c_int32)), shape=(max(n, 1),))[:n].copy()
+    lib().o_free(colp)
+    return row_ptr, col
+
+
+# --------------------------------------------------------------------------- O2
+def boundary(V: int, elems: np.ndarray) -> np.ndarray:
+    """O2 -- fixed mask: vertices of edges/faces in exactly one element (Alg. 1 'interior vertices')."""
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    fixed = np.zeros(V, dtype=np.uint8)
+    _chk(lib().o_boundary(V, elems.shape[1], elems.shape[0], _p(elems), _p(fixed)), "o_boundary")
+    return fixed
+
+
+# --------------------------------------------------------------------------- O3
+def quality(coords, elems: np.ndarray, return_elem: bool = False):
+    """O3 -- edge-length-ratio quality, per element and per vertex."""
+    coords = [np.ascontiguousarray(c, dtype=np.float64) for c in coords]
+    elems = np.ascontiguousarray(elems, dtype=np.int32)
+    V = coords[0].shape[0]
+    qv = np.zeros(V, dtype=np.float64)
+    qe = np.zeros(max(elems.shape[0], 1), dtype=np.float64)
+    st = lib().o_quality(len(coords), V, _ptrs(coords), elems.shape[1], elems.shape[0],
+                         _p(elems), _p(qe), _p(qv))
+    _chk(st, "o_quality")
+    return (qv, qe[:elems.shape[0]]) if return_elem else qv
+
+
+def global_quality(q_v: np.ndarray) -> float:
+    """Alg. 1 lines 4-8: Global_quality = (1/|V|) * sum of vertex qualities."""
+    q_v = np.ascontiguousarray(q_v, dtype=np.float64)
+    return lib().o_global_quality(q_v.shape[0], _p(q_v))
+
+
+# --------------------------------------------------------------------------- O4
+def colour(row_ptr, col, fixed, orig_id=None):
+    """O4 -- greedy first-fit colouring of free vertices in ascending orig_id (reading Z2)."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    fixed = np.ascontiguousarray(fixed, dtype=np.uint8)
+    V = row_ptr.shape[0] - 1
+    out = np.zeros(V, dtype=np.int8)
+    oid = None if orig_id is None else np.ascontiguousarray(orig_id, dtype=np.int32)
+    C = lib().o_colour(V, _p(row_ptr), _p(col), _p(fixed), None if oid is None else _p(oid), _p(out))
+    if C < 0:
+        raise OracleError(C, "o_colour")
+    return out, int(C)
+
+
+# --------------------------------------------------------------------------- O5
+def hash_u64(seed: int, stream: int, i: int) -> int:
+    return int(lib().o_hash(seed, stream, i))
+
+
+def order_original(V: int) -> np.ndarray:
+    perm = np.zeros(V, dtype=np.int32)
+    lib().o_order_original(V, _p(perm))
+    return perm
+
+
+def order_random(V: int, seed: int) -> np.ndarray:
+    """Random ordering: argsort of H(seed, 4, i) (reading Z15)."""
+    perm = np.zeros(V, dtype=np.int32)
+    _chk(lib().o_order_random(V, seed, _p(perm)), "o_order_random")
+    return perm
+
+
+def order_bfs(row_ptr, col, seed_vertex: int = 0) -> np.ndarray:
+    """BFS ordering (reading Z14)."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    V = row_ptr.shape[0] - 1
+    perm = np.zeros(V, dtype=np.int32)
+    _chk(lib().o_order_bfs(V, _p(row_ptr), _p(col), seed_vertex, _p(perm)), "o_order_bfs")
+    return perm
+
+
+def order_rdr(row_ptr, col, fixed, q, stats: bool = False):
+    """RDR ordering, Alg. 2, literal (readings Z9-Z12)."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    fixed = np.ascontiguousarray(fixed, dtype=np.uint8)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    V = row_ptr.shape[0] - 1
+    perm = np.zeros(V, dtype=np.int32)
+    nw, nt = ct.c_int64(), ct.c_int64()
+    st = lib().o_order_rdr(V, _p(row_ptr), _p(col), _p(fixed), _p(q), _p(perm), ct.byref(nw), ct.byref(nt))
+    _chk(st, "o_order_rdr")
+    if stats:
+        return perm, dict(walks=nw.value, tail=nt.value)
+    return perm
+
+
+# --------------------------------------------------------------------------- O6
+def inverse_perm(perm) -> np.ndarray:
+    perm = np.ascontiguousarray(perm, dtype=np.int32)
+    inv = np.zeros(perm.shape[0], dtype=np.int32)
+    _chk(lib().o_inverse_perm(perm.shape[0], _p(perm), _p(inv)), "o_inverse_perm")
+    return inv
+
+
+def permute_mesh(mesh: dict, perm) -> dict:
+    """O6 -- relabel a mesh dict (coords/fixed/orig_id/colour/elems/csr) with perm[new] = old."""
+    perm = np.ascontiguousarray(perm, dtype=np.int32)
+    inv = inverse_perm(perm)
+    out = dict(mesh)
+    out["coords"] = [np.ascontiguousarray(c[perm]) for c in mesh["coords"]]
+    for key in ("fixed", "orig_id", "colour", "q"):
+        if key in mesh and mesh[key] is not None:
+            out[key] = np.ascontiguousarray(mesh[key][perm])
+    if mesh.get("elems") is not None:
+        el = np.ascontiguousarray(mesh["elems"], dtype=np.int32)
+        e2 = np.zeros_like(el)
+        lib().o_permute_elems(el.shape[0], el.shape[1], _p(inv), _p(el), _p(e2))
+        out["elems"] = e2
+    if mesh.get("row_ptr") is not None:
+        rp = np.ascontiguousarray(mesh["row_ptr"], dtype=np.int64)
+        cl = np.ascontiguousarray(mesh["col"], dtype=np.int32)
+        rp2 = np.zeros_like(rp)
+        cl2 = np.zeros_like(cl)
+        lib().o_permute_csr(rp.shape[0] - 1, _p(perm), _p(inv), _p(rp), _p(cl), _p(rp2), _p(cl2))
+        out["row_ptr"], out["col"] = rp2, cl2
+    return out
+
+
+# --------------------------------------------------------------------------- O7-O9
+def smooth(coords, row_ptr, col, colour_arr, C: int, sweeps: int, threads: int = 0):
+    """O7 (threads=0) / O8 (threads>0) -- colour-ordered Gauss-Seidel LMS sweeps,
+    Eq. 1 in Alg. 1's loop.  Returns new coordinate arrays
+    (and the thread count used when threads>0)."""
+    X = [np.array(c, dtype=np.float64, copy=True) for c in coords]
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    colour_arr = np.ascontiguousarray(colour_arr, dtype=np.int8)
+    V = X[0].shape[0]
+    if threads <= 0:
+        st = lib().o_smooth(len(X), V, _ptrs(X), _p(row_ptr), _p(col), _p(colour_arr), C, sweeps)
+        _chk(st, "o_smooth")
+        return X
+    used = lib().o_smooth_omp(len(X), V, _ptrs(X), _p(row_ptr), _p(col), _p(colour_arr), C, sweeps, threads)
+    if used < 0:
+        raise OracleError(used, "o_smooth_omp")
+    return X, used
+
+
+def smooth_partitioned(coords, row_ptr, col, colour_arr, C: int, sweeps: int, P: int):
+    """O9 -- P contiguous parts with per-colour ghost refresh; returns (coords, bounds)."""
+    X = [np.array(c, dtype=np.float64, copy=True) for c in coords]
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    colour_arr = np.ascontiguousarray(colour_arr, dtype=np.int8)
+    bounds = np.zeros(P + 1, dtype=np.int64)
+    st = lib().o_smooth_partitioned(len(X), X[0].shape[0], _ptrs(X), _p(row_ptr), _p(col),
+                                    _p(colour_arr), C, sweeps, P, _p(bounds))
+    _chk(st, "o_smooth_partitioned")
+    return X, bounds
+
+
+# --------------------------------------------------------------------------- pipeline
+def prepare(mesh: dict) -> dict:
+    """The full oracle pipeline on an input mesh (A2-A5): CSR, fixed mask
+    (generator mask wins when given, reading Z5), colouring from orig_id = label."""
+    V = mesh["coords"][0].shape[0]
+    row_ptr, col = build_csr(V, mesh["elems"])
+    fixed = mesh.get("fixed")
+    if fixed is None:
+        fixed = boundary(V, mesh["elems"])
+    colr, C = colour(row_ptr, col, fixed)
+    out = dict(mesh)
+    out.update(row_ptr=row_ptr, col=col, fixed=np.asarray(fixed, dtype=np.uint8), colour=colr, C=C,
+               orig_id=np.arange(V, dtype=np.int32))
+    return out
+
+
+def order(mesh: dict, kind: str, seed: int = 0) -> np.ndarray:
+    """Dispatch to the four orderings of PAPER.md Fig. 1 / Alg. 2 on a prepared mesh."""
+    V = mesh["coords"][0].shape[0]
+    if kind == "original":
+        return order_original(V)
+    if kind == "random":
+        return order_random(V, seed)
+    if kind == "bfs":
+        return order_bfs(mesh["row_ptr"], mesh["col"], seed)
+    if kind == "rdr":
+        q = mesh.get("q")
+        if q is None:
+            q = quality(mesh["coords"], mesh["elems"])
+        return order_rdr(mesh["row_ptr"], mesh["col"], mesh["fixed"], q)
+    raise ValueError(kind)
