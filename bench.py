@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""bench.py -- vertex-updates/s of the LMS sweep and % of HBM roofline on B200.
+
+Metric (BASELINE.json): "vertex-updates/sec per LMS sweep and % of HBM roofline
+at 1/2/4/8 B200".  Workload at N=1: configs[3] (C4, 2D jittered grid 4096^2,
+16.8 M vertices, 50 sweeps, 738 MB CSR+coords -- larger than the 126 MB L2, so
+no L2 flush is needed between steps), best ordering (original, row-major).
+
+One timed STEP = lms_smooth(mesh, 50 sweeps) on the HBM-resident relabelled
+mesh (A9, the hot loop).  The preparation rows of the path (A2-A8: CSR build,
+fixed mask, colouring, ordering, relabelling, schedule) are timed separately in
+the same run ("setup_ms"), and the end-to-end number ("e2e") runs the WHOLE
+path per step through the public API from pinned host buffers: H2D of
+coordinates + elements, build_csr, order, permute, smooth(50), D2H of the
+smoothed coordinates.
+
+value = V_free * sweeps * steps / t  (t = max over ranks of the CUDA-event time).
+roofline.achieved = B_sweep * sweeps / (sweep-kernel time per step),
+B_sweep = 4(V+1) + 4 nnz + 8 d V + 8 d V_free bytes.
+
+--impl reference: the CPU oracle (oracle/, test infrastructure) timed as it
+stands on the host cores, each step one colour-GS sweep of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import meshgen  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C4")
+    p.add_argument("--ordering", default="original")
+    p.add_argument("--sweeps", type=int, default=0, help="0 = the config's sweep count")
+    p.add_argument("--schedule", default="auto", choices=["auto", "s1", "s3"])
+    p.add_argument("--tile", type=int, default=0)
+    p.add_argument("--lag", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-sweeps", type=int, default=2)
+    return p.parse_args()
+
+
+def b_sweep(dim, V, nnz, vfree):
+    return 4 * (V + 1) + 4 * nnz + 8 * dim * V + 8 * dim * vfree
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.maxclk = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.maxclk = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def record(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.maxclk, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.maxclk,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def load_traffic(config, ordering, kernel):
+    """ncu dram bytes per launch of the sweep kernel from the committed summary (or None)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        for rec in d.get("kernels", []):
+            if rec.get("config") == config and rec.get("ordering") == ordering and rec.get("kernel") == kernel:
+                return rec
+    except Exception:
+        pass
+    return None
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The CPU oracle as it stands on the host cores (bounded sample per step)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    cfg = meshgen.CONFIGS[args.config]
+    m = meshgen.make_config(args.config)
+    om = oracle.prepare(m)
+    if args.ordering != "original":
+        om = oracle.permute_mesh(om, oracle.order(om, args.ordering, meshgen.RANDOM_ORDER_SEED))
+    V = om["coords"][0].shape[0]
+    vfree = int((om["fixed"] == 0).sum())
+    cores = len(os.sched_getaffinity(0))
+    X = om["coords"]
+    for _ in range(args.warmup):
+        X, used = oracle.smooth(X, om["row_ptr"], om["col"], om["colour"], om["C"], 1, threads=cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        X, used = oracle.smooth(X, om["row_ptr"], om["col"], om["colour"], om["C"], 1, threads=cores)
+    dt = time.perf_counter() - t0
+    value = vfree * args.steps / dt
+    sample = f"{args.config} ({V} vertices, {args.ordering} ordering), 1 colour-GS sweep per step, o_smooth_omp"
+    line = {"impl": "reference", "metric": "vertex-updates/sec per LMS sweep", "value": value,
+            "unit": "vertex-updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['args']}, {args.ordering} ordering",
+                       "sweeps_per_step": 1},
+            "cpu_baseline": {"value": value, "unit": "vertex-updates/s", "cores": used, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "vertex-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- our arm
+def cpu_baseline(args, m):
+    import oracle
+    t0 = time.perf_counter()
+    om = oracle.prepare(m)
+    if args.ordering != "original":
+        om = oracle.permute_mesh(om, oracle.order(om, args.ordering, meshgen.RANDOM_ORDER_SEED))
+    prep = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    vfree = int((om["fixed"] == 0).sum())
+    t0 = time.perf_counter()
+    X, used = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], args.cpu_sweeps,
+                            threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": vfree * args.cpu_sweeps / dt, "unit": "vertex-updates/s", "cores": used, "kind": "oracle",
+            "sample": f"{args.cpu_sweeps} colour-GS sweeps of the full {args.config} mesh ({args.ordering}), "
+                      f"o_smooth_omp, sweep loop only (oracle prep {prep:.1f}s untimed)"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1606_00803_b200 as lms
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    cfg = meshgen.CONFIGS[args.config]
+    sweeps = args.sweeps or cfg["sweeps"]
+    m = meshgen.make_config(args.config)
+    dim = m["dim"]
+    V = m.V
+
+    # ---------------- setup phases (A2-A8), each timed with CUDA events
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+    coords_d = [torch.from_numpy(c).to(dev) for c in m["coords"]]
+    elems_d = torch.from_numpy(m["elems"]).to(dev)
+    torch.cuda.synchronize()
+    setup = {}
+    e0 = ev()
+    gm = lms.Mesh.build_csr(coords_d, elems_d)
+    e1 = ev()
+    perm = gm.order(args.ordering, meshgen.RANDOM_ORDER_SEED if args.ordering == "random" else 0)
+    e2 = ev()
+    gm.permute(perm)
+    e3 = ev()
+    gm.set_schedule(args.schedule, args.tile, args.lag)
+    gm.smooth(0)
+    # schedule build happens lazily on the first non-zero smooth: time it via 1 sweep minus a sweep
+    torch.cuda.synchronize()
+    setup["build_csr+boundary+colour"] = e0.elapsed_time(e1)
+    setup["order_" + args.ordering] = e1.elapsed_time(e2)
+    setup["permute"] = e2.elapsed_time(e3)
+    e4 = ev()
+    gm.smooth(1)  # builds the schedule + 1 sweep
+    e5 = ev()
+    torch.cuda.synchronize()
+    setup["schedule+1sweep"] = e4.elapsed_time(e5)
+    info = gm.info()
+    sinfo = gm.schedule_info()
+    nnz, C, vfree = info["nnz"], info["C"], sinfo["n_free"]
+    bsw = b_sweep(dim, V, nnz, vfree)
+
+    # ---------------- timed steps: lms_smooth(sweeps)
+    for _ in range(args.warmup):
+        gm.smooth(sweeps)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lms.kernel_launches()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            starts[i].record(stream)
+            gm.smooth(sweeps)
+            ends[i].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = lms.kernel_launches() - launches0
+    t_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kernel_ms = statistics.mean(step_ms)  # one sweep kernel launch (S3) / the graph of colour kernels (S1)
+    value = vfree * sweeps * args.steps / (t_ms / 1e3) * world
+    peak, peak_src = peaks()
+    achieved = bsw * sweeps / (kernel_ms / 1e3) / 1e9
+    kname = "k_sweep_s3" if sinfo["kind"] == "s3" else "k_sweep_s1"
+    tr = load_traffic(args.config, args.ordering, kname)
+    traffic = None
+    if tr is not None and tr.get("sweeps"):
+        traffic = tr["dram_bytes"] / tr["sweeps"] * sweeps
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": peak_src, "kernel": kname,
+            "bytes_per_launch": bsw * sweeps, "launch_ms": kernel_ms,
+            "b_sweep": bsw, "frac_of_8TBs_nominal": achieved / 8000.0}
+
+    # ---------------- e2e: whole path from pinned host buffers, every step
+    e2e = None
+    if not args.no_e2e:
+        hc = [torch.from_numpy(c).pin_memory() for c in m["coords"]]
+        he = torch.from_numpy(m["elems"]).pin_memory()
+        hout = [torch.empty(V, dtype=torch.float64).pin_memory() for _ in range(dim)]
+        h2d = sum(t.numel() * t.element_size() for t in hc) + he.numel() * he.element_size()
+        d2h = sum(t.numel() * t.element_size() for t in hout)
+
+        def e2e_step():
+            dc = [t.to(dev, non_blocking=True) for t in hc]
+            de = he.to(dev, non_blocking=True)
+            g = lms.Mesh.build_csr(dc, de)
+            p = g.order(args.ordering, meshgen.RANDOM_ORDER_SEED if args.ordering == "random" else 0)
+            g.permute(p)
+            g.set_schedule(args.schedule, args.tile, args.lag)
+            g.smooth(sweeps)
+            out = g.coords()
+            for o, h in zip(out, hout):
+                h.copy_(o, non_blocking=True)
+            torch.cuda.synchronize()
+            g.close()
+        e2e_step()
+        n_e2e = max(1, min(args.steps, 3))
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = a.elapsed_time(b) / n_e2e
+        e2e = {"value": vfree * sweeps / (e_ms / 1e3) * world, "unit": "vertex-updates/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
+               "steps": n_e2e,
+               "path": "H2D coords+elems -> build_csr -> order -> permute -> smooth(%d) -> D2H coords" % sweeps}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(args, m)
+
+    if rank == 0:
+        line = {
+            "metric": "vertex-updates/sec per LMS sweep (and % of HBM roofline)",
+            "value": value, "unit": "vertex-updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: 2D jittered grid {cfg['args']}, {args.ordering} ordering, "
+                                   f"{sweeps} colour-GS sweeps per step",
+                       "config": args.config, "ordering": args.ordering, "sweeps_per_step": sweeps,
+                       "V": V, "V_free": vfree, "nnz": nnz, "colours": C, "schedule": sinfo,
+                       "l2": "inputs larger than L2 (resident CSR+coords %.0f MB > 126 MB); no flush" %
+                             ((4 * (V + 1) + 4 * nnz + 8 * dim * V) / 1e6),
+                       "parallelism": f"contiguous vertex ranges x{world}" if world > 1 else "1 GPU"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.record(),
+            "setup_ms": setup,
+        }
+        print(json.dumps(line), flush=True)
+    gm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * lms.h -- C ABI of liblms.so, the B200 (sm_100a) implementation of the
+ * data-parallel hot path of Aupy, Park & Raghavan, "Locality-Aware Laplacian
+ * Mesh Smoothing" (arXiv 1606.00803).  PAPER.md lines are cited as P:<n>.
+ *
+ * The path: build the vertex-adjacency CSR of a triangle/tetrahedral mesh,
+ * compute a vertex ordering (random, original, BFS, or the paper's RDR,
+ * Alg. 2), relabel the mesh by it, and run Laplacian smoothing sweeps
+ * (Eq. 1) with a fixed vertex-colouring Gauss-Seidel schedule.
+ *
+ * Conventions (all entry points):
+ *  - Pointers named d_* are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *    on the current CUDA device; the caller owns them.  They are read (or
+ *    written, for outputs) during the call and never retained.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Work is enqueued on it; calls that must inspect device results (sizes,
+ *    validation flags) synchronise it before returning.
+ *  - Coordinates are structure-of-arrays fp64: d_coords is a HOST array of
+ *    `dim` device pointers, each to double[n_vertices].
+ *  - Indices are int32 (meshes with fewer than 2^31 vertices and 2^31 CSR
+ *    entries); elements are element-major int32[n_elems][verts_per_elem].
+ *  - Every function returns an lms_status; on a non-OK status,
+ *    lms_last_error() returns a message (thread-local) and the mesh handle is
+ *    left unchanged (lms_permute validates before it mutates).
+ *  - A handle must not be used by two threads at once; distinct handles are
+ *    independent.  The handle owns all derived device memory.
+ */
+#ifndef LMS_H
+#define LMS_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lms_mesh_s* lms_mesh_t;
+typedef void* lms_stream_t; /* cudaStream_t */
+
+typedef enum {
+    LMS_OK = 0,
+    LMS_E_ARG = -1,        /* bad argument: dim not in {2,3}, k not in {3,4}, sweeps < 0, unknown kind,
+                              BFS seed vertex out of range, NULL pointer, size overflow */
+    LMS_E_INDEX = -2,      /* element index out of [0, V), or a repeated vertex within one element */
+    LMS_E_ISOLATED = -3,   /* a vertex with no neighbour (deg 0) */
+    LMS_E_PERM = -4,       /* perm is not a bijection of [0, V) */
+    LMS_E_DEGENERATE = -5, /* element whose vertices all coincide (quality undefined) */
+    LMS_E_NOMEM = -6,      /* device allocation failed */
+    LMS_E_CUDA = -7,       /* CUDA runtime error (message in lms_last_error) */
+    LMS_E_NCCL = -8,       /* reserved for the multi-GPU path */
+    LMS_E_STATE = -9       /* handle not in a state that allows the call (e.g. RDR without quality) */
+} lms_status;
+
+typedef enum {
+    LMS_ORDER_ORIGINAL = 0, /* identity: the generator / Triangle order */
+    LMS_ORDER_RANDOM = 1,   /* random storage order: argsort of H(seed, 4, i) */
+    LMS_ORDER_BFS = 2,      /* breadth-first order, Strout-Hovland */
+    LMS_ORDER_RDR = 3       /* Reuse-Distance-Reducing order, Alg. 2 */
+} lms_order_kind;
+
+typedef enum {
+    LMS_SCHED_AUTO = 0,     /* pick per mesh: S3 when the ordering is banded, else S1 */
+    LMS_SCHED_S1 = 1,       /* one launch per colour (CUDA-graph captured sweep) */
+    LMS_SCHED_S3 = 3        /* persistent colour-pipelined sweep with per-tile progress flags */
+} lms_schedule_kind;
+
+/* ---------------------------------------------------------------------------
+ * lms_build_csr -- build a mesh handle from elements.
+ *  Computes, on the GPU:
+ *   - the vertex adjacency N(v) = {u != v : u, v share an element}, rows
+ *     ascending ("N neighbored vertices", Eq. 1);
+ *   - the fixed mask: if d_fixed is NULL, a vertex is fixed iff it lies on an
+ *     edge (triangles) / face (tetrahedra) that belongs to exactly one element
+ *     (Alg. 1 smooths "interior vertices"); else the caller's mask
+ *     (1 = fixed) is copied;
+ *   - orig_id = input label, and the colouring schedule: greedy first-fit
+ *     over free vertices in ascending orig_id (reading Z2).
+ *  dim: 2 or 3; verts_per_elem: 3 (triangles) or 4 (tetrahedra).
+ *  d_coords: host array of dim device pointers, double[n_vertices] each.
+ *  d_elems: int32[n_elems * verts_per_elem].  d_fixed: uint8[n_vertices] or NULL.
+ *  Errors: LMS_E_ARG, LMS_E_INDEX (out-of-range or repeated vertex in an
+ *  element), LMS_E_ISOLATED, LMS_E_NOMEM, LMS_E_CUDA.  *out is set only on OK.
+ *  The elements are copied into the handle (needed for quality / RDR).
+ */
+lms_status lms_build_csr(int32_t dim, int64_t n_vertices, const double* const* d_coords,
+                         int32_t verts_per_elem, int64_t n_elems, const int32_t* d_elems,
+                         const uint8_t* d_fixed, lms_stream_t stream, lms_mesh_t* out);
+
+/* lms_mesh_from_csr -- build a handle from a ready CSR (test/debug entry).
+ *  d_row_ptr int32[V+1], d_col_idx int32[nnz] (rows ascending, symmetric, no
+ *  self loops -- not re-validated beyond index range and deg >= 1).
+ *  d_fixed uint8[V] (required).  d_orig_id int32[V] or NULL (= identity).
+ *  d_colour int8[V] or NULL (= computed from orig_id as in lms_build_csr);
+ *  fixed vertices must carry colour -1.  d_quality double[V] or NULL (RDR then
+ *  needs it: without elements there is no quality).  Errors as lms_build_csr. */
+lms_status lms_mesh_from_csr(int32_t dim, int64_t n_vertices, const double* const* d_coords,
+                             const uint8_t* d_fixed, const int32_t* d_row_ptr, const int32_t* d_col_idx,
+                             const int32_t* d_orig_id, const int8_t* d_colour, const double* d_quality,
+                             lms_stream_t stream, lms_mesh_t* out);
+
+void lms_mesh_destroy(lms_mesh_t m);
+
+/* ---------------------------------------------------------------------------
+ * lms_order -- compute a vertex ordering of the mesh in its CURRENT labels
+ * (SURVEY 8(a) A6).  d_perm (out): int32[V], perm[new] = old (P:420,
+ * "V_new[next_num] <- V[i]").
+ *  ORIGINAL: identity.  RANDOM: indices sorted by H(seed, 4, i) (SplitMix64
+ *  counter hash, reading Z15).  BFS: queue BFS from vertex `seed`,
+ *  neighbours in ascending label, restart at the smallest unvisited label
+ *  (reading Z14); LMS_E_ARG if seed >= V.  RDR: Alg. 2 over the
+ *  initial vertex qualities (edge-length ratio) with ties broken
+ *  by label, l[0] = lowest-(quality,label) unprocessed neighbour, fixed
+ *  vertices allowed inside walks, never-reached vertices appended in
+ *  ascending label (readings Z9-Z13); `seed` unused.  RDR computes the
+ *  quality from the stored elements (LMS_E_DEGENERATE on a degenerate one)
+ *  or uses the quality given to lms_mesh_from_csr (else LMS_E_STATE).
+ */
+lms_status lms_order(lms_mesh_t m, lms_order_kind kind, uint64_t seed, int32_t* d_perm,
+                     lms_stream_t stream);
+
+/* lms_permute -- relabel the mesh in place by d_perm (int32[V], perm[new]=old)
+ * (SURVEY 8(a) A7): coordinates, fixed, colour, orig_id and quality are
+ * gathered (X'[k] = X[perm[k]]), elements remapped through inv (element and
+ * slot order kept), CSR rows remapped and re-sorted ascending.  The colour
+ * moves with its vertex, so lms_smooth's result is ordering-independent up to
+ * the rounding of the neighbour sums.  LMS_E_PERM if not a bijection
+ * (checked before anything is modified). */
+lms_status lms_permute(lms_mesh_t m, const int32_t* d_perm, lms_stream_t stream);
+
+/* lms_smooth -- run exactly `sweeps` LMS sweeps in place.
+ * One sweep = for c in 0..C-1: every free vertex v of colour c moves to
+ * (sum of its neighbours' coordinates, in CSR order) / deg(v), per axis, with
+ * IEEE binary64 round-to-nearest adds and division and no FMA (Eq. 1,
+ * P:244-251, inside Alg. 1's loop over interior vertices, under
+ * the colour-ordered Gauss-Seidel schedule of DESIGN.md reading Z1).  Fixed
+ * vertices never move.  sweeps == 0 is a no-op; sweeps < 0 -> LMS_E_ARG.
+ * The schedule (S1/S3) is chosen by lms_set_schedule; all are bit-identical. */
+lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream);
+
+/* lms_set_schedule -- choose the sweep kernel.  tile: vertices per tile
+ * (0 = default); lag: S3 tile lag L (0 = automatic).  Takes effect at the next
+ * lms_smooth (the internal schedule is rebuilt lazily). */
+lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, int32_t lag);
+
+/* ---------------------------------------------------------------------------
+ * Accessors.  Outputs are caller-owned device buffers of the stated sizes.   */
+lms_status lms_mesh_info(lms_mesh_t m, int64_t* n_vertices, int64_t* nnz, int32_t* n_colours,
+                         int32_t* dim);
+/* n_free: free (non-fixed) vertices; sched_kind: the kernel the next lms_smooth
+ * uses (resolved AUTO); tile/lag: its parameters (0 before the first smooth). */
+lms_status lms_schedule_info(lms_mesh_t m, int64_t* n_free, int32_t* sched_kind, int32_t* tile,
+                             int32_t* lag);
+lms_status lms_export_coords(lms_mesh_t m, double* const* d_out, lms_stream_t stream);
+lms_status lms_import_coords(lms_mesh_t m, const double* const* d_in, lms_stream_t stream);
+lms_status lms_export_csr(lms_mesh_t m, int32_t* d_row_ptr, int32_t* d_col_idx, lms_stream_t stream);
+lms_status lms_export_colour(lms_mesh_t m, int8_t* d_colour, lms_stream_t stream);
+lms_status lms_export_fixed(lms_mesh_t m, uint8_t* d_fixed, lms_stream_t stream);
+lms_status lms_export_orig_id(lms_mesh_t m, int32_t* d_orig_id, lms_stream_t stream);
+/* d_elems int32[n_elems * k]; LMS_E_STATE if the handle has no elements. */
+lms_status lms_export_elems(lms_mesh_t m, int32_t* d_elems, lms_stream_t stream);
+/* Vertex quality q_v (mean edge-length ratio of attached
+ * elements), computed from the current coordinates (A4). */
+lms_status lms_export_quality(lms_mesh_t m, double* d_quality, lms_stream_t stream);
+
+/* Thread-local message for the last non-OK status of this thread. */
+const char* lms_last_error(void);
+/* Number of CUDA kernels this library launched on this thread since load
+ * (used by bench.py for its gpu_launches claim). */
+int64_t lms_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMS_H */

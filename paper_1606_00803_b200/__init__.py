@@ -1,0 +1,13 @@
+"""B200-native LMS (Laplacian Mesh Smoothing) hot path of arXiv 1606.00803.
+
+Thin Python binding over liblms.so (include/lms.h): argument marshalling only.
+Every step of the path -- CSR build, fixed mask, colouring, quality, the four
+orderings, relabelling and the sweep -- runs in the library's CUDA kernels.
+PyTorch provides device memory and streams only.  There is no CPU fallback:
+if the CUDA library or a GPU is missing, calls raise.
+"""
+from ._lms import (  # noqa: F401
+    LMSError, Mesh, ORDERINGS, SCHEDULES, lib, load_library, kernel_launches,
+)
+
+__all__ = ["LMSError", "Mesh", "ORDERINGS", "SCHEDULES", "lib", "load_library", "kernel_launches"]

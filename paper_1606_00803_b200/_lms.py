@@ -1,0 +1,266 @@
+"""ctypes binding of liblms.so; names follow include/lms.h.
+
+Arguments are torch CUDA tensors (device memory) and torch CUDA streams; the
+binding only checks dtypes/shapes/devices and passes raw pointers.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+import torch
+
+from . import build_lib
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+
+ORDERINGS = {"original": 0, "random": 1, "bfs": 2, "rdr": 3}
+SCHEDULES = {"auto": 0, "s1": 1, "s3": 3}
+SCHED_NAMES = {v: k for k, v in SCHEDULES.items()}
+
+LMS_STATUS = {0: "LMS_OK", -1: "LMS_E_ARG", -2: "LMS_E_INDEX", -3: "LMS_E_ISOLATED", -4: "LMS_E_PERM",
+              -5: "LMS_E_DEGENERATE", -6: "LMS_E_NOMEM", -7: "LMS_E_CUDA", -8: "LMS_E_NCCL", -9: "LMS_E_STATE"}
+
+# every symbol include/lms.h declares (tests check the library exports them all)
+EXPORTS = ["lms_build_csr", "lms_mesh_from_csr", "lms_mesh_destroy", "lms_order", "lms_permute", "lms_smooth",
+           "lms_set_schedule", "lms_mesh_info", "lms_schedule_info", "lms_export_coords", "lms_import_coords",
+           "lms_export_csr", "lms_export_colour", "lms_export_fixed", "lms_export_orig_id", "lms_export_elems",
+           "lms_export_quality", "lms_last_error", "lms_kernel_launches"]
+
+
+class LMSError(RuntimeError):
+    def __init__(self, status: int, what: str, msg: str):
+        super().__init__(f"{what}: {LMS_STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = LMS_STATUS.get(status, str(status))
+
+
+_lib = None
+
+
+def load_library(build: bool = True):
+    """Load (building if stale and `build`) the in-tree liblms.so."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = build_lib.build() if build else build_lib.LIB
+    if not os.path.exists(path):
+        raise RuntimeError(f"liblms.so not found at {path}; run __graft_entry__.build()")
+    L = ct.CDLL(path)
+    P, i32, i64, u64 = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_uint64
+    PP = ct.POINTER(ct.c_void_p)
+    sig = {
+        "lms_build_csr": [i32, i64, PP, i32, i64, P, P, P, ct.POINTER(P)],
+        "lms_mesh_from_csr": [i32, i64, PP, P, P, P, P, P, P, P, ct.POINTER(P)],
+        "lms_mesh_destroy": [P],
+        "lms_order": [P, i32, u64, P, P],
+        "lms_permute": [P, P, P],
+        "lms_smooth": [P, i32, P],
+        "lms_set_schedule": [P, i32, i32, i32],
+        "lms_mesh_info": [P, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i32), ct.POINTER(i32)],
+        "lms_schedule_info": [P, ct.POINTER(i64), ct.POINTER(i32), ct.POINTER(i32), ct.POINTER(i32)],
+        "lms_export_coords": [P, PP, P],
+        "lms_import_coords": [P, PP, P],
+        "lms_export_csr": [P, P, P, P],
+        "lms_export_colour": [P, P, P],
+        "lms_export_fixed": [P, P, P],
+        "lms_export_orig_id": [P, P, P],
+        "lms_export_elems": [P, P, P],
+        "lms_export_quality": [P, P, P],
+        "lms_last_error": [],
+        "lms_kernel_launches": [],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = i32
+    L.lms_mesh_destroy.restype = None
+    L.lms_last_error.restype = ct.c_char_p
+    L.lms_kernel_launches.restype = i64
+    _lib = L
+    return L
+
+
+def lib():
+    return load_library()
+
+
+def kernel_launches() -> int:
+    return int(lib().lms_kernel_launches())
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        raise LMSError(st, what, lib().lms_last_error().decode(errors="replace"))
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ct.c_void_p(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor, dtype, n=None, name="tensor"):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"{name} must have {n} elements, got {t.numel()}")
+    return ct.c_void_p(t.data_ptr())
+
+
+def _ptr_array(ts):
+    arr = (ct.c_void_p * 3)()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr()
+    return ct.cast(arr, ct.POINTER(ct.c_void_p)), arr
+
+
+class Mesh:
+    """Owner of an lms_mesh_t handle (include/lms.h)."""
+
+    def __init__(self, handle: ct.c_void_p):
+        self._h = handle
+
+    # ------------------------------------------------------------ constructors
+    @classmethod
+    def build_csr(cls, coords, elems: torch.Tensor, fixed: torch.Tensor | None = None, stream=None) -> "Mesh":
+        """lms_build_csr: coords = list of dim float64 CUDA tensors [V]; elems int32 [n_el, k]."""
+        dim = len(coords)
+        V = coords[0].numel()
+        for c in coords:
+            _dev(c, torch.float64, V, "coords")
+        if elems.dim() != 2:
+            raise ValueError("elems must be [n_elems, verts_per_elem]")
+        pe = _dev(elems, torch.int32, name="elems")
+        pf = None if fixed is None else _dev(fixed, torch.uint8, V, "fixed")
+        pp, keep = _ptr_array(coords)
+        h = ct.c_void_p()
+        _check(lib().lms_build_csr(dim, V, pp, elems.shape[1], elems.shape[0], pe, pf, _stream(stream),
+                                   ct.byref(h)), "lms_build_csr")
+        return cls(h)
+
+    @classmethod
+    def from_csr(cls, coords, fixed, row_ptr, col, orig_id=None, colour=None, quality=None, stream=None) -> "Mesh":
+        dim = len(coords)
+        V = coords[0].numel()
+        for c in coords:
+            _dev(c, torch.float64, V, "coords")
+        pp, keep = _ptr_array(coords)
+        h = ct.c_void_p()
+        _check(lib().lms_mesh_from_csr(
+            dim, V, pp, _dev(fixed, torch.uint8, V, "fixed"), _dev(row_ptr, torch.int32, V + 1, "row_ptr"),
+            _dev(col, torch.int32, name="col"),
+            None if orig_id is None else _dev(orig_id, torch.int32, V, "orig_id"),
+            None if colour is None else _dev(colour, torch.int8, V, "colour"),
+            None if quality is None else _dev(quality, torch.float64, V, "quality"),
+            _stream(stream), ct.byref(h)), "lms_mesh_from_csr")
+        return cls(h)
+
+    def close(self):
+        if self._h:
+            lib().lms_mesh_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ------------------------------------------------------------ info
+    def info(self):
+        V, nnz, C, dim = ct.c_int64(), ct.c_int64(), ct.c_int32(), ct.c_int32()
+        _check(lib().lms_mesh_info(self._h, ct.byref(V), ct.byref(nnz), ct.byref(C), ct.byref(dim)), "lms_mesh_info")
+        return dict(V=V.value, nnz=nnz.value, C=C.value, dim=dim.value)
+
+    def schedule_info(self):
+        nf, kind, tile, lag = ct.c_int64(), ct.c_int32(), ct.c_int32(), ct.c_int32()
+        _check(lib().lms_schedule_info(self._h, ct.byref(nf), ct.byref(kind), ct.byref(tile), ct.byref(lag)),
+               "lms_schedule_info")
+        return dict(n_free=nf.value, kind=SCHED_NAMES.get(kind.value, kind.value), tile=tile.value, lag=lag.value)
+
+    @property
+    def V(self):
+        return self.info()["V"]
+
+    # ------------------------------------------------------------ the path
+    def order(self, kind: str, seed: int = 0, stream=None) -> torch.Tensor:
+        """lms_order -> perm int32[V] (perm[new] = old)."""
+        V = self.V
+        perm = torch.empty(V, dtype=torch.int32, device="cuda")
+        _check(lib().lms_order(self._h, ORDERINGS[kind], seed, _dev(perm, torch.int32, V), _stream(stream)),
+               "lms_order")
+        return perm
+
+    def order_into(self, kind: str, perm: torch.Tensor, seed: int = 0, stream=None):
+        _check(lib().lms_order(self._h, ORDERINGS[kind], seed, _dev(perm, torch.int32, self.V), _stream(stream)),
+               "lms_order")
+
+    def permute(self, perm: torch.Tensor, stream=None):
+        _check(lib().lms_permute(self._h, _dev(perm, torch.int32, self.V, "perm"), _stream(stream)), "lms_permute")
+
+    def smooth(self, sweeps: int, stream=None):
+        _check(lib().lms_smooth(self._h, sweeps, _stream(stream)), "lms_smooth")
+
+    def set_schedule(self, kind: str = "auto", tile: int = 0, lag: int = 0):
+        _check(lib().lms_set_schedule(self._h, SCHEDULES[kind], tile, lag), "lms_set_schedule")
+
+    # ------------------------------------------------------------ export / import
+    def coords(self, stream=None):
+        inf = self.info()
+        out = [torch.empty(inf["V"], dtype=torch.float64, device="cuda") for _ in range(inf["dim"])]
+        self.export_coords(out, stream)
+        return out
+
+    def export_coords(self, out, stream=None):
+        inf = self.info()
+        for t in out:
+            if t.dtype != torch.float64 or t.numel() != inf["V"] or not t.is_contiguous():
+                raise ValueError("coordinate buffers must be contiguous float64[V]")
+        pp, keep = _ptr_array(out)
+        _check(lib().lms_export_coords(self._h, pp, _stream(stream)), "lms_export_coords")
+
+    def import_coords(self, coords, stream=None):
+        inf = self.info()
+        for t in coords:
+            if t.dtype != torch.float64 or t.numel() != inf["V"] or not t.is_contiguous():
+                raise ValueError("coordinate buffers must be contiguous float64[V]")
+        pp, keep = _ptr_array(coords)
+        _check(lib().lms_import_coords(self._h, pp, _stream(stream)), "lms_import_coords")
+
+    def csr(self, stream=None):
+        inf = self.info()
+        rp = torch.empty(inf["V"] + 1, dtype=torch.int32, device="cuda")
+        col = torch.empty(max(inf["nnz"], 1), dtype=torch.int32, device="cuda")
+        _check(lib().lms_export_csr(self._h, ct.c_void_p(rp.data_ptr()), ct.c_void_p(col.data_ptr()),
+                                    _stream(stream)), "lms_export_csr")
+        return rp, col[:inf["nnz"]]
+
+    def colour(self, stream=None):
+        out = torch.empty(self.V, dtype=torch.int8, device="cuda")
+        _check(lib().lms_export_colour(self._h, ct.c_void_p(out.data_ptr()), _stream(stream)), "lms_export_colour")
+        return out
+
+    def fixed(self, stream=None):
+        out = torch.empty(self.V, dtype=torch.uint8, device="cuda")
+        _check(lib().lms_export_fixed(self._h, ct.c_void_p(out.data_ptr()), _stream(stream)), "lms_export_fixed")
+        return out
+
+    def orig_id(self, stream=None):
+        out = torch.empty(self.V, dtype=torch.int32, device="cuda")
+        _check(lib().lms_export_orig_id(self._h, ct.c_void_p(out.data_ptr()), _stream(stream)), "lms_export_orig_id")
+        return out
+
+    def quality(self, stream=None):
+        out = torch.empty(self.V, dtype=torch.float64, device="cuda")
+        _check(lib().lms_export_quality(self._h, ct.c_void_p(out.data_ptr()), _stream(stream)), "lms_export_quality")
+        return out

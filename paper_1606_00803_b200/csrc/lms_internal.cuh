@@ -1,0 +1,155 @@
+// lms_internal.cuh -- shared internals of liblms.so (the CUDA product path).
+// Nothing here is shared with oracle/ (the CPU oracle is independent).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/lms.h"
+
+namespace lms {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+void note_launch(int64_t n = 1);
+
+struct Err {
+  lms_status st;
+  std::string msg;
+};
+
+#define LMS_TRY_CUDA(expr)                                                                     \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess) {                                                                   \
+      throw ::lms::Err{_e == cudaErrorMemoryAllocation ? LMS_E_NOMEM : LMS_E_CUDA,             \
+                       std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" + __FILE__ + \
+                           ":" + std::to_string(__LINE__)};                                    \
+    }                                                                                          \
+  } while (0)
+
+#define LMS_CHECK_LAUNCH()                \
+  do {                                    \
+    ::lms::note_launch();                 \
+    LMS_TRY_CUDA(cudaGetLastError());     \
+  } while (0)
+
+inline void fail(lms_status st, const std::string& msg) { throw Err{st, msg}; }
+
+// ----------------------------------------------------------------- device buffers
+// RAII device buffer allocated stream-ordered (cudaMallocAsync) on the handle's stream.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    // the old buffer is freed in the order of the NEW buffer's stream (the
+    // stream of the call that produced the replacement)
+    if (this != &o) {
+      if (p) cudaFreeAsync(p, o.s);
+      p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) LMS_TRY_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+// ----------------------------------------------------------------- schedule
+// Sweep schedule: free vertices grouped into work items
+// (tile k, colour c), tile = T consecutive storage positions; inside an item
+// the vertices are in ascending storage index.  Rows are copied in CSR order
+// ("colour-sliced CSR"), so each item streams its own rows contiguously.
+struct Schedule {
+  bool valid = false;
+  int kind = 0;          // LMS_SCHED_S1 or LMS_SCHED_S3 (resolved)
+  int tile = 0;          // T
+  int lag = 0;           // S3 tile lag L
+  int64_t K = 0;         // number of tiles
+  int64_t n_free = 0;
+  int max_reach = 0;     // max over tiles of (khi - k)
+  DBuf<int32_t> item_ptr;   // [K*C + 1] slot offsets, item index = k*C + c
+  DBuf<int32_t> sv;         // [n_free] vertex of each slot
+  DBuf<int32_t> sptr;       // [n_free + 1] row offsets into scol
+  DBuf<int32_t> scol;       // [nnz_free] neighbour ids, CSR order
+  DBuf<int32_t> klo, khi;   // [K] tile dependency range (inclusive)
+  DBuf<int32_t> prog;       // [K] S3 per-tile progress (stages completed)
+  DBuf<unsigned long long> ticket;  // [1] S3 work counter
+  // S1 CUDA graphs: [0] one sweep, [1] eight sweeps (C kernel nodes per sweep)
+  cudaGraphExec_t graphs[2] = {nullptr, nullptr};
+  ~Schedule() {
+    for (auto& g : graphs)
+      if (g) cudaGraphExecDestroy(g);
+  }
+};
+
+}  // namespace lms
+
+struct lms_mesh_s {
+  int dim = 2;
+  int k = 0;              // verts per element (0 = no elements)
+  int64_t V = 0, nnz = 0, n_el = 0, n_free = 0;
+  int32_t C = 0;
+  int device = 0;
+  cudaStream_t s0 = nullptr;   // stream used for allocations
+  lms::DBuf<double> x[3];
+  lms::DBuf<uint8_t> fixed;
+  lms::DBuf<int32_t> row_ptr, col;
+  lms::DBuf<int8_t> colour;
+  lms::DBuf<int32_t> orig_id;
+  lms::DBuf<int32_t> elems;
+  lms::DBuf<double> quality;   // valid if has_quality
+  bool has_quality = false;    // externally supplied (from_csr) or cached
+  bool quality_external = false;
+  int sched_req = LMS_SCHED_AUTO, tile_req = 0, lag_req = 0;
+  lms::Schedule sched;
+  lms::DBuf<int> err;          // device error flag
+};
+
+namespace lms {
+
+// Device-side error flag helpers (error codes are lms_status values).
+__device__ __forceinline__ void raise_err(int* flag, int code) { atomicCAS(flag, 0, code); }
+void check_err_flag(lms_mesh_s* m, cudaStream_t s, const char* what);
+
+inline unsigned grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > (int64_t)1 << 30) g = (int64_t)1 << 30;
+  return (unsigned)g;
+}
+
+// Pipeline pieces (implemented in build.cu, colour.cu, order.cu, permute.cu, smooth.cu)
+void build_csr_from_elems(lms_mesh_s* m, const int32_t* d_elems, bool want_boundary, cudaStream_t s);
+void compute_colouring(lms_mesh_s* m, cudaStream_t s);
+void compute_quality(lms_mesh_s* m, cudaStream_t s);
+void order_random(lms_mesh_s* m, uint64_t seed, int32_t* d_perm, cudaStream_t s);
+void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s);
+void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s);
+void permute_mesh(lms_mesh_s* m, const int32_t* d_perm, cudaStream_t s);
+void build_schedule(lms_mesh_s* m, cudaStream_t s);
+void run_sweeps(lms_mesh_s* m, int sweeps, cudaStream_t s);
+void segmented_sort_rows(int32_t* d_col, const int32_t* d_row_ptr, int64_t V, int64_t nnz, cudaStream_t s);
+int64_t count_free(lms_mesh_s* m, cudaStream_t s);
+void fill_iota(int32_t* p, int64_t n, cudaStream_t s);
+
+}  // namespace lms

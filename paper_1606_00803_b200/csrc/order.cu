@@ -1,0 +1,319 @@
+// order.cu -- the four vertex orderings of the paper, as GPU kernels.
+// perm[new] = old ("V_new[next_num] <- V[i]").
+//
+//  RANDOM:   perm = argsort of H(seed, 4, i), H the SplitMix64 counter
+//                   hash (reading Z15); radix sort of (key, i) pairs.
+//  BFS:   queue BFS from `seed`, neighbours in ascending label, restart
+//                   at the smallest unvisited label (reading Z14).  Level-
+//                   synchronous: each new vertex gets key (rank of its first
+//                   discoverer in the current level, label); sorting a level's
+//                   keys reproduces the queue order exactly.
+//  RDR (Alg. 2): neighbour rows pre-sorted by (quality, label) and
+//                   the free vertices sorted by (quality, label) in parallel;
+//                   the greedy walk itself is inherently sequential and runs in
+//                   ONE warp: each step checks a whole row's `processed` /
+//                   `sorted` flags with one warp load, appends the unsorted
+//                   members of l in order with a ballot prefix, and advances
+//                   to l[0] (readings Z9-Z12).  Never-sorted vertices are
+//                   appended in ascending label.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
+
+#include "lms_internal.cuh"
+
+namespace lms {
+
+__device__ __forceinline__ unsigned long long sm64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_random_keys(unsigned long long base, int64_t V, unsigned long long* keys, int32_t* idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = sm64(base + (unsigned long long)i);
+    idx[i] = (int32_t)i;
+  }
+}
+
+void order_random(lms_mesh_s* m, uint64_t seed, int32_t* d_perm, cudaStream_t s) {
+  const int64_t V = m->V;
+  // H(seed, 4, i) = SM(SM(seed + 4) + i): the inner SM is a host constant
+  unsigned long long z = seed + 4ull;
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  const unsigned long long base = z ^ (z >> 31);
+  DBuf<unsigned long long> keys(V, s), keys2(V, s);
+  DBuf<int32_t> idx(V, s);
+  k_random_keys<<<grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256), 256, 0, s>>>(base, V, keys.p, idx.p);
+  LMS_CHECK_LAUNCH();
+  size_t tb = 0;
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, keys2.p, idx.p, d_perm, V, 0, 64, s));
+  DBuf<char> tmp(tb, s);
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, keys2.p, idx.p, d_perm, V, 0, 64, s));
+}
+
+// ------------------------------------------------------------------------ BFS
+__global__ void k_bfs_init(int64_t V, int32_t* rank, int32_t* minpar) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x) {
+    rank[i] = -1;
+    minpar[i] = 0x7fffffff;
+  }
+}
+
+__global__ void k_bfs_set(int32_t* perm, int32_t* rank, int64_t pos, const int* vtx) {
+  perm[pos] = *vtx;
+  rank[*vtx] = (int32_t)pos;
+}
+
+// expand level perm[head, tail): discover unvisited neighbours, min discoverer rank
+__global__ void k_bfs_expand(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ perm, int64_t head, int64_t tail,
+                             const int32_t* __restrict__ rank, int32_t* minpar, int32_t* cand, int* ncand) {
+  // one warp per level vertex: lanes stride the row
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = head + w; i < tail; i += nw) {
+    const int32_t p = perm[i];
+    for (int32_t j = rp[p] + lane; j < rp[p + 1]; j += 32) {
+      const int32_t u = col[j];
+      if (rank[u] < 0) {
+        int32_t old = atomicMin(&minpar[u], (int32_t)i);
+        if (old == 0x7fffffff) cand[atomicAdd(ncand, 1)] = u;
+      }
+    }
+  }
+}
+
+__global__ void k_bfs_keys(const int32_t* __restrict__ cand, int n, const int32_t* __restrict__ minpar, int b,
+                           unsigned long long* keys) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int32_t u = cand[i];
+    keys[i] = ((unsigned long long)minpar[u] << b) | (unsigned long long)u;
+  }
+}
+
+__global__ void k_bfs_place(const unsigned long long* __restrict__ keys, int n, int b, int64_t tail, int32_t* perm,
+                            int32_t* rank) {
+  const unsigned long long mask = (1ull << b) - 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int32_t u = (int32_t)(keys[i] & mask);
+    perm[tail + i] = u;
+    rank[u] = (int32_t)(tail + i);
+  }
+}
+
+__global__ void k_min_unvisited(const int32_t* __restrict__ rank, int64_t V, int* out) {
+  int best = 0x7fffffff;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
+    if (rank[i] < 0) { best = (int)i; break; }
+  for (int o = 16; o; o >>= 1) best = min(best, __shfl_down_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best != 0x7fffffff) atomicMin(out, best);
+}
+
+static int bits_for2(int64_t n) {
+  int b = 1;
+  while (((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s) {
+  const int64_t V = m->V;
+  const int b = bits_for2(V + 1);
+  DBuf<int32_t> rank(V, s), minpar(V, s), cand(V, s);
+  DBuf<unsigned long long> keys(V, s), keys2(V, s);
+  DBuf<int> dint(2, s);  // [0] = ncand, [1] = vertex scratch
+  const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
+  k_bfs_init<<<Gv, 256, 0, s>>>(V, rank.p, minpar.p);
+  LMS_CHECK_LAUNCH();
+  size_t tb_max = 0;
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb_max, keys.p, keys2.p, (int)V, 0, 2 * b, s));
+  DBuf<char> tmp(tb_max, s);
+  int hseed = (int)seed;
+  LMS_TRY_CUDA(cudaMemcpyAsync(dint.p + 1, &hseed, sizeof(int), cudaMemcpyHostToDevice, s));
+  k_bfs_set<<<1, 1, 0, s>>>(d_perm, rank.p, 0, dint.p + 1);
+  LMS_CHECK_LAUNCH();
+  int64_t head = 0, tail = 1;
+  while (tail < V) {
+    if (head == tail) {  // component exhausted: restart at the smallest unvisited label
+      int big = 0x7fffffff;
+      LMS_TRY_CUDA(cudaMemcpyAsync(dint.p + 1, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+      k_min_unvisited<<<Gv, 256, 0, s>>>(rank.p, V, dint.p + 1);
+      LMS_CHECK_LAUNCH();
+      k_bfs_set<<<1, 1, 0, s>>>(d_perm, rank.p, tail, dint.p + 1);
+      LMS_CHECK_LAUNCH();
+      ++tail;
+      continue;
+    }
+    LMS_TRY_CUDA(cudaMemsetAsync(dint.p, 0, sizeof(int), s));
+    const int64_t nlev = tail - head;
+    unsigned G = grid_for(nlev * 32, 256);
+    if (G > 4096) G = 4096;
+    k_bfs_expand<<<G, 256, 0, s>>>(m->row_ptr.p, m->col.p, d_perm, head, tail, rank.p, minpar.p, cand.p, dint.p);
+    LMS_CHECK_LAUNCH();
+    int n = 0;
+    LMS_TRY_CUDA(cudaMemcpyAsync(&n, dint.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    head = tail;
+    if (n == 0) continue;
+    unsigned Gn = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
+    k_bfs_keys<<<Gn, 256, 0, s>>>(cand.p, n, minpar.p, b, keys.p);
+    LMS_CHECK_LAUNCH();
+    size_t tb = tb_max;
+    LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, keys2.p, n, 0, 2 * b, s));
+    k_bfs_place<<<Gn, 256, 0, s>>>(keys2.p, n, b, tail, d_perm, rank.p);
+    LMS_CHECK_LAUNCH();
+    tail += n;
+  }
+}
+
+// ------------------------------------------------------------------------ RDR
+__global__ void k_row_qkeys(const int32_t* __restrict__ col, int64_t nnz, const double* __restrict__ q,
+                            unsigned long long* keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = (unsigned long long)__double_as_longlong(q[col[i]]);
+}
+
+__global__ void k_free_qkeys(const uint8_t* __restrict__ fixed, const double* __restrict__ q, int64_t V,
+                             unsigned long long* keys, int32_t* ids, int* n) {
+  // compaction keeps ascending id order within a warp only; ids are re-sorted
+  // stably by the (q, id) radix sort below, which needs ascending ids for ties:
+  // so we write (q, id) keys into a V-sized array with sentinel for fixed.
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    ids[v] = (int32_t)v;
+    keys[v] = fixed[v] ? ~0ull : (unsigned long long)__double_as_longlong(q[v]);
+    if (!fixed[v]) atomicAdd(n, 1);
+  }
+}
+
+__global__ void k_rdr_walk(const int32_t* __restrict__ rp, const int32_t* __restrict__ scol,
+                           const int32_t* __restrict__ outer, int64_t n_outer, uint8_t* processed,
+                           uint8_t* sorted, int32_t* perm, long long* stats /* [next, walks] */) {
+  const int lane = threadIdx.x;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  long long next = 0, walks = 0;
+  volatile uint8_t* P = processed;
+  volatile uint8_t* S = sorted;
+  int64_t oi = 0;
+  while (oi < n_outer) {
+    const int64_t idx = oi + lane;
+    const int32_t i_l = idx < n_outer ? outer[idx] : -1;
+    const int p_l = i_l >= 0 ? P[i_l] : 1;
+    const unsigned bal = __ballot_sync(FULL, p_l == 0);
+    if (bal == 0) { oi += 32; continue; }
+    const int first = __ffs(bal) - 1;
+    const int32_t i = __shfl_sync(FULL, i_l, first);
+    oi += first + 1;
+    // Alg. 2 lines: if not sorted[i]: append; processed[i] <- True
+    const int si = S[i];
+    if (lane == 0) {
+      if (!si) { perm[next] = i; S[i] = 1; }
+      P[i] = 1;
+    }
+    next += si ? 0 : 1;
+    ++walks;
+    __syncwarp();
+    int32_t cur = i;
+    for (;;) {
+      const int32_t b = rp[cur], e = rp[cur + 1];
+      int32_t l0 = -1;
+      for (int32_t base = b; base < e; base += 32) {
+        const int32_t j = base + lane;
+        const int32_t u = j < e ? scol[j] : -1;
+        const int pu = u >= 0 ? P[u] : 1;
+        const int su = u >= 0 ? S[u] : 1;
+        const unsigned unp = __ballot_sync(FULL, pu == 0);
+        if (unp && l0 < 0) l0 = __shfl_sync(FULL, u, __ffs(unp) - 1);
+        const unsigned app = __ballot_sync(FULL, pu == 0 && su == 0);
+        if (pu == 0 && su == 0) {
+          perm[next + __popc(app & lt)] = u;
+          S[u] = 1;
+        }
+        next += __popc(app);
+      }
+      __syncwarp();
+      if (l0 < 0) break;
+      if (lane == 0) P[l0] = 1;
+      __syncwarp();
+      cur = l0;
+    }
+  }
+  if (lane == 0) { stats[0] = next; stats[1] = walks; }
+}
+
+__global__ void k_unsorted_flags(const uint8_t* __restrict__ sorted, int64_t V, uint8_t* flags, int32_t* ids) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    flags[v] = sorted[v] ? 0 : 1;
+    ids[v] = (int32_t)v;
+  }
+}
+
+void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s) {
+  const int64_t V = m->V, nnz = m->nnz;
+  compute_quality(m, s);
+  const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
+  // rows presorted by (q, label): stable segmented sort of (q bits, col) pairs
+  DBuf<int32_t> scol(nnz, s);
+  {
+    DBuf<unsigned long long> k1(nnz, s), k2(nnz, s);
+    const unsigned Gn = grid_for(nnz, 256) > 8192 ? 8192 : grid_for(nnz, 256);
+    k_row_qkeys<<<Gn, 256, 0, s>>>(m->col.p, nnz, m->quality.p, k1.p);
+    LMS_CHECK_LAUNCH();
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, k1.p, k2.p, m->col.p, scol.p, nnz, V,
+                                                           m->row_ptr.p, m->row_ptr.p + 1, s));
+    DBuf<char> tmp(tb, s);
+    LMS_TRY_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp.p, tb, k1.p, k2.p, m->col.p, scol.p, nnz, V,
+                                                           m->row_ptr.p, m->row_ptr.p + 1, s));
+  }
+  // outer list: free vertices by (q, label); fixed get key ~0 and sort last
+  DBuf<int32_t> outer(V, s);
+  int64_t n_outer = 0;
+  {
+    DBuf<unsigned long long> k1(V, s), k2(V, s);
+    DBuf<int32_t> ids(V, s);
+    DBuf<int> n(1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(n.p, 0, sizeof(int), s));
+    k_free_qkeys<<<Gv, 256, 0, s>>>(m->fixed.p, m->quality.p, V, k1.p, ids.p, n.p);
+    LMS_CHECK_LAUNCH();
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, ids.p, outer.p, V, 0, 64, s));
+    DBuf<char> tmp(tb, s);
+    LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k1.p, k2.p, ids.p, outer.p, V, 0, 64, s));
+    int hn = 0;
+    LMS_TRY_CUDA(cudaMemcpyAsync(&hn, n.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    n_outer = hn;
+  }
+  DBuf<uint8_t> processed(V, s), sorted(V, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(processed.p, 0, V, s));
+  LMS_TRY_CUDA(cudaMemsetAsync(sorted.p, 0, V, s));
+  DBuf<long long> stats(2, s);
+  k_rdr_walk<<<1, 32, 0, s>>>(m->row_ptr.p, scol.p, outer.p, n_outer, processed.p, sorted.p, d_perm, stats.p);
+  LMS_CHECK_LAUNCH();
+  long long hs[2] = {0, 0};
+  LMS_TRY_CUDA(cudaMemcpyAsync(hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  if (hs[0] < V) {  // tail: never-sorted vertices in ascending label (reading Z12)
+    DBuf<uint8_t> flags(V, s);
+    DBuf<int32_t> ids(V, s);
+    DBuf<int> nsel(1, s);
+    k_unsorted_flags<<<Gv, 256, 0, s>>>(sorted.p, V, flags.p, ids.p);
+    LMS_CHECK_LAUNCH();
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids.p, flags.p, d_perm + hs[0], nsel.p, V, s));
+    DBuf<char> tmp(tb, s);
+    LMS_TRY_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, ids.p, flags.p, d_perm + hs[0], nsel.p, V, s));
+    int hn = 0;
+    LMS_TRY_CUDA(cudaMemcpyAsync(&hn, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    if (hs[0] + hn != V) fail(LMS_E_CUDA, "RDR did not order every vertex exactly once");
+  }
+}
+
+}  // namespace lms

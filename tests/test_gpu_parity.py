@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star):
+  * CSR, fixed mask, colouring, permutations, orig_id, elements: bit-exact;
+  * coordinates: bit-exact on the same ordering (CSR-order sums, IEEE division,
+    no FMA on either side); across orderings max-abs <= 1e-12 * bbox diagonal.
+Sizes span many tiles and a ragged tail; BASELINE.json's C2 (1024^2, 100
+sweeps) and C3 run at full size; C4 (the bench workload, S3 launch config) runs
+at full size for a few sweeps.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import meshgen
+import oracle
+from conftest import csr_from_rows
+from gpu_helpers import bits_equal, cuda, gpu_coords, gpu_csr, gpu_mesh, np_
+
+pytestmark = pytest.mark.gpu
+
+lms = pytest.importorskip("paper_1606_00803_b200")
+
+SMALL = [
+    ("grid3x3", lambda: meshgen.grid2d(3, 3, 0.0)),
+    ("grid33x31_1023", lambda: meshgen.grid2d(33, 31, 0.3, seed=1)),      # V = 2^10 - 1
+    ("grid41x25_1025", lambda: meshgen.grid2d(41, 25, 0.3, seed=2)),      # V = 2^10 + 1
+    ("grid100_C1", lambda: meshgen.make_config("C1")),
+    ("grid37x53_unjit", lambda: meshgen.grid2d(37, 53, 0.0, seed=3)),     # quality ties
+    ("kuhn7", lambda: meshgen.kuhn3d(7, 0.25, seed=4)),
+    ("kuhn12", lambda: meshgen.kuhn3d(12, 0.25, seed=5)),
+    ("graded", lambda: meshgen.grid2d(64, 32, 0.3, seed=6, warp_x2=True)),
+]
+
+
+@pytest.fixture(scope="module", params=SMALL, ids=[s[0] for s in SMALL])
+def pair(request):
+    m = request.param[1]()
+    om = oracle.prepare(m)
+    om["fixed"] = oracle.boundary(m.V, m["elems"])
+    gm = gpu_mesh(m)
+    yield m, om, gm
+    gm.close()
+
+
+def test_csr_fixed_colour_bit_exact(pair):
+    m, om, gm = pair
+    rp, col = gpu_csr(gm)
+    assert np.array_equal(rp, om["row_ptr"]) and np.array_equal(col, om["col"])
+    assert np.array_equal(np_(gm.fixed()), om["fixed"])
+    assert np.array_equal(np_(gm.colour()), om["colour"])
+    assert gm.info()["C"] == om["C"]
+    assert np.array_equal(np_(gm.orig_id()), np.arange(m.V))
+
+
+def test_quality_bit_exact(pair):
+    m, om, gm = pair
+    q = oracle.quality(m["coords"], m["elems"])
+    assert bits_equal([np_(gm.quality())], [q])
+
+
+@pytest.mark.parametrize("kind", ["original", "random", "bfs", "rdr"])
+def test_orderings_bit_exact(pair, kind):
+    m, om, gm = pair
+    seed = 803 if kind == "random" else 0
+    p = np_(gm.order(kind, seed))
+    assert np.array_equal(p, oracle.order(om, kind, seed))
+
+
+def test_bfs_other_seed(pair):
+    m, om, gm = pair
+    s = m.V // 2
+    assert np.array_equal(np_(gm.order("bfs", s)), oracle.order_bfs(om["row_ptr"], om["col"], s))
+
+
+@pytest.mark.parametrize("sched", [("s1", 0), ("s3", 0), ("s3", 64), ("s3", 96)])
+def test_sweeps_bit_exact_all_orderings(pair, sched):
+    m, om, gm0 = pair
+    for kind in ["original", "random", "bfs", "rdr"]:
+        seed = 803 if kind == "random" else 0
+        perm = oracle.order(om, kind, seed)
+        pm = oracle.permute_mesh(om, perm)
+        want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 7)
+        with gpu_mesh(m) as gm:
+            gm.permute(cuda(perm))
+            gm.set_schedule(sched[0], tile=sched[1])
+            gm.smooth(3)
+            gm.smooth(4)
+            got = gpu_coords(gm)
+            assert bits_equal(got, want), (kind, sched, gm.schedule_info())
+            # the relabelled mesh itself is bit-exact too
+            rp, col = gpu_csr(gm)
+            assert np.array_equal(rp, pm["row_ptr"]) and np.array_equal(col, pm["col"])
+            assert np.array_equal(np_(gm.colour()), pm["colour"])
+            assert np.array_equal(np_(gm.orig_id()), pm["orig_id"])
+
+
+def test_cross_ordering_tolerance(pair):
+    m, om, gm = pair
+    X = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 10)
+    diag = math.sqrt(len(X))
+    for kind in ["random", "rdr"]:
+        with gpu_mesh(m) as gm2:
+            perm = gm2.order(kind, 803)
+            gm2.permute(perm)
+            gm2.smooth(10)
+            got = gpu_coords(gm2)
+            p = np_(perm)
+            for a in range(len(X)):
+                assert np.abs(got[a] - X[a][p]).max() <= 1e-12 * diag
+
+
+def test_w1_from_csr():
+    import json, os
+    w1 = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "w1.json")))
+    rp, col = csr_from_rows(w1["rows"])
+    V = w1["n_vertices"]
+    fixed = np.array([0 if v in w1["free"] else 1 for v in range(V)], dtype=np.uint8)
+    x0 = np.array(w1["x0"], dtype=np.float64)
+    y0 = -2.0 * x0
+    q = np.array(w1["quality"])
+    gm = lms.Mesh.from_csr([cuda(x0), cuda(y0)], cuda(fixed), cuda(rp.astype(np.int32)), cuda(col),
+                           quality=cuda(q))
+    assert np_(gm.colour()).tolist() == w1["colour"]
+    assert np_(gm.order("rdr")).tolist() == w1["rdr_perm"]
+    assert np_(gm.order("bfs", 0)).tolist() == w1["bfs_perm_from_0"]
+    from fractions import Fraction
+    gm.smooth(1)
+    x = np_(gm.coords()[0])
+    want1 = oracle.smooth([x0], rp, col, oracle.colour(rp, col, fixed)[0], 2, 1)[0]
+    assert bits_equal([x], [want1])
+    assert abs(x[0] - float(Fraction(23, 3))) < 1e-15 and x[2] == 9.0
+    gm.smooth(1)
+    x = np_(gm.coords()[0])
+    want2 = oracle.smooth([x0], rp, col, oracle.colour(rp, col, fixed)[0], 2, 2)[0]
+    assert bits_equal([x], [want2])
+    gm.close()
+
+
+def test_fixed_mask_supplied_wins():
+    m = meshgen.grid2d(20, 20, 0.3, seed=9)
+    fx = m["fixed"].copy()
+    fx[45] = 1                                    # an interior vertex pinned by the caller
+    m2 = dict(m); m2["fixed"] = fx
+    gm = gpu_mesh(m2, use_fixed=True)
+    assert np.array_equal(np_(gm.fixed()), fx)
+    om = oracle.prepare(m2)
+    assert np.array_equal(np_(gm.colour()), om["colour"])
+    gm.smooth(5)
+    want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 5)
+    assert bits_equal(gpu_coords(gm), want)
+    gm.close()
+
+
+# ------------------------------------------------------------------ error paths (T5)
+def _expect(status, fn, *a, **k):
+    with pytest.raises(lms.LMSError) as e:
+        fn(*a, **k)
+    assert e.value.name == status, str(e.value)
+
+
+def test_errors():
+    x = cuda(np.array([0.0, 1.0, 0.0, 1.0])); y = cuda(np.array([0.0, 0.0, 1.0, 1.0]))
+    _expect("LMS_E_INDEX", lms.Mesh.build_csr, [x, y], cuda(np.array([[0, 1, 4]], dtype=np.int32)))
+    _expect("LMS_E_INDEX", lms.Mesh.build_csr, [x, y], cuda(np.array([[0, 1, 1]], dtype=np.int32)))
+    _expect("LMS_E_ISOLATED", lms.Mesh.build_csr, [x, y], cuda(np.array([[0, 1, 2]], dtype=np.int32)))
+    m = meshgen.grid2d(6, 5, 0.3)
+    gm = gpu_mesh(m)
+    before = gpu_coords(gm)
+    rp0, col0 = gpu_csr(gm)
+    bad = np.arange(m.V, dtype=np.int32); bad[3] = 4
+    _expect("LMS_E_PERM", gm.permute, cuda(bad))
+    bad2 = np.arange(m.V, dtype=np.int32); bad2[0] = m.V
+    _expect("LMS_E_PERM", gm.permute, cuda(bad2))
+    rp1, col1 = gpu_csr(gm)                         # handle unchanged on error
+    assert np.array_equal(rp0, rp1) and np.array_equal(col0, col1) and bits_equal(before, gpu_coords(gm))
+    _expect("LMS_E_ARG", gm.order, "bfs", m.V)
+    _expect("LMS_E_ARG", gm.smooth, -1)
+    gm.smooth(0)
+    assert bits_equal(before, gpu_coords(gm))
+    gm.close()
+    # degenerate element -> RDR quality fails
+    z = cuda(np.zeros(4))
+    gd = lms.Mesh.build_csr([z, z.clone()], cuda(np.array([[0, 1, 2], [1, 2, 3]], dtype=np.int32)))
+    _expect("LMS_E_DEGENERATE", gd.order, "rdr")
+    gd.close()
+    # RDR on a CSR-built handle without quality
+    rp, col = csr_from_rows([[1], [0]])
+    gc = lms.Mesh.from_csr([cuda(np.zeros(2)), cuda(np.zeros(2))], cuda(np.array([0, 1], dtype=np.uint8)),
+                           cuda(rp.astype(np.int32)), cuda(col))
+    _expect("LMS_E_STATE", gc.order, "rdr")
+    gc.close()
+
+
+# ------------------------------------------------------------------ full-size configs
+def test_C2_full_all_orderings_100_sweeps():
+    """BASELINE.json configs[1]: 1024^2, 100 sweeps, each ordering, bit-exact."""
+    m = meshgen.make_config("C2")
+    om = oracle.prepare(m)
+    base = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 100)
+    for kind in ["original", "bfs", "random", "rdr"]:
+        gm = gpu_mesh(m)
+        perm_g = gm.order(kind, 803)
+        perm = oracle.order(om, kind, 803)
+        assert np.array_equal(np_(perm_g), perm), kind
+        gm.permute(perm_g)
+        gm.smooth(100)
+        got = gpu_coords(gm)
+        pm = oracle.permute_mesh(om, perm)
+        want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 100)
+        assert bits_equal(got, want), (kind, gm.schedule_info())
+        for a in range(2):
+            assert np.abs(got[a] - base[a][perm]).max() <= 1e-12 * math.sqrt(2)
+        gm.close()
+
+
+def test_C3_full_bfs_rdr():
+    """BASELINE.json configs[2]: 3D Kuhn 128^3 (BFS vs RDR); 10 sweeps bit-exact."""
+    m = meshgen.make_config("C3")
+    om = oracle.prepare(m)
+    gm0 = gpu_mesh(m)
+    rp, col = gpu_csr(gm0)
+    assert np.array_equal(rp, om["row_ptr"]) and np.array_equal(col, om["col"])
+    assert np.array_equal(np_(gm0.fixed()), m["fixed"]) and gm0.info()["C"] == om["C"]
+    gm0.close()
+    for kind in ["bfs", "rdr"]:
+        gm = gpu_mesh(m)
+        perm = oracle.order(om, kind, 0)
+        assert np.array_equal(np_(gm.order(kind)), perm), kind
+        gm.permute(cuda(perm))
+        gm.smooth(10)
+        pm = oracle.permute_mesh(om, perm)
+        want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 10)
+        assert bits_equal(gpu_coords(gm), want), (kind, gm.schedule_info())
+        gm.close()
+
+
+def test_C4_full_bench_config():
+    """BASELINE.json configs[3] (the bench workload), original ordering, the
+    launch configuration bench.py times (AUTO -> S3), 3 sweeps bit-exact."""
+    m = meshgen.make_config("C4")
+    om = oracle.prepare(m)
+    gm = gpu_mesh(m)
+    rp, col = gpu_csr(gm)
+    assert np.array_equal(rp, om["row_ptr"]) and np.array_equal(col, om["col"])
+    assert np.array_equal(np_(gm.colour()), om["colour"])
+    gm.smooth(3)
+    want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 3)
+    assert bits_equal(gpu_coords(gm), want), gm.schedule_info()
+    gm.close()
