@@ -143,6 +143,17 @@ lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream);
  * lms_smooth (the internal schedule is rebuilt lazily). */
 lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, int32_t lag);
 
+typedef enum {
+    LMS_TILING_AUTO = 0,    /* S3: SPATIAL, S1: STORAGE */
+    LMS_TILING_STORAGE = 1, /* tile = T consecutive storage positions (processing follows the ordering) */
+    LMS_TILING_SPATIAL = 2  /* tile = cell of a regular grid over the initial coordinates (~T vertices) */
+} lms_tiling_kind;
+
+/* lms_set_tiling -- how the schedule groups free vertices into work items.
+ * A scheduling choice only: every tiling replays the same colour schedule, so
+ * lms_smooth's result is bit-identical for all of them. */
+lms_status lms_set_tiling(lms_mesh_t m, lms_tiling_kind kind);
+
 /* ---------------------------------------------------------------------------
  * Accessors.  Outputs are caller-owned device buffers of the stated sizes.   */
 lms_status lms_mesh_info(lms_mesh_t m, int64_t* n_vertices, int64_t* nnz, int32_t* n_colours,
@@ -151,6 +162,9 @@ lms_status lms_mesh_info(lms_mesh_t m, int64_t* n_vertices, int64_t* nnz, int32_
  * uses (resolved AUTO); tile/lag: its parameters (0 before the first smooth). */
 lms_status lms_schedule_info(lms_mesh_t m, int64_t* n_free, int32_t* sched_kind, int32_t* tile,
                              int32_t* lag);
+/* tiling: resolved lms_tiling_kind; n_tiles: tiles K; max_reach: max |k' - k| over
+ * dependent tiles (S3 needs lag > max_reach) -- all 0 before the first smooth. */
+lms_status lms_schedule_info2(lms_mesh_t m, int32_t* tiling, int64_t* n_tiles, int32_t* max_reach);
 lms_status lms_export_coords(lms_mesh_t m, double* const* d_out, lms_stream_t stream);
 lms_status lms_import_coords(lms_mesh_t m, const double* const* d_in, lms_stream_t stream);
 lms_status lms_export_csr(lms_mesh_t m, int32_t* d_row_ptr, int32_t* d_col_idx, lms_stream_t stream);

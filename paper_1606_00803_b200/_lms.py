@@ -17,6 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 ORDERINGS = {"original": 0, "random": 1, "bfs": 2, "rdr": 3}
 SCHEDULES = {"auto": 0, "s1": 1, "s3": 3}
 SCHED_NAMES = {v: k for k, v in SCHEDULES.items()}
+TILINGS = {"auto": 0, "storage": 1, "spatial": 2}
+TILING_NAMES = {v: k for k, v in TILINGS.items()}
 
 LMS_STATUS = {0: "LMS_OK", -1: "LMS_E_ARG", -2: "LMS_E_INDEX", -3: "LMS_E_ISOLATED", -4: "LMS_E_PERM",
               -5: "LMS_E_DEGENERATE", -6: "LMS_E_NOMEM", -7: "LMS_E_CUDA", -8: "LMS_E_NCCL", -9: "LMS_E_STATE"}
@@ -25,7 +27,7 @@ LMS_STATUS = {0: "LMS_OK", -1: "LMS_E_ARG", -2: "LMS_E_INDEX", -3: "LMS_E_ISOLAT
 EXPORTS = ["lms_build_csr", "lms_mesh_from_csr", "lms_mesh_destroy", "lms_order", "lms_permute", "lms_smooth",
            "lms_set_schedule", "lms_mesh_info", "lms_schedule_info", "lms_export_coords", "lms_import_coords",
            "lms_export_csr", "lms_export_colour", "lms_export_fixed", "lms_export_orig_id", "lms_export_elems",
-           "lms_export_quality", "lms_last_error", "lms_kernel_launches"]
+           "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_set_tiling", "lms_schedule_info2"]
 
 
 class LMSError(RuntimeError):
@@ -67,6 +69,8 @@ def load_library(build: bool = True):
         "lms_export_orig_id": [P, P, P],
         "lms_export_elems": [P, P, P],
         "lms_export_quality": [P, P, P],
+        "lms_set_tiling": [P, i32],
+        "lms_schedule_info2": [P, ct.POINTER(i32), ct.POINTER(i64), ct.POINTER(i32)],
         "lms_last_error": [],
         "lms_kernel_launches": [],
     }
@@ -186,7 +190,10 @@ class Mesh:
         nf, kind, tile, lag = ct.c_int64(), ct.c_int32(), ct.c_int32(), ct.c_int32()
         _check(lib().lms_schedule_info(self._h, ct.byref(nf), ct.byref(kind), ct.byref(tile), ct.byref(lag)),
                "lms_schedule_info")
-        return dict(n_free=nf.value, kind=SCHED_NAMES.get(kind.value, kind.value), tile=tile.value, lag=lag.value)
+        tl, nt, mr = ct.c_int32(), ct.c_int64(), ct.c_int32()
+        _check(lib().lms_schedule_info2(self._h, ct.byref(tl), ct.byref(nt), ct.byref(mr)), "lms_schedule_info2")
+        return dict(n_free=nf.value, kind=SCHED_NAMES.get(kind.value, kind.value), tile=tile.value, lag=lag.value,
+                    tiling=TILING_NAMES.get(tl.value, tl.value), n_tiles=nt.value, max_reach=mr.value)
 
     @property
     def V(self):
@@ -211,8 +218,10 @@ class Mesh:
     def smooth(self, sweeps: int, stream=None):
         _check(lib().lms_smooth(self._h, sweeps, _stream(stream)), "lms_smooth")
 
-    def set_schedule(self, kind: str = "auto", tile: int = 0, lag: int = 0):
+    def set_schedule(self, kind: str = "auto", tile: int = 0, lag: int = 0, tiling: str | None = None):
         _check(lib().lms_set_schedule(self._h, SCHEDULES[kind], tile, lag), "lms_set_schedule")
+        if tiling is not None:
+            _check(lib().lms_set_tiling(self._h, TILINGS[tiling]), "lms_set_tiling")
 
     # ------------------------------------------------------------ export / import
     def coords(self, stream=None):

@@ -250,6 +250,27 @@ lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, 
   LMS_API_END
 }
 
+lms_status lms_set_tiling(lms_mesh_t m, lms_tiling_kind kind) {
+  LMS_API_BEGIN
+  if (!m) fail(LMS_E_ARG, "NULL handle");
+  if (kind != LMS_TILING_AUTO && kind != LMS_TILING_STORAGE && kind != LMS_TILING_SPATIAL)
+    fail(LMS_E_ARG, "unknown tiling");
+  m->tiling_req = kind;
+  m->sched.valid = false;
+  return LMS_OK;
+  LMS_API_END
+}
+
+lms_status lms_schedule_info2(lms_mesh_t m, int32_t* tiling, int64_t* n_tiles, int32_t* max_reach) {
+  LMS_API_BEGIN
+  if (!m) fail(LMS_E_ARG, "NULL handle");
+  if (tiling) *tiling = m->sched.valid ? m->sched.tiling : 0;
+  if (n_tiles) *n_tiles = m->sched.valid ? m->sched.K : 0;
+  if (max_reach) *max_reach = m->sched.valid ? m->sched.max_reach : 0;
+  return LMS_OK;
+  LMS_API_END
+}
+
 lms_status lms_mesh_info(lms_mesh_t m, int64_t* V, int64_t* nnz, int32_t* n_colours, int32_t* dim) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");

@@ -84,6 +84,7 @@ struct Schedule {
   int kind = 0;          // LMS_SCHED_S1 or LMS_SCHED_S3 (resolved)
   int tile = 0;          // T
   int lag = 0;           // S3 tile lag L
+  int tiling = 0;        // LMS_TILING_STORAGE or LMS_TILING_SPATIAL (resolved)
   int64_t K = 0;         // number of tiles
   int64_t n_free = 0;
   int max_reach = 0;     // max over tiles of (khi - k)
@@ -92,7 +93,14 @@ struct Schedule {
   DBuf<int32_t> sptr;       // [n_free + 1] row offsets into scol
   DBuf<int32_t> scol;       // [nnz_free] neighbour ids, CSR order
   DBuf<int32_t> klo, khi;   // [K] tile dependency range (inclusive)
-  DBuf<int32_t> prog;       // [K] S3 per-tile progress (stages completed)
+  DBuf<int32_t> tdep_ptr;   // [K+1] per-tile neighbour-tile lists (CSR, self excluded)
+  DBuf<int32_t> tdep;
+  DBuf<int32_t> prog;       // [K] S3 per-tile completed-chunk counters
+  DBuf<int32_t> tpre;       // [K*(C+1)] S3 per-tile chunk prefix over colours
+  DBuf<int32_t> iw;         // [K*C] S3 slab width (max row length) of each item
+  DBuf<long long> ioff;     // [K*C+1] S3 slab offset (ints) of each item
+  DBuf<int32_t> slab;       // S3 slab: per chunk 32 vertex ids + W x 32 neighbour ids
+  DBuf<int32_t> irec;       // [K*C*32] S3 128-byte item records (see smooth.cu)
   DBuf<unsigned long long> ticket;  // [1] S3 work counter
   // S1 CUDA graphs: [0] one sweep, [1] eight sweeps (C kernel nodes per sweep)
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
@@ -120,7 +128,7 @@ struct lms_mesh_s {
   lms::DBuf<double> quality;   // valid if has_quality
   bool has_quality = false;    // externally supplied (from_csr) or cached
   bool quality_external = false;
-  int sched_req = LMS_SCHED_AUTO, tile_req = 0, lag_req = 0;
+  int sched_req = LMS_SCHED_AUTO, tile_req = 0, lag_req = 0, tiling_req = LMS_TILING_AUTO;
   lms::Schedule sched;
   lms::DBuf<int> err;          // device error flag
 };

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "lms.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(lms_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(lms_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_the_four_calls():
@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     from paper_1606_00803_b200 import _lms, build_lib
     path = build_lib.build()
     out = subprocess.check_output(["nm", "-D", "--defined-only", path]).decode()
-    exported = set(re.findall(r"\bT (lms_[a-z_]+)\b", out))
+    exported = set(re.findall(r"\bT (lms_[a-z0-9_]+)\b", out))
     missing = [s for s in declared_symbols() if s not in exported]
     assert not missing, missing
     assert sorted(_lms.EXPORTS) == declared_symbols()
