@@ -177,6 +177,19 @@ lms_status lms_export_elems(lms_mesh_t m, int32_t* d_elems, lms_stream_t stream)
  * elements), computed from the current coordinates (A4). */
 lms_status lms_export_quality(lms_mesh_t m, double* d_quality, lms_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Multi-GPU building blocks (driven by paper_1606_00803_b200/dist.py
+ * with NCCL over NVLink between the pack and the unpack).
+ *  lms_smooth_colour: one colour stage of the sweep (every free vertex of colour
+ *    `colour` moves, Eq. 1) -- a sweep is the stages 0..C-1 in order.
+ *  lms_gather_coords: d_out[a*n + i] = x_a[d_idx[i]] (halo pack), d_out double[dim*n].
+ *  lms_scatter_coords: x_a[d_idx[i]] = d_in[a*n + i] (halo unpack).
+ *  d_idx int32[n] local vertex ids (not validated). */
+lms_status lms_smooth_colour(lms_mesh_t m, int32_t colour, lms_stream_t stream);
+lms_status lms_gather_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, double* d_out, lms_stream_t stream);
+lms_status lms_scatter_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, const double* d_in,
+                              lms_stream_t stream);
+
 /* Thread-local message for the last non-OK status of this thread. */
 const char* lms_last_error(void);
 /* Number of CUDA kernels this library launched on this thread since load

@@ -27,7 +27,8 @@ LMS_STATUS = {0: "LMS_OK", -1: "LMS_E_ARG", -2: "LMS_E_INDEX", -3: "LMS_E_ISOLAT
 EXPORTS = ["lms_build_csr", "lms_mesh_from_csr", "lms_mesh_destroy", "lms_order", "lms_permute", "lms_smooth",
            "lms_set_schedule", "lms_mesh_info", "lms_schedule_info", "lms_export_coords", "lms_import_coords",
            "lms_export_csr", "lms_export_colour", "lms_export_fixed", "lms_export_orig_id", "lms_export_elems",
-           "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_set_tiling", "lms_schedule_info2"]
+           "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_set_tiling", "lms_schedule_info2",
+           "lms_smooth_colour", "lms_gather_coords", "lms_scatter_coords"]
 
 
 class LMSError(RuntimeError):
@@ -71,6 +72,9 @@ def load_library(build: bool = True):
         "lms_export_quality": [P, P, P],
         "lms_set_tiling": [P, i32],
         "lms_schedule_info2": [P, ct.POINTER(i32), ct.POINTER(i64), ct.POINTER(i32)],
+        "lms_smooth_colour": [P, i32, P],
+        "lms_gather_coords": [P, P, i64, P, P],
+        "lms_scatter_coords": [P, P, i64, P, P],
         "lms_last_error": [],
         "lms_kernel_launches": [],
     }
@@ -217,6 +221,22 @@ class Mesh:
 
     def smooth(self, sweeps: int, stream=None):
         _check(lib().lms_smooth(self._h, sweeps, _stream(stream)), "lms_smooth")
+
+    def smooth_colour(self, colour: int, stream=None):
+        """lms_smooth_colour: one colour stage of the sweep."""
+        _check(lib().lms_smooth_colour(self._h, colour, _stream(stream)), "lms_smooth_colour")
+
+    def gather_coords(self, idx: torch.Tensor, out: torch.Tensor, stream=None):
+        """lms_gather_coords: out[a*n + i] = x_a[idx[i]] (halo pack)."""
+        n = idx.numel()
+        _check(lib().lms_gather_coords(self._h, _dev(idx, torch.int32, name="idx"), n,
+                                       _dev(out, torch.float64, name="out"), _stream(stream)), "lms_gather_coords")
+
+    def scatter_coords(self, idx: torch.Tensor, src: torch.Tensor, stream=None):
+        """lms_scatter_coords: x_a[idx[i]] = src[a*n + i] (halo unpack)."""
+        n = idx.numel()
+        _check(lib().lms_scatter_coords(self._h, _dev(idx, torch.int32, name="idx"), n,
+                                        _dev(src, torch.float64, name="src"), _stream(stream)), "lms_scatter_coords")
 
     def set_schedule(self, kind: str = "auto", tile: int = 0, lag: int = 0, tiling: str | None = None):
         _check(lib().lms_set_schedule(self._h, SCHEDULES[kind], tile, lag), "lms_set_schedule")

@@ -1,0 +1,84 @@
+// halo.cu -- building blocks of the multi-GPU sweep:
+// one colour stage of the schedule, and gather/scatter of coordinates by an
+// index list (halo pack / unpack).  The exchange itself runs over NCCL
+// (torch.distributed) between the pack and the unpack.
+#include "lms_internal.cuh"
+
+namespace lms {
+
+void run_colour_stage(lms_mesh_s* m, int c, cudaStream_t s);  // smooth.cu
+
+__global__ void k_gather_coords(const double* __restrict__ x, const double* __restrict__ y,
+                                const double* __restrict__ z, const int32_t* __restrict__ idx, int64_t n,
+                                double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = idx[i];
+    out[i] = x[v];
+    out[n + i] = y[v];
+    if (z) out[2 * n + i] = z[v];
+  }
+}
+
+__global__ void k_scatter_coords(double* __restrict__ x, double* __restrict__ y, double* __restrict__ z,
+                                 const int32_t* __restrict__ idx, int64_t n, const double* __restrict__ in) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = idx[i];
+    x[v] = in[i];
+    y[v] = in[n + i];
+    if (z) z[v] = in[2 * n + i];
+  }
+}
+
+}  // namespace lms
+
+using namespace lms;
+
+extern "C" {
+
+lms_status lms_smooth_colour(lms_mesh_t m, int32_t colour, lms_stream_t stream) {
+  try {
+    if (!m) fail(LMS_E_ARG, "NULL handle");
+    if (colour < 0 || colour >= m->C) fail(LMS_E_ARG, "colour out of range");
+    if (m->n_free == 0) return LMS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!m->sched.valid) build_schedule(m, s);
+    run_colour_stage(m, colour, s);
+    return LMS_OK;
+  } catch (const Err& e) {
+    set_error(e.msg);
+    return e.st;
+  }
+}
+
+lms_status lms_gather_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, double* d_out, lms_stream_t stream) {
+  try {
+    if (!m || (n > 0 && (!d_idx || !d_out)) || n < 0) fail(LMS_E_ARG, "bad argument");
+    if (n == 0) return LMS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    k_gather_coords<<<grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256), 256, 0, s>>>(
+        m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_out);
+    LMS_CHECK_LAUNCH();
+    return LMS_OK;
+  } catch (const Err& e) {
+    set_error(e.msg);
+    return e.st;
+  }
+}
+
+lms_status lms_scatter_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, const double* d_in,
+                              lms_stream_t stream) {
+  try {
+    if (!m || (n > 0 && (!d_idx || !d_in)) || n < 0) fail(LMS_E_ARG, "bad argument");
+    if (n == 0) return LMS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    k_scatter_coords<<<grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256), 256, 0, s>>>(
+        m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_in);
+    LMS_CHECK_LAUNCH();
+    return LMS_OK;
+  } catch (const Err& e) {
+    set_error(e.msg);
+    return e.st;
+  }
+}
+
+}  // extern "C"

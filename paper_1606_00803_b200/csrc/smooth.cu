@@ -1353,6 +1353,17 @@ static cudaGraphExec_t get_graph(lms_mesh_s* m, int which) {
   return ge;
 }
 
+// one colour stage with the S1 kernel (used by the multi-GPU sweep, which
+// exchanges halos between stages)
+void run_colour_stage(lms_mesh_s* m, int c, cudaStream_t s) {
+  const unsigned G = (unsigned)(m->sched.K < 65535 * 16 ? m->sched.K : 65535 * 16);
+  if (m->dim == 2)
+    launch_s1_t<2, OPT_DEFAULT>(m, s, c, G);
+  else
+    launch_s1_t<3, OPT_DEFAULT>(m, s, c, G);
+  LMS_CHECK_LAUNCH();
+}
+
 void run_sweeps(lms_mesh_s* m, int sweeps, cudaStream_t s) {
   Schedule& S = m->sched;
   if (S.kind == LMS_SCHED_S1) {
