@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--config", default="C4")
     p.add_argument("--ordering", default="original")
     p.add_argument("--sweeps", type=int, default=0, help="0 = the config's sweep count")
-    p.add_argument("--schedule", default="auto", choices=["auto", "s1", "s3"])
+    p.add_argument("--schedule", default="auto", choices=["auto", "s1", "s3", "gz"])
     p.add_argument("--tile", type=int, default=0)
     p.add_argument("--lag", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")

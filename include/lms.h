@@ -60,9 +60,14 @@ typedef enum {
 } lms_order_kind;
 
 typedef enum {
-    LMS_SCHED_AUTO = 0,     /* pick per mesh: S3 when the ordering is banded, else S1 */
+    LMS_SCHED_AUTO = 0,     /* pick per mesh: GZ for 2D meshes with <= 6 colours, else S3 when the
+                               ordering is banded, else S1 */
     LMS_SCHED_S1 = 1,       /* one launch per colour (CUDA-graph captured sweep) */
-    LMS_SCHED_S3 = 3        /* persistent colour-pipelined sweep with per-tile progress flags */
+    LMS_SCHED_S3 = 3,       /* persistent colour-pipelined sweep with per-tile progress flags */
+    LMS_SCHED_GZ = 4        /* ghost-zone tiled sweep: one launch per P sweeps; each CTA stages a
+                               spatial tile plus every vertex within C*P hops in shared memory,
+                               runs the P sweeps' colour stages there and writes its owned vertices
+                               to a second coordinate buffer (no inter-CTA synchronisation) */
 } lms_schedule_kind;
 
 /* ---------------------------------------------------------------------------
@@ -139,8 +144,11 @@ lms_status lms_permute(lms_mesh_t m, const int32_t* d_perm, lms_stream_t stream)
 lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream);
 
 /* lms_set_schedule -- choose the sweep kernel.  tile: vertices per tile
- * (0 = default); lag: S3 tile lag L (0 = automatic).  Takes effect at the next
- * lms_smooth (the internal schedule is rebuilt lazily). */
+ * (0 = default); lag: S3 tile lag L (0 = automatic); for LMS_SCHED_GZ `lag` is
+ * the number of sweeps P fused into one pass (0 = 1; at most 8).  Takes effect
+ * at the next lms_smooth (the internal schedule is rebuilt lazily).  GZ
+ * returns LMS_E_STATE from lms_smooth if no tile size makes a region fit in
+ * shared memory. */
 lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, int32_t lag);
 
 typedef enum {

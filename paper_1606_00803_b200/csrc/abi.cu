@@ -230,7 +230,10 @@ lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream) {
   if (sweeps < 0) fail(LMS_E_ARG, "sweeps < 0");
   if (sweeps == 0 || m->n_free == 0) return LMS_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (!m->sched.valid) build_schedule(m, s);
+  if (!m->sched.valid) {
+    sync_soa(m, s);
+    build_schedule(m, s);
+  }
   run_sweeps(m, sweeps, s);
   return LMS_OK;
   LMS_API_END
@@ -239,7 +242,9 @@ lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream) {
 lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, int32_t lag) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
-  if (kind != LMS_SCHED_AUTO && kind != LMS_SCHED_S1 && kind != LMS_SCHED_S3) fail(LMS_E_ARG, "unknown schedule");
+  if (kind != LMS_SCHED_AUTO && kind != LMS_SCHED_S1 && kind != LMS_SCHED_S3 && kind != LMS_SCHED_GZ)
+    fail(LMS_E_ARG, "unknown schedule");
+  if (kind == LMS_SCHED_GZ && lag > 8) fail(LMS_E_ARG, "GZ: at most 8 sweeps per pass");
   if (tile < 0 || lag < 0) fail(LMS_E_ARG, "tile/lag < 0");
   if (tile != 0 && (tile < 32 || tile > (1 << 20))) fail(LMS_E_ARG, "tile must be in [32, 2^20]");
   m->sched_req = kind;
@@ -264,8 +269,9 @@ lms_status lms_set_tiling(lms_mesh_t m, lms_tiling_kind kind) {
 lms_status lms_schedule_info2(lms_mesh_t m, int32_t* tiling, int64_t* n_tiles, int32_t* max_reach) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
-  if (tiling) *tiling = m->sched.valid ? m->sched.tiling : 0;
-  if (n_tiles) *n_tiles = m->sched.valid ? m->sched.K : 0;
+  const bool gz = m->sched.valid && m->sched.kind == LMS_SCHED_GZ;
+  if (tiling) *tiling = m->sched.valid ? (gz ? (int)LMS_TILING_SPATIAL : m->sched.tiling) : 0;
+  if (n_tiles) *n_tiles = m->sched.valid ? (gz ? m->sched.gz_K : m->sched.K) : 0;
   if (max_reach) *max_reach = m->sched.valid ? m->sched.max_reach : 0;
   return LMS_OK;
   LMS_API_END
@@ -287,8 +293,9 @@ lms_status lms_schedule_info(lms_mesh_t m, int64_t* n_free, int32_t* sched_kind,
   if (!m) fail(LMS_E_ARG, "NULL handle");
   if (n_free) *n_free = m->n_free;
   if (sched_kind) *sched_kind = m->sched.valid ? m->sched.kind : m->sched_req;
-  if (tile) *tile = m->sched.valid ? m->sched.tile : 0;
-  if (lag) *lag = m->sched.valid ? m->sched.lag : 0;
+  const bool gz = m->sched.valid && m->sched.kind == LMS_SCHED_GZ;
+  if (tile) *tile = m->sched.valid ? (gz ? m->sched.gz_T : m->sched.tile) : 0;
+  if (lag) *lag = m->sched.valid ? (gz ? m->sched.gz_P : m->sched.lag) : 0;
   return LMS_OK;
   LMS_API_END
 }
@@ -297,6 +304,7 @@ lms_status lms_export_coords(lms_mesh_t m, double* const* d_out, lms_stream_t st
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
   check_coords(m->dim, d_out);
+  sync_soa(m, (cudaStream_t)stream);
   for (int a = 0; a < m->dim; ++a)
     LMS_TRY_CUDA(cudaMemcpyAsync(d_out[a], m->x[a].p, m->V * sizeof(double), cudaMemcpyDefault, (cudaStream_t)stream));
   return LMS_OK;
@@ -309,6 +317,7 @@ lms_status lms_import_coords(lms_mesh_t m, const double* const* d_in, lms_stream
   check_coords(m->dim, d_in);
   for (int a = 0; a < m->dim; ++a)
     LMS_TRY_CUDA(cudaMemcpyAsync(m->x[a].p, d_in[a], m->V * sizeof(double), cudaMemcpyDefault, (cudaStream_t)stream));
+  soa_changed(m);
   return LMS_OK;
   LMS_API_END
 }

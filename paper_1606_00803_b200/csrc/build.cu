@@ -286,6 +286,7 @@ __global__ void k_mark_untouched(const unsigned long long* __restrict__ keys, in
 void compute_quality(lms_mesh_s* m, cudaStream_t s) {
   if (m->quality_external) return;
   if (!m->k) fail(LMS_E_STATE, "quality needs elements (or a quality given to lms_mesh_from_csr)");
+  sync_soa(m, s);
   const int64_t n_el = m->n_el, V = m->V;
   const int k = m->k;
   DBuf<double> qe(n_el, s);

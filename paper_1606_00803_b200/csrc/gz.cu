@@ -1,0 +1,1359 @@
+// gz.cu -- ghost-zone tiled LMS sweep (schedule kind LMS_SCHED_GZ).
+//
+// Method: Eq. 1 inside Alg. 1's in-place loop over the
+// interior vertices, replayed under the fixed colouring schedule
+// (reading Z1): per sweep, for c = 0..C-1, every free colour-c vertex
+// moves to (sum of its neighbours in CSR order) / deg, IEEE binary64, no FMA.
+//
+// Why a ghost zone gives the exact colour-GS result.  Inside one sweep a vertex
+// of colour c reads the CURRENT values of its neighbours: a neighbour of a
+// lower colour has already moved in this sweep, one of a higher colour has not.
+// So after P sweeps (P*C stages) the value of v depends on the values at the
+// start of the pass only through chains v = w0 ~ w1 ~ ... ~ wd in which each
+// w_i was updated at a strictly earlier stage than w_{i-1}; a vertex at hop
+// distance d from v therefore matters only at stages <= P*C - 1 - d.  Hence a
+// tile of owned vertices can be advanced P whole sweeps EXACTLY in isolation:
+//   * update vertex w (free, hop distance d from the tile, colour c) in sweep j
+//     of the pass iff d + c + j*C <= P*C - 1   ("update set", per stage);
+//   * stage every vertex read by an update (the update set and its
+//     neighbours) from the coordinates X at the start of the pass.
+// Every owned vertex then ends the pass with exactly the value of the global
+// sequential colour schedule (bit-identical: same rows, same summation order,
+// same division).  Halo vertices may end with wrong values; they are never
+// written back.  Distances are hop counts through free vertices only (a fixed
+// vertex never moves, so no dependency chain passes through it).
+//
+// Kernel (k_sweep_gz): one persistent CTA per SM works through its share of
+// the tiles.  Producer warps stage each tile's region coordinates in a shared
+// memory ring buffer (the region ids arrive by a TMA bulk copy, the
+// coordinates by 16-byte cp.async gathers that complete on an mbarrier).
+// Worker warps take "items" -- 32 updates of one stage of one tile -- from a
+// CTA-wide cursor in (tile, stage) order, stream the item's record (neighbour
+// slots in CSR order, owned flags, global ids, dependency list) straight from
+// HBM into registers one item ahead, wait only for the earlier items of the
+// same tile whose touched slot intervals overlap theirs (dependency flags in
+// shared memory; no stage barriers), update in shared memory and store owned
+// vertices of the pass's last sweep to the second coordinate buffer X'.
+// CTAs never synchronise with each other; every tile reads the same X.
+//
+// Data (built once per mesh/ordering/tiling by build_gz, all on the GPU):
+//   meta blob, per tile (16-byte aligned): u32 hdr[HW], HW = round4(4 + P*C + 1):
+//       [0] n_items [1] n_slots [2] R [3] n_runs [4 + s] first item of stage s
+//       (s = 0..P*C); then, if n_runs > 0, the region as runs of consecutive
+//       ids: u32 {first id, first slot}[n_runs] (one TMA bulk copy per run),
+//       else i32 gid[round4(n_slots)] (one cp.async per vertex; used when
+//       runs are short, e.g. random orderings).  Slot = rank of the id.
+//   record blob, per item (rec16 * 16 bytes, R = the tile's longest row
+//   rounded up to 8):
+//       u16 rows[32][R]   lane l's neighbour slots in CSR order (0xFFFF pad)
+//       u32 pb[32]        slot of lane l's vertex | owned << 15 | dep_l << 16
+//                         (dep_l: l-th item this one waits for, 0xFFFF none)
+//       i32 gid[32]       global id of lane l's vertex
+//       u32 desc[4]       {n | sweep << 8 | stage << 16, mode, n_deps, 0};
+//                         mode 1 = wait for whole stages (too many deps)
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <utility>
+
+#include "lms_internal.cuh"
+
+namespace lms {
+
+constexpr int GZ_MAX_C = 15;    // colours: 4 bits of the update sort key
+constexpr int GZ_MAX_P = 8;     // sweeps per pass: 3 bits of the update sort key
+constexpr uint16_t GZ_PAD = 0xFFFF;
+constexpr int GZ_MAX_REGION = 32767;  // slots are 15 bits (bit 15 = owned flag)
+constexpr int GZ_MAX_DEPS = 32;       // one per lane; more -> wait for whole stages
+constexpr int GZ_BS = 8;              // records per record-ring batch
+
+__host__ __device__ inline int64_t r4(int64_t n) { return (n + 3) & ~(int64_t)3; }
+__host__ __device__ inline int gz_hdr_words(int C, int P) { return (int)r4(4 + P * C + 1); }
+__host__ __device__ inline int gz_rec16(int R) { return (64 * R + 128 + 128 + 16) / 16; }
+
+
+// ---------------------------------------------------------------- build kernels
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* __restrict__ a, int64_t lo, int64_t hi,
+                                                   uint64_t key) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// level 0: one key (tile << 32 | v) per vertex; fixed vertices get the
+// sentinel ~0 (sorted to the end and dropped)
+__global__ void k_gz_lvl0(const uint8_t* __restrict__ fixed, const int32_t* __restrict__ tile_of, int64_t V,
+                          uint64_t* keys) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+    keys[v] = fixed[v] ? ~0ull : (((uint64_t)(uint32_t)tile_of[v] << 32) | (uint32_t)v);
+}
+
+// expansion counts: neighbours of free entries (+1 for the entry itself if self)
+__global__ void k_gz_cnt(const uint64_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ rp,
+                         const uint8_t* __restrict__ fixed, int self, int64_t* cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = (int32_t)(keys[i] & 0xffffffffull);
+    cnt[i] = (fixed[v] ? 0 : (int64_t)(rp[v + 1] - rp[v])) + self;
+  }
+}
+
+__global__ void k_gz_emit(const uint64_t* __restrict__ keys, int64_t n, const int64_t* __restrict__ off,
+                          const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                          const uint8_t* __restrict__ fixed, int self, uint64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[i];
+    const uint64_t hi = key & 0xffffffff00000000ull;
+    const int32_t v = (int32_t)(key & 0xffffffffull);
+    int64_t o = off[i];
+    if (self) out[o++] = key;
+    if (!fixed[v])
+      for (int32_t e = rp[v]; e < rp[v + 1]; ++e) out[o++] = hi | (uint32_t)col[e];
+  }
+}
+
+// keep candidates that are in neither of the two previous BFS levels
+__global__ void k_gz_not_in(const uint64_t* __restrict__ cand, int64_t n, const uint64_t* __restrict__ a, int64_t na,
+                            const uint64_t* __restrict__ b, int64_t nb, uint8_t* keep) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = cand[i];
+    bool in = false;
+    if (na) {
+      const int64_t p = lower_bound_u64(a, 0, na, key);
+      in = p < na && a[p] == key;
+    }
+    if (!in && nb) {
+      const int64_t p = lower_bound_u64(b, 0, nb, key);
+      in = p < nb && b[p] == key;
+    }
+    keep[i] = in ? 0 : 1;
+  }
+}
+
+// update set of one level: free entries with L + colour <= D - 1
+__global__ void k_gz_collect_u(const uint64_t* __restrict__ keys, int64_t n, int L, int D,
+                               const uint8_t* __restrict__ fixed, const int8_t* __restrict__ colour,
+                               uint64_t* ukey, uint8_t* ud, unsigned long long* nu) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = (int32_t)(keys[i] & 0xffffffffull);
+    if (fixed[v] || L + colour[v] > D - 1) continue;
+    const unsigned long long p = atomicAdd(nu, 1ull);
+    ukey[p] = keys[i];
+    ud[p] = (uint8_t)L;
+  }
+}
+
+// offsets of tile k inside a sorted key array (tile in the high 32 bits)
+__global__ void k_gz_tile_off(const uint64_t* __restrict__ keys, int64_t n, int64_t K, int64_t* off) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= K; k += (int64_t)gridDim.x * blockDim.x)
+    off[k] = lower_bound_u64(keys, 0, n, (uint64_t)k << 32);
+}
+
+__global__ void k_gz_low32(const uint64_t* __restrict__ keys, int64_t n, int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)(keys[i] & 0xffffffffull);
+}
+
+__global__ void k_gz_nonempty(const int64_t* __restrict__ nreg, int64_t K, uint8_t* flag, int32_t* ids) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    flag[k] = nreg[k] > 0;
+    ids[k] = (int32_t)k;
+  }
+}
+
+// update sort key: tile << 23 | colour << 19 | (P - sweeps needed) << 16 | local index
+__global__ void k_gz_ukey(const uint64_t* __restrict__ ukey, const uint8_t* __restrict__ ud, int64_t n,
+                          const uint64_t* __restrict__ reg, const int64_t* __restrict__ reg_off,
+                          const int8_t* __restrict__ colour, int C, int P, uint64_t* ck, int32_t* cv) {
+  const int D = C * P;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = ukey[i];
+    const int64_t k = (int64_t)(key >> 32);
+    const int32_t v = (int32_t)(key & 0xffffffffull);
+    const int c = colour[v];
+    const int d = ud[i];
+    int nsw = (D - 1 - d - c) / C + 1;  // sweeps 0..nsw-1 of the pass update v
+    if (nsw > P) nsw = P;
+    const int64_t lv = lower_bound_u64(reg, reg_off[k], reg_off[k + 1], key) - reg_off[k];
+    ck[i] = ((uint64_t)k << 23) | ((uint64_t)c << 19) | ((uint64_t)(P - nsw) << 16) | (uint64_t)lv;
+    cv[i] = v;
+  }
+}
+
+// per (tile, colour): first update, and per sweep j the number of updates
+__global__ void k_gz_kc(const uint64_t* __restrict__ ck, int64_t n, int64_t K, int C, int P, int64_t* kc_off,
+                        int32_t* cntj, int64_t* nch) {
+  for (int64_t kc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; kc <= K * C;
+       kc += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = kc / C;
+    const int c = (int)(kc - k * C);
+    const uint64_t base = ((uint64_t)k << 23) | ((uint64_t)c << 19);
+    const int64_t lo = lower_bound_u64(ck, 0, n, base);
+    kc_off[kc] = lo;
+    if (kc == K * C) continue;
+    const int64_t hi = lower_bound_u64(ck, lo, n, base + (1ull << 19));
+    for (int j = 0; j < P; ++j)
+      cntj[kc * P + j] = (int32_t)(lower_bound_u64(ck, lo, hi, base | ((uint64_t)(P - j) << 16)) - lo);
+    nch[kc] = (hi - lo + 31) >> 5;
+  }
+}
+
+
+// per tile: longest row among the tile's updates
+__global__ void k_gzd_tile_r(const uint64_t* __restrict__ ck, const int32_t* __restrict__ cv, int64_t n,
+                             const int32_t* __restrict__ rp, int* tR) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicMax(&tR[ck[i] >> 23], rp[cv[i] + 1] - rp[cv[i]]);
+}
+
+// items per (tile, stage): ceil(updates / 32), stage s = j*C + c
+__global__ void k_gzd_stage_items(const int32_t* __restrict__ cntj, int64_t K, int C, int P, int64_t* ns) {
+  const int PC = P * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K * PC; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i / PC;
+    const int sg = (int)(i - k * PC);
+    const int j = sg / C, c = sg - j * C;
+    ns[i] = (cntj[(k * C + c) * P + j] + 31) >> 5;
+  }
+}
+
+// item -> (tile*PC + stage, chunk q)
+__global__ void k_gzd_item_map(const int64_t* __restrict__ sfirst, int64_t nks, int32_t* it_ks, int32_t* it_q) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nks; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t t = sfirst[i]; t < sfirst[i + 1]; ++t) {
+      it_ks[t] = (int32_t)i;
+      it_q[t] = (int32_t)(t - sfirst[i]);
+    }
+}
+
+// per tile: table entry, record / meta sizes (16-byte units)
+__global__ void k_gzd_tile_sizes(int64_t K, int C, int P, int dim, const int* __restrict__ tR,
+                                 const int64_t* __restrict__ sfirst, const int64_t* __restrict__ reg_off,
+                                 const int64_t* __restrict__ rs, int64_t* rec_sz, int64_t* meta_sz, int64_t* nitems,
+                                 int64_t* nslots, int64_t* nruns) {
+  const int PC = P * C;
+  const int HW = gz_hdr_words(C, P);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    const int R = (max(tR[k], 1) + 7) & ~7;
+    const int64_t ni = sfirst[(k + 1) * PC] - sfirst[k * PC];
+    const int64_t nr = reg_off[k + 1] - reg_off[k];
+    nitems[k] = ni;
+    nslots[k] = nr;
+    rec_sz[k] = ni * gz_rec16(R);
+    const int64_t runs = rs[reg_off[k + 1]] - rs[reg_off[k]];
+    const bool use_runs = dim == 2 && runs > 0 && nr >= 4 * runs;  // 2D (interleaved) and runs long enough
+    nruns[k] = use_runs ? runs : 0;
+    meta_sz[k] = nr > 0 ? (4 * (int64_t)HW + (use_runs ? 8 * runs : 4 * r4(nr)) + 15) / 16 : 0;
+  }
+}
+
+__global__ void k_gzd_tiles(int64_t K, int C, int P, const int* __restrict__ tR, const int64_t* __restrict__ rec_off,
+                            const int64_t* __restrict__ meta_off, const int64_t* __restrict__ nitems,
+                            const int64_t* __restrict__ nslots, const int64_t* __restrict__ nruns,
+                            const int64_t* __restrict__ sfirst, GzTile* tab,
+                            int32_t* item_sweep, uint32_t* meta32) {
+  const int PC = P * C;
+  const int HW = gz_hdr_words(C, P);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    const int R = (max(tR[k], 1) + 7) & ~7;
+    GzTile t;
+    t.rec_base = rec_off[k];
+    t.meta_base = meta_off[k];
+    t.meta16 = (uint32_t)(meta_off[k + 1] - meta_off[k]);
+    t.rec16 = (uint32_t)gz_rec16(R);
+    t.n_items = (uint32_t)nitems[k];
+    t.n_slots = (uint32_t)nslots[k];
+    t.R = (uint32_t)R;
+    t.pad0 = t.pad1 = t.pad2 = 0;
+    tab[k] = t;
+    const int64_t f0 = sfirst[k * PC];
+    for (int j = 0; j <= P; ++j) item_sweep[k * (P + 1) + j] = (int32_t)(sfirst[k * PC + j * C] - f0);
+    if (t.meta16 == 0) continue;
+    uint32_t* h = meta32 + meta_off[k] * 4;
+    for (int q = 0; q < HW; ++q) h[q] = 0;
+    h[0] = t.n_items;
+    h[1] = t.n_slots;
+    h[2] = (uint32_t)R;
+    h[3] = (uint32_t)nruns[k];
+    for (int sg = 0; sg <= PC; ++sg) h[4 + sg] = (uint32_t)(sfirst[k * PC + sg] - f0);
+  }
+}
+
+// run starts of the region lists (a new run at a tile start or an id gap)
+__global__ void k_gzd_runflag(const uint64_t* __restrict__ reg, int64_t n, int64_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (i == 0 || (reg[i] >> 32) != (reg[i - 1] >> 32) || reg[i] != reg[i - 1] + 1) ? 1 : 0;
+}
+
+// the region into each tile's meta block (after the header): runs or ids
+__global__ void k_gzd_region(const uint64_t* __restrict__ reg, int64_t n, int C, int P,
+                             const int64_t* __restrict__ reg_off, const int64_t* __restrict__ rs,
+                             const int64_t* __restrict__ nruns, const int64_t* __restrict__ meta_off,
+                             uint32_t* meta32) {
+  const int HW = gz_hdr_words(C, P);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = (int64_t)(reg[i] >> 32);
+    const uint32_t g = (uint32_t)(reg[i] & 0xffffffffull);
+    uint32_t* base = meta32 + meta_off[k] * 4 + HW;
+    if (nruns[k] > 0) {
+      if (rs[i + 1] != rs[i]) {  // run start
+        const int64_t r = rs[i] - rs[reg_off[k]];
+        base[2 * r] = g;
+        base[2 * r + 1] = (uint32_t)(i - reg_off[k]);
+      }
+    } else {
+      base[i - reg_off[k]] = g;
+    }
+  }
+}
+
+// one warp per item: the record (rows, slots + owned flags, ids, descriptor)
+// and the item's touched slot interval [lo, hi]
+__global__ void k_gzd_records(const int32_t* __restrict__ it_ks, const int32_t* __restrict__ it_q, int64_t NI,
+                              int C, int P, const int64_t* __restrict__ kc_off, const int32_t* __restrict__ cntj,
+                              const uint64_t* __restrict__ ck, const int32_t* __restrict__ cv,
+                              const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
+                              const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const int32_t* __restrict__ tile_of, const uint64_t* __restrict__ reg,
+                              const int64_t* __restrict__ reg_off, uint4* rec, int32_t* it_lo, int32_t* it_hi) {
+  const int lane = threadIdx.x & 31;
+  const int PC = P * C;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = w0; it < NI; it += nw) {
+    const int64_t ks = it_ks[it];
+    const int64_t k = ks / PC;
+    const int sg = (int)(ks - k * PC);
+    const int j = sg / C, c = sg - j * C;
+    const int q = it_q[it];
+    const int64_t kc = k * C + c;
+    const int nupd = cntj[kc * P + j];
+    const int n = min(32, nupd - 32 * q);
+    const GzTile t = tab[k];
+    const int R = (int)t.R;
+    const int64_t tloc = it - sfirst[k * PC];  // item index inside the tile
+    unsigned char* base = reinterpret_cast<unsigned char*>(rec + t.rec_base + tloc * t.rec16);
+    uint16_t* rows = reinterpret_cast<uint16_t*>(base);
+    uint32_t* pb = reinterpret_cast<uint32_t*>(base + 64 * R);
+    int32_t* gid = reinterpret_cast<int32_t*>(base + 64 * R + 128);
+    uint32_t* desc = reinterpret_cast<uint32_t*>(base + 64 * R + 256);
+    int lo = 0x7fffffff, hi = -1;
+    uint32_t p = 0xffff0000u | 0x7fffu;
+    int32_t g = -1;
+    const uint64_t kh = (uint64_t)k << 32;
+    const int64_t ra = reg_off[k], rb = reg_off[k + 1];
+    if (lane < n) {
+      const int64_t u = kc_off[kc] + 32 * q + lane;
+      const int32_t v = cv[u];
+      const int lv = (int)(ck[u] & 0xffffull);
+      g = v;
+      p = 0xffff0000u | (uint32_t)lv | (tile_of[v] == (int32_t)k ? 0x8000u : 0u);
+      lo = hi = lv;
+      const int32_t b = rp[v], d = rp[v + 1] - b;
+      for (int w = 0; w < R; ++w) {
+        uint16_t li = GZ_PAD;
+        if (w < d) {
+          const int sl = (int)(lower_bound_u64(reg, ra, rb, kh | (uint32_t)col[b + w]) - ra);
+          li = (uint16_t)sl;
+          lo = min(lo, sl);
+          hi = max(hi, sl);
+        }
+        rows[lane * R + w] = li;
+      }
+    } else {
+      for (int w = 0; w < R; ++w) rows[lane * R + w] = GZ_PAD;
+    }
+    pb[lane] = p;
+    gid[lane] = g;
+    for (int o = 16; o; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      desc[0] = (uint32_t)n | ((uint32_t)j << 8) | ((uint32_t)sg << 16);
+      desc[1] = 0;
+      desc[2] = 0;
+      desc[3] = 0;
+      it_lo[it] = lo;
+      it_hi[it] = hi;
+    }
+  }
+}
+
+// dependencies: the earlier items of stages [s - C, s - 1] of the same tile
+// whose touched slot intervals overlap this item's (a superset of the items it
+// shares a vertex with; older stages are ordered transitively through them)
+__global__ void k_gzd_deps(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P,
+                           const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
+                           const int32_t* __restrict__ it_lo, const int32_t* __restrict__ it_hi, uint4* rec) {
+  const int PC = P * C;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < NI; it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ks = it_ks[it];
+    const int64_t k = ks / PC;
+    const int sg = (int)(ks - k * PC);
+    const GzTile t = tab[k];
+    const int64_t f0 = sfirst[k * PC];
+    unsigned char* base = reinterpret_cast<unsigned char*>(rec + t.rec_base + (it - f0) * t.rec16);
+    uint32_t* pb = reinterpret_cast<uint32_t*>(base + 64 * t.R);
+    uint32_t* desc = reinterpret_cast<uint32_t*>(base + 64 * t.R + 256);
+    const int lo = it_lo[it], hi = it_hi[it];
+    const int64_t a = sfirst[k * PC + (sg - C > 0 ? sg - C : 0)], b = sfirst[k * PC + sg];
+    int nd = 0;
+    for (int64_t o = a; o < b; ++o)
+      if (it_lo[o] <= hi && it_hi[o] >= lo) {
+        if (nd < GZ_MAX_DEPS) pb[nd] = (pb[nd] & 0xffffu) | ((uint32_t)(o - f0) << 16);
+        ++nd;
+      }
+    desc[1] = nd > GZ_MAX_DEPS ? 1u : 0u;
+    desc[2] = (uint32_t)nd;
+  }
+}
+
+__global__ void k_gzd_nonempty(const int64_t* __restrict__ nslots, int64_t K, uint8_t* flag, int32_t* ids) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    flag[k] = nslots[k] > 0;
+    ids[k] = (int32_t)k;
+  }
+}
+
+// ---------------------------------------------------------------- the sweep kernel
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// arrives on b once all of this thread's earlier cp.async copies have landed
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+// streamed once per pass: skip L1, evict first from L2
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld_stream16(const uint4* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream4(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ void unpack8(const uint4 q, uint16_t* u) {
+  u[0] = (uint16_t)(q.x & 0xffff); u[1] = (uint16_t)(q.x >> 16);
+  u[2] = (uint16_t)(q.y & 0xffff); u[3] = (uint16_t)(q.y >> 16);
+  u[4] = (uint16_t)(q.z & 0xffff); u[5] = (uint16_t)(q.z >> 16);
+  u[6] = (uint16_t)(q.w & 0xffff); u[7] = (uint16_t)(q.w >> 16);
+}
+
+// An item's record held in registers (this lane's part).
+template <int RMAX>
+struct GzRec {
+  uint4 row[RMAX / 8];
+  uint32_t pb;
+  int32_t gid;
+  uint4 desc;
+  int tile;   // index into the CTA's tile list, -1 = no more work
+  int t;      // item index inside the tile
+};
+
+// Eq. 1 for this lane's update: neighbours (CSR order) from shared memory,
+// ordered IEEE adds, IEEE division, result back to shared memory; returns the
+// new value through (ox, oy, oz).
+template <int DIM, int RMAX>
+__device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uint4* __restrict__ rowg, double* sc,
+                                          int nr4, double& ox, double& oy, double& oz) {
+  const int v = (int)(r.pb & 0x7fffu);
+  uint16_t u[RMAX];
+#pragma unroll
+  for (int p = 0; p < RMAX / 8; ++p) unpack8(r.row[p], u + 8 * p);
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  int d = 0;
+  if (DIM == 2) {
+    const double2* s2 = reinterpret_cast<const double2*>(sc);
+    double2 g[RMAX];
+#pragma unroll
+    for (int w = 0; w < RMAX; ++w) g[w] = (u[w] != GZ_PAD) ? s2[u[w]] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int w = 0; w < RMAX; ++w)
+      if (u[w] != GZ_PAD) {
+        if (w == 0) { sx = g[w].x; sy = g[w].y; }
+        else { sx = __dadd_rn(sx, g[w].x); sy = __dadd_rn(sy, g[w].y); }
+        ++d;
+      }
+    for (int p = RMAX / 8; p * 8 < R; ++p) {  // rows longer than RMAX: ordered tail from global
+      uint16_t t[8];
+      unpack8(rowg[p], t);
+      for (int q = 0; q < 8 && t[q] != GZ_PAD; ++q) {
+        const double2 e = s2[t[q]];
+        sx = __dadd_rn(sx, e.x);
+        sy = __dadd_rn(sy, e.y);
+        ++d;
+      }
+    }
+    const double dd = (double)d;
+    ox = __ddiv_rn(sx, dd);
+    oy = __ddiv_rn(sy, dd);
+    reinterpret_cast<double2*>(sc)[v] = make_double2(ox, oy);
+  } else {
+    double gx[RMAX], gy[RMAX], gz[RMAX];
+#pragma unroll
+    for (int w = 0; w < RMAX; ++w) {
+      const bool ok = u[w] != GZ_PAD;
+      gx[w] = ok ? sc[u[w]] : 0.0;
+      gy[w] = ok ? sc[nr4 + u[w]] : 0.0;
+      gz[w] = ok ? sc[2 * nr4 + u[w]] : 0.0;
+    }
+#pragma unroll
+    for (int w = 0; w < RMAX; ++w)
+      if (u[w] != GZ_PAD) {
+        if (w == 0) { sx = gx[w]; sy = gy[w]; sz = gz[w]; }
+        else { sx = __dadd_rn(sx, gx[w]); sy = __dadd_rn(sy, gy[w]); sz = __dadd_rn(sz, gz[w]); }
+        ++d;
+      }
+    for (int p = RMAX / 8; p * 8 < R; ++p) {
+      uint16_t t[8];
+      unpack8(rowg[p], t);
+      for (int q = 0; q < 8 && t[q] != GZ_PAD; ++q) {
+        sx = __dadd_rn(sx, sc[t[q]]);
+        sy = __dadd_rn(sy, sc[nr4 + t[q]]);
+        sz = __dadd_rn(sz, sc[2 * nr4 + t[q]]);
+        ++d;
+      }
+    }
+    const double dd = (double)d;
+    ox = __ddiv_rn(sx, dd);
+    oy = __ddiv_rn(sy, dd);
+    oz = __ddiv_rn(sz, dd);
+    sc[v] = ox;
+    sc[nr4 + v] = oy;
+    sc[2 * nr4 + v] = oz;
+  }
+}
+
+// Shared-memory layout of k_sweep_gz: see GzLayout (lms_internal.cuh) and plan_layout.
+
+// Warp roles: warp 0 stages tile regions into the coordinate ring (TMA bulk
+// copies of id runs, or 16-byte cp.async gathers), warp 1 streams item
+// records into the record ring (one TMA bulk copy per record, in claim
+// order), warps 2.. are workers (one claimed item at a time).
+template <int DIM, int RMAX>
+__global__ void __launch_bounds__(DIM == 2 ? 640 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
+                                                                      const GzTile* __restrict__ tab,
+                                                                      const int32_t* __restrict__ item_sweep,
+                                                                      const uint4* __restrict__ meta,
+                                                                      const uint4* __restrict__ rec,
+                                                                      const double2* __restrict__ a0,
+                                                                      double2* __restrict__ a1,
+                                                                      const double* __restrict__ x0,
+                                                                      const double* __restrict__ y0,
+                                                                      const double* __restrict__ z0,
+                                                                      double* __restrict__ x1,
+                                                                      double* __restrict__ y1,
+                                                                      double* __restrict__ z1, int C, int P, int j0,
+                                                                      GzLayout L, unsigned long long* stats) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int NB = L.NB, RR = L.RR;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);     // [NB] region coordinates of the buffer's tile landed
+  uint64_t* empty = full + NB;                          // [NB] buffer's tile finished
+  uint64_t* rfull = empty + NB;                         // [RR] record batch landed
+  uint64_t* rempty = rfull + RR;                        // [RR] record batch consumed (GZ_BS arrivals)
+  uint64_t* sbar = rempty + RR;                         // [1] producer staging copy landed
+  int* ctl = reinterpret_cast<int*>(sbar + 1);          // [0] cursor, [1..NB] buf_tile, [NB+1..2NB] ndone
+  volatile int* buf_tile = ctl + 1;
+  int* ndone = ctl + 1 + NB;
+  long long* t_rec = reinterpret_cast<long long*>(sm + L.off_tab);
+  int* t_rec16 = reinterpret_cast<int*>(t_rec + L.tiles_cap);
+  int* t_R = t_rec16 + L.tiles_cap;
+  int* t_item0 = t_R + L.tiles_cap;
+  int* t_pre = t_item0 + L.tiles_cap;  // [n_my + 1]
+  unsigned char* stg = sm + L.off_stage;
+  unsigned char* rring = sm + L.off_rec;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_my = ntiles > (int)blockIdx.x ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int PC = P * C;
+  const int HW = gz_hdr_words(C, P);
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(full + b, 32);
+      mbar_init(empty + b, 1);
+      buf_tile[b] = -1;
+      ndone[b] = 0;
+    }
+    for (int r = 0; r < RR; ++r) {
+      mbar_init(rfull + r, 1);
+      mbar_init(rempty + r, GZ_BS);
+    }
+    mbar_init(sbar, 1);
+    ctl[0] = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // dependency flags are tagged with the tile index + 1, so they must start
+  // below every tag (shared memory is not cleared between launches)
+  for (int b = 0; b < NB; ++b) {
+    int* f = reinterpret_cast<int*>(sm + L.off_ring + (size_t)b * L.buf_bytes + L.flag_off);
+    for (int q = threadIdx.x; q < (L.cnt_off - L.flag_off) / 4; q += blockDim.x) f[q] = 0;
+  }
+  for (int i = threadIdx.x; i < n_my; i += blockDim.x) {
+    const int k = tiles[blockIdx.x + (long long)i * gridDim.x];
+    const GzTile t = tab[k];
+    t_rec[i] = t.rec_base;
+    t_rec16[i] = (int)t.rec16;
+    t_R[i] = (int)t.R;
+    const int a = item_sweep[k * (P + 1) + j0];
+    t_item0[i] = a;
+    t_pre[i + 1] = (int)t.n_items - a;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // prefix of the items this CTA runs, in tile order
+    t_pre[0] = 0;
+    for (int i = 0; i < n_my; ++i) t_pre[i + 1] += t_pre[i];
+  }
+  __syncthreads();
+  const int total = t_pre[n_my];
+
+  if (warp == 0) {  // -------------------------------------------- region producer
+    for (int i = 0; i < n_my; ++i) {
+      const int b = i % NB;
+      const uint32_t ph = (uint32_t)(i / NB) & 1u;
+      if (i >= NB) mbar_wait(empty + b, ph ^ 1u);
+      const int k = tiles[blockIdx.x + (long long)i * gridDim.x];
+      const GzTile t = tab[k];
+      const uint32_t bytes = t.meta16 * 16u;
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging was read generically
+        mbar_expect_tx(sbar, bytes);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(meta + t.meta_base);
+        constexpr uint32_t PIECE = 1u << 15;
+        for (uint32_t o = 0; o < bytes; o += PIECE)
+          bulk_g2s(stg + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, sbar);
+      }
+      mbar_wait(sbar, (uint32_t)i & 1u);
+      unsigned char* buf = sm + L.off_ring + (size_t)b * L.buf_bytes;
+      const uint32_t* hsrc = reinterpret_cast<const uint32_t*>(stg);
+      uint32_t* hdst = reinterpret_cast<uint32_t*>(buf);
+      for (int q = lane; q < HW; q += 32) hdst[q] = hsrc[q];
+      int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
+      for (int q = lane; q < PC; q += 32) cnt[q] = 0;
+      const int nr = (int)hsrc[1];
+      const int nruns = (int)hsrc[3];
+      const int nr4 = (int)r4(nr);
+      double* sc = reinterpret_cast<double*>(buf + L.coord_off);
+      if (DIM == 2 && nruns > 0) {
+        // contiguous id runs: TMA bulk copies of the interleaved coordinates
+        const uint32_t* runs = hsrc + HW;
+        if (lane == 0) mbar_expect_tx_only(full + b, (uint32_t)nr * 16u);
+        __syncwarp();
+        for (int r = lane; r < nruns; r += 32) {
+          const uint32_t g = runs[2 * r], s0 = runs[2 * r + 1];
+          const uint32_t s1 = r + 1 < nruns ? runs[2 * r + 3] : (uint32_t)nr;
+          bulk_g2s(sc + 2 * s0, a0 + g, (s1 - s0) * 16u, full + b);
+        }
+        mbar_arrive(full + b);  // the 32 arrivals; the phase also waits for the bytes
+      } else {
+        const int32_t* gid = reinterpret_cast<const int32_t*>(hsrc + HW);
+        for (int idx = lane; idx < nr; idx += 32) {
+          const int32_t gv = gid[idx];
+          if (DIM == 2) {
+            cp_async16(sc + 2 * idx, a0 + gv);
+          } else {
+            cp_async8(sc + idx, x0 + gv);
+            cp_async8(sc + nr4 + idx, y0 + gv);
+            cp_async8(sc + 2 * nr4 + idx, z0 + gv);
+          }
+        }
+        mbar_arrive_cp_async(full + b);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        ndone[b] = 0;
+        __threadfence_block();
+        buf_tile[b] = i;
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  if (warp == 1) {  // ---------------------------------------------- record loader
+    // batch g = claims [g*BS, (g+1)*BS) -> batch slot g % RR, record q of the
+    // batch at q * rec_bytes; consecutive records of one tile are contiguous
+    // in HBM, so a batch is one bulk copy per tile it touches (when the
+    // tile's record size equals the slot stride, else one per record)
+    if (lane == 0) {
+      int ti = 0;
+      const int nbat = (total + GZ_BS - 1) / GZ_BS;
+      for (int g = 0; g < nbat; ++g) {
+        const int slot = g % RR;
+        if (g >= RR) mbar_wait(rempty + slot, ((uint32_t)(g / RR) & 1u) ^ 1u);
+        const int k0 = g * GZ_BS, k1 = min(total, k0 + GZ_BS);
+        uint32_t bytes = 0;
+        for (int kc = k0, tj = ti; kc < k1;) {  // pass 1: bytes of the batch
+          while (kc >= t_pre[tj + 1]) ++tj;
+          const int kend = min(k1, t_pre[tj + 1]);
+          bytes += (uint32_t)(kend - kc) * (uint32_t)t_rec16[tj] * 16u;
+          kc = kend;
+        }
+        mbar_expect_tx(rfull + slot, bytes);
+        unsigned char* dst = rring + (size_t)slot * GZ_BS * L.rec_bytes;
+        for (int kc = k0; kc < k1;) {
+          while (kc >= t_pre[ti + 1]) ++ti;
+          const int kend = min(k1, t_pre[ti + 1]);
+          const int t = t_item0[ti] + (kc - t_pre[ti]);
+          const uint32_t rb = (uint32_t)t_rec16[ti] * 16u;
+          const uint4* src = rec + t_rec[ti] + (long long)t * t_rec16[ti];
+          if ((int)rb == L.rec_bytes) {
+            bulk_g2s(dst + (size_t)(kc - k0) * L.rec_bytes, src, (uint32_t)(kend - kc) * rb, rfull + slot);
+          } else {
+            for (int q = kc; q < kend; ++q)
+              bulk_g2s(dst + (size_t)(q - k0) * L.rec_bytes, src + (long long)(q - kc) * t_rec16[ti], rb,
+                       rfull + slot);
+          }
+          kc = kend;
+        }
+      }
+    }
+    return;
+  }
+  if (warp >= 2 + L.NW) return;
+  // ------------------------------------------------------------------- workers
+  const unsigned FULL = 0xffffffffu;
+  int ti = 0;  // this warp's position in the tile list (claims are increasing)
+  unsigned long long w_wait = 0, w_dep = 0, w_comp = 0, w_items = 0;
+  for (;;) {
+    int kc = 0;
+    if (lane == 0) kc = atomicAdd(ctl, 1);
+    kc = __shfl_sync(FULL, kc, 0);
+    if (kc >= total) break;
+    while (kc >= t_pre[ti + 1]) ++ti;
+    const int i = ti;
+    const int t = t_item0[i] + (kc - t_pre[i]);
+    const int R = t_R[i];
+    const long long c0 = stats ? clock64() : 0;
+    // the item's record, from the record ring
+    const int bat = kc / GZ_BS;
+    const int slot = bat % RR;
+    if (lane == 0) mbar_wait(rfull + slot, (uint32_t)(bat / RR) & 1u);
+    __syncwarp();
+    const unsigned char* rbase = rring + ((size_t)slot * GZ_BS + (kc - bat * GZ_BS)) * L.rec_bytes;
+    GzRec<RMAX> r;
+    {
+      const unsigned char* rb = rbase;
+      const uint4* rows = reinterpret_cast<const uint4*>(rb) + lane * (R >> 3);
+#pragma unroll
+      for (int p = 0; p < RMAX / 8; ++p) r.row[p] = (p * 8 < R) ? rows[p] : make_uint4(~0u, ~0u, ~0u, ~0u);
+      const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rb + 64 * R);
+      r.pb = pbs[lane];
+      r.gid = (int32_t)pbs[32 + lane];
+      r.desc = *reinterpret_cast<const uint4*>(rb + 64 * R + 256);
+      r.tile = i;
+      r.t = t;
+    }
+    const uint4* rowtail = reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3);
+    // the region of the item's tile
+    const int b = i % NB;
+    unsigned char* buf = sm + L.off_ring + (size_t)b * L.buf_bytes;
+    if (lane == 0) {
+      while (buf_tile[b] != i) __nanosleep(32);
+      mbar_wait(full + b, (uint32_t)(i / NB) & 1u);
+    }
+    __syncwarp();
+    const long long c1 = stats ? clock64() : 0;
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(buf);
+    volatile int* flags = reinterpret_cast<volatile int*>(buf + L.flag_off);
+    int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
+    const int n = (int)(r.desc.x & 0xffu);
+    const int j = (int)((r.desc.x >> 8) & 0xffu);
+    const int sg = (int)(r.desc.x >> 16);
+    const int item0 = t_item0[i];
+    // this item's dependencies
+    if (r.desc.y == 0) {
+      const int dep = (int)(r.pb >> 16);
+      if (dep != 0xffff && dep >= item0)
+        while (flags[dep] != i + 1) __nanosleep(20);
+    } else if (lane == 0) {
+      const int s0 = max(sg - C, j0 * C);
+      for (int s2 = s0; s2 < sg; ++s2) {
+        const int need = (int)(hdr[4 + s2 + 1] - hdr[4 + s2]);
+        while (*(volatile int*)(cnt + s2) != need) __nanosleep(20);
+      }
+    }
+    __syncwarp();
+    __threadfence_block();
+    const long long c2 = stats ? clock64() : 0;
+    if (lane < n) {
+      const int nr4 = (int)r4(hdr[1]);
+      double* sc = reinterpret_cast<double*>(buf + L.coord_off);
+      double ox, oy, oz;
+      gz_update<DIM, RMAX>(r, R, rowtail, sc, nr4, ox, oy, oz);
+      if (j == P - 1 && (r.pb & 0x8000u)) {  // owned vertex, final value of the pass
+        if (DIM == 2) {
+          a1[r.gid] = make_double2(ox, oy);
+        } else {
+          x1[r.gid] = ox;
+          y1[r.gid] = oy;
+          z1[r.gid] = oz;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(rempty + slot);  // one of the batch's records consumed (rows > RMAX were read in gz_update)
+      __threadfence_block();
+      flags[t] = i + 1;
+      atomicAdd(cnt + sg, 1);
+      const int n_eff = t_pre[i + 1] - t_pre[i];
+      if (atomicAdd(ndone + b, 1) == n_eff - 1) mbar_arrive(empty + b);
+    }
+    if (stats) {
+      const long long c3 = clock64();
+      w_wait += c1 - c0;
+      w_dep += c2 - c1;
+      w_comp += c3 - c2;
+      w_items += 1;
+    }
+  }
+  if (stats && lane == 0) {
+    atomicAdd(stats + 0, w_wait);
+    atomicAdd(stats + 1, w_dep);
+    atomicAdd(stats + 2, w_comp);
+    atomicAdd(stats + 3, w_items);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static unsigned gsz(int64_t n, int block = 256, unsigned cap = 8192) {
+  const unsigned g = grid_for(n, block);
+  return g > cap ? cap : g;
+}
+
+static void sort_keys(DBuf<uint64_t>& keys, int64_t n, int end_bit, cudaStream_t s) {
+  if (n <= 1) return;
+  DBuf<uint64_t> out(n, s);
+  size_t tb = 0;
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.p, out.p, n, 0, end_bit, s));
+  DBuf<char> tmp(tb, s);
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, out.p, n, 0, end_bit, s));
+  keys = std::move(out);
+}
+
+static int64_t read_i64(const void* dptr, bool is64, cudaStream_t s) {
+  int64_t h = 0;
+  if (is64) {
+    LMS_TRY_CUDA(cudaMemcpyAsync(&h, dptr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  } else {
+    int hi = 0;
+    LMS_TRY_CUDA(cudaMemcpyAsync(&hi, dptr, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    return hi;
+  }
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+static int64_t unique_keys(DBuf<uint64_t>& keys, int64_t n, cudaStream_t s) {
+  if (n <= 1) return n;
+  DBuf<uint64_t> out(n, s);
+  DBuf<int> nsel(1, s);
+  size_t tb = 0;
+  LMS_TRY_CUDA(cub::DeviceSelect::Unique(nullptr, tb, keys.p, out.p, nsel.p, n, s));
+  DBuf<char> tmp(tb, s);
+  LMS_TRY_CUDA(cub::DeviceSelect::Unique(tmp.p, tb, keys.p, out.p, nsel.p, n, s));
+  keys = std::move(out);
+  return read_i64(nsel.p, false, s);
+}
+
+// exclusive scan of n int64 values into out[0..n] (out[n] = total); returns the total
+static int64_t scan_i64(const int64_t* in, int64_t n, int64_t* out, cudaStream_t s) {
+  LMS_TRY_CUDA(cudaMemsetAsync(out + n, 0, sizeof(int64_t), s));
+  if (n > 0) {
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out + 1, n, s));
+    DBuf<char> tmp(tb, s);
+    LMS_TRY_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, in, out + 1, n, s));
+  }
+  LMS_TRY_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), s));
+  return read_i64(out + n, true, s);
+}
+
+// expand entries: neighbours of free entries (+ the entries themselves if self)
+static int64_t expand(const DBuf<uint64_t>& keys, int64_t n, lms_mesh_s* m, int self, DBuf<uint64_t>& out,
+                      cudaStream_t s) {
+  DBuf<int64_t> cnt(n > 0 ? n : 1, s), off(n + 1, s);
+  if (n > 0) {
+    k_gz_cnt<<<gsz(n), 256, 0, s>>>(keys.p, n, m->row_ptr.p, m->fixed.p, self, cnt.p);
+    LMS_CHECK_LAUNCH();
+  }
+  const int64_t tot = scan_i64(cnt.p, n, off.p, s);
+  out.alloc(tot > 0 ? tot : 1, s);
+  if (n > 0 && tot > 0) {
+    k_gz_emit<<<gsz(n), 256, 0, s>>>(keys.p, n, off.p, m->row_ptr.p, m->col.p, m->fixed.p, self, out.p);
+    LMS_CHECK_LAUNCH();
+  }
+  return tot;
+}
+
+static int bits_for(int64_t n) {
+  int b = 1;
+  while (((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+struct GzNeeds {
+  int64_t max_slots = 0, max_items = 0, max_meta16 = 0, max_row = 0;
+};
+
+// Build the GZ schedule for tiles of ~T owned vertices and P sweeps per pass.
+// Returns false (nothing kept) if the limits (region <= 32767 slots, items per
+// tile, `fits`: the shared-memory plan) are not met.
+template <typename Fits>
+static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* out, Fits fits) {
+
+  Schedule& S = m->sched;
+  const int64_t V = m->V;
+  const int C = m->C;
+  const int D = C * P;
+  DBuf<int32_t> tile_of(V, s);
+  const int64_t K = spatial_tiles(m, T, tile_of.p, s);
+  const int kbits = bits_for(K + 1);
+  const int end_bit = 32 + kbits;
+
+  // level 0: the owned free vertices of every tile, sorted by (tile, id)
+  std::vector<DBuf<uint64_t>> lev(D);
+  std::vector<int64_t> nlev(D, 0);
+  lev[0].alloc(V, s);
+  k_gz_lvl0<<<gsz(V), 256, 0, s>>>(m->fixed.p, tile_of.p, V, lev[0].p);
+  LMS_CHECK_LAUNCH();
+  {
+    DBuf<uint64_t>& l0 = lev[0];
+    if (V > 1) {
+      DBuf<uint64_t> out(V, s);
+      size_t tb = 0;
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, l0.p, out.p, V, 0, 64, s));
+      DBuf<char> tmp(tb, s);
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, l0.p, out.p, V, 0, 64, s));
+      l0 = std::move(out);
+    }
+  }
+  nlev[0] = m->n_free;
+  // levels 1..D-1: breadth-first rings through free vertices, per tile
+  for (int L = 1; L < D; ++L) {
+    DBuf<uint64_t> cand;
+    int64_t nc = expand(lev[L - 1], nlev[L - 1], m, 0, cand, s);
+    sort_keys(cand, nc, end_bit, s);
+    nc = unique_keys(cand, nc, s);
+    DBuf<uint8_t> keep(nc > 0 ? nc : 1, s);
+    if (nc > 0) {
+      k_gz_not_in<<<gsz(nc), 256, 0, s>>>(cand.p, nc, lev[L - 1].p, nlev[L - 1], L >= 2 ? lev[L - 2].p : nullptr,
+                                          L >= 2 ? nlev[L - 2] : 0, keep.p);
+      LMS_CHECK_LAUNCH();
+    }
+    lev[L].alloc(nc > 0 ? nc : 1, s);
+    DBuf<int> nsel(1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(nsel.p, 0, sizeof(int), s));
+    if (nc > 0) {
+      size_t tb = 0;
+      LMS_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, cand.p, keep.p, lev[L].p, nsel.p, nc, s));
+      DBuf<char> tmp(tb, s);
+      LMS_TRY_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, cand.p, keep.p, lev[L].p, nsel.p, nc, s));
+    }
+    nlev[L] = read_i64(nsel.p, false, s);
+  }
+  // update set U: free entries with L + colour <= D - 1
+  int64_t ntot = 0;
+  for (int L = 0; L < D; ++L) ntot += nlev[L];
+  DBuf<uint64_t> ukey(ntot > 0 ? ntot : 1, s);
+  DBuf<uint8_t> ud(ntot > 0 ? ntot : 1, s);
+  DBuf<unsigned long long> nu(1, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(nu.p, 0, sizeof(unsigned long long), s));
+  for (int L = 0; L < D; ++L)
+    if (nlev[L] > 0) {
+      k_gz_collect_u<<<gsz(nlev[L]), 256, 0, s>>>(lev[L].p, nlev[L], L, D, m->fixed.p, m->colour.p, ukey.p, ud.p,
+                                                   nu.p);
+      LMS_CHECK_LAUNCH();
+    }
+  const int64_t nU = read_i64(nu.p, true, s);
+  for (int L = 1; L < D; ++L) lev[L].release();
+  // region = U and its neighbours, sorted by (tile, id)
+  DBuf<uint64_t> reg;
+  int64_t nreg_all = expand(ukey, nU, m, 1, reg, s);
+  sort_keys(reg, nreg_all, end_bit, s);
+  nreg_all = unique_keys(reg, nreg_all, s);
+  DBuf<int64_t> reg_off(K + 1, s);
+  k_gz_tile_off<<<gsz(K + 1), 256, 0, s>>>(reg.p, nreg_all, K, reg_off.p);
+  LMS_CHECK_LAUNCH();
+  DBuf<int64_t> own_off(K + 1, s);
+  k_gz_tile_off<<<gsz(K + 1), 256, 0, s>>>(lev[0].p, nlev[0], K, own_off.p);
+  LMS_CHECK_LAUNCH();
+  // updates sorted by (tile, colour, sweeps needed desc, local index)
+  DBuf<uint64_t> ck(nU > 0 ? nU : 1, s), ck2(nU > 0 ? nU : 1, s);
+  DBuf<int32_t> cv(nU > 0 ? nU : 1, s), cv2(nU > 0 ? nU : 1, s);
+  if (nU > 0) {
+    k_gz_ukey<<<gsz(nU), 256, 0, s>>>(ukey.p, ud.p, nU, reg.p, reg_off.p, m->colour.p, C, P, ck.p, cv.p);
+    LMS_CHECK_LAUNCH();
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ck.p, ck2.p, cv.p, cv2.p, nU, 0, 23 + kbits, s));
+    DBuf<char> tmp(tb, s);
+    LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, ck.p, ck2.p, cv.p, cv2.p, nU, 0, 23 + kbits, s));
+  }
+  ukey.release();
+  ud.release();
+  const int64_t nkc = K * C;
+  const int PC = P * C;
+  DBuf<int64_t> kc_off(nkc + 1, s), nch(nkc > 0 ? nkc : 1, s);
+  DBuf<int32_t> cntj(nkc * P > 0 ? nkc * P : 1, s);
+  k_gz_kc<<<gsz(nkc + 1), 256, 0, s>>>(ck2.p, nU, K, C, P, kc_off.p, cntj.p, nch.p);
+  LMS_CHECK_LAUNCH();
+  nch.release();
+  own_off.release();
+  // items: per (tile, stage) ceil(updates / 32), tile-major then stage-major
+  const int64_t nks = K * PC;
+  DBuf<int64_t> ns(nks > 0 ? nks : 1, s), sfirst(nks + 1, s);
+  k_gzd_stage_items<<<gsz(nks), 256, 0, s>>>(cntj.p, K, C, P, ns.p);
+  LMS_CHECK_LAUNCH();
+  const int64_t NI = scan_i64(ns.p, nks, sfirst.p, s);
+  ns.release();
+  DBuf<int32_t> it_ks(NI > 0 ? NI : 1, s), it_q(NI > 0 ? NI : 1, s);
+  if (NI > 0) {
+    k_gzd_item_map<<<gsz(nks), 256, 0, s>>>(sfirst.p, nks, it_ks.p, it_q.p);
+    LMS_CHECK_LAUNCH();
+  }
+  DBuf<int> tR(K, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(tR.p, 0, K * sizeof(int), s));
+  if (nU > 0) {
+    k_gzd_tile_r<<<gsz(nU), 256, 0, s>>>(ck2.p, cv2.p, nU, m->row_ptr.p, tR.p);
+    LMS_CHECK_LAUNCH();
+  }
+  // runs of consecutive ids in each region: rs = exclusive scan of run starts
+  DBuf<int64_t> rs(nreg_all + 1, s);
+  {
+    DBuf<int64_t> rflag(nreg_all > 0 ? nreg_all : 1, s);
+    if (nreg_all > 0) {
+      k_gzd_runflag<<<gsz(nreg_all), 256, 0, s>>>(reg.p, nreg_all, rflag.p);
+      LMS_CHECK_LAUNCH();
+    }
+    scan_i64(rflag.p, nreg_all, rs.p, s);
+  }
+  DBuf<int64_t> rec_sz(K, s), meta_sz(K, s), nitems(K, s), nslots(K, s), nruns(K, s), rec_off(K + 1, s),
+      meta_off(K + 1, s);
+  k_gzd_tile_sizes<<<gsz(K), 256, 0, s>>>(K, C, P, m->dim, tR.p, sfirst.p, reg_off.p, rs.p, rec_sz.p, meta_sz.p, nitems.p,
+                                          nslots.p, nruns.p);
+  LMS_CHECK_LAUNCH();
+  const int64_t rec16_all = scan_i64(rec_sz.p, K, rec_off.p, s);
+  const int64_t meta16_all = scan_i64(meta_sz.p, K, meta_off.p, s);
+  // size limits: largest region, items per tile, meta block, row length
+  int64_t mx[4] = {0, 0, 0, 0};
+  {
+    DBuf<int64_t> r(4, s);
+    DBuf<int> rr(1, s);
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceReduce::Max(nullptr, tb, nslots.p, r.p, K, s));
+    DBuf<char> tmp(tb, s);
+    LMS_TRY_CUDA(cub::DeviceReduce::Max(tmp.p, tb, nslots.p, r.p, K, s));
+    LMS_TRY_CUDA(cub::DeviceReduce::Max(tmp.p, tb, nitems.p, r.p + 1, K, s));
+    LMS_TRY_CUDA(cub::DeviceReduce::Max(tmp.p, tb, meta_sz.p, r.p + 2, K, s));
+    size_t tb2 = 0;
+    LMS_TRY_CUDA(cub::DeviceReduce::Max(nullptr, tb2, tR.p, rr.p, K, s));
+    DBuf<char> tmp2(tb2, s);
+    LMS_TRY_CUDA(cub::DeviceReduce::Max(tmp2.p, tb2, tR.p, rr.p, K, s));
+    LMS_TRY_CUDA(cudaMemcpyAsync(mx, r.p, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    int hr = 0;
+    LMS_TRY_CUDA(cudaMemcpyAsync(&hr, rr.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    mx[3] = hr;
+  }
+  out->max_slots = mx[0];
+  out->max_items = mx[1];
+  out->max_meta16 = mx[2];
+  out->max_row = mx[3];
+  if (mx[0] > GZ_MAX_REGION || mx[1] > 65534) return false;
+  if (!fits(*out)) return false;
+  // the blobs
+  DBuf<GzTile> tab(K > 0 ? K : 1, s);
+  DBuf<int32_t> item_sweep(K * (P + 1) > 0 ? K * (P + 1) : 1, s);
+  DBuf<uint4> meta(meta16_all > 0 ? meta16_all : 1, s), rec(rec16_all > 0 ? rec16_all : 1, s);
+  k_gzd_tiles<<<gsz(K), 256, 0, s>>>(K, C, P, tR.p, rec_off.p, meta_off.p, nitems.p, nslots.p, nruns.p, sfirst.p, tab.p,
+                                     item_sweep.p, reinterpret_cast<uint32_t*>(meta.p));
+  LMS_CHECK_LAUNCH();
+  if (nreg_all > 0) {
+    k_gzd_region<<<gsz(nreg_all), 256, 0, s>>>(reg.p, nreg_all, C, P, reg_off.p, rs.p, nruns.p, meta_off.p,
+                                               reinterpret_cast<uint32_t*>(meta.p));
+    LMS_CHECK_LAUNCH();
+  }
+  if (NI > 0) {
+    DBuf<int32_t> it_lo(NI, s), it_hi(NI, s);
+    k_gzd_records<<<gsz(NI * 32), 256, 0, s>>>(it_ks.p, it_q.p, NI, C, P, kc_off.p, cntj.p, ck2.p, cv2.p, tab.p,
+                                               sfirst.p, m->row_ptr.p, m->col.p, tile_of.p, reg.p, reg_off.p, rec.p,
+                                               it_lo.p, it_hi.p);
+    LMS_CHECK_LAUNCH();
+    k_gzd_deps<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, tab.p, sfirst.p, it_lo.p, it_hi.p, rec.p);
+    LMS_CHECK_LAUNCH();
+  }
+  // the non-empty tiles, in tile order
+  DBuf<int32_t> tiles(K > 0 ? K : 1, s);
+  int64_t nt = 0;
+  {
+    DBuf<uint8_t> flag(K > 0 ? K : 1, s);
+    k_gzd_nonempty<<<gsz(K), 256, 0, s>>>(nslots.p, K, flag.p, tiles.p);
+    LMS_CHECK_LAUNCH();
+    DBuf<int32_t> o(K > 0 ? K : 1, s);
+    DBuf<int> nsel(1, s);
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, tiles.p, flag.p, o.p, nsel.p, K, s));
+    DBuf<char> tmp(tb, s);
+    LMS_TRY_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, tiles.p, flag.p, o.p, nsel.p, K, s));
+    nt = read_i64(nsel.p, false, s);
+    tiles = std::move(o);
+  }
+  S.gz_tiles = std::move(tiles);
+  S.gz_ntiles = nt;
+  S.gz_tab = std::move(tab);
+  S.gz_item_sweep = std::move(item_sweep);
+  S.gz_meta = std::move(meta);
+  S.gz_rec = std::move(rec);
+  S.gz_P = P;
+  S.gz_nreg = nreg_all;
+  S.gz_nupd = nU;
+  S.gz_items = NI;
+  S.gz_bytes = (rec16_all + meta16_all) * 16;
+  S.gz_max_reg = (int)mx[0];
+  S.gz_K = K;
+  S.gz_T = T;
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  return true;
+}
+
+static int env_int(const char* name, int dflt, int lo, int hi) {
+  int v = dflt;
+  if (const char* e = getenv(name)) v = atoi(e);
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+static int r16i(int64_t n) { return (int)((n + 15) & ~(int64_t)15); }
+
+// Shared-memory plan for given limits; returns total bytes (> cap if none fits).
+static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int cap, int want_nb, int nw, int tiles_cap,
+                           GzLayout* L) {
+  L->NPW = 1;
+  L->NW = nw;
+  // record ring: RR batches of GZ_BS records; RR * GZ_BS - GZ_BS >= workers keeps
+  // every mbarrier phase unambiguous (a claim is never a full ring ahead)
+  L->RR = std::max(8, (nw + GZ_BS - 1) / GZ_BS + 2);
+  L->rec_bytes = gz_rec16(nd.max_row > 0 ? (int)((nd.max_row + 7) & ~7) : 8) * 16;
+  const int HW = gz_hdr_words(C, P);
+  L->hdr_bytes = r16i(4 * (int64_t)HW);
+  L->flag_off = L->hdr_bytes;
+  L->cnt_off = L->flag_off + r16i(4 * nd.max_items);
+  L->coord_off = (L->cnt_off + r16i(4 * (int64_t)P * C) + 127) & ~127;
+  const int64_t coords = dim == 2 ? 16 * nd.max_slots : 24 * r4(nd.max_slots);
+  L->buf_bytes = (int)((L->coord_off + coords + 127) & ~(int64_t)127);
+  L->stage_bytes = r16i(16 * nd.max_meta16);
+  L->tiles_cap = tiles_cap;
+  for (int nb = want_nb > 0 ? want_nb : 8; nb >= 1; --nb) {
+    L->NB = nb;
+    const int ctl = (2 * nb + 2 * L->RR + 1) * 8 + (1 + 2 * nb) * 4;
+    L->off_tab = r16i(ctl);
+    const int tab_bytes = r16i((int64_t)tiles_cap * (8 + 4 + 4 + 4) + 4 * ((int64_t)tiles_cap + 1));
+    L->off_stage = L->off_tab + tab_bytes;
+    L->off_rec = L->off_stage + L->stage_bytes;
+    L->off_ring = (L->off_rec + L->RR * GZ_BS * L->rec_bytes + 127) & ~127;
+    const int64_t total = (int64_t)L->off_ring + (int64_t)nb * L->buf_bytes;
+    if (total <= cap) return total;
+    if (want_nb > 0) return total;
+  }
+  return (int64_t)cap + 1;
+}
+
+bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
+  if (P < 1) P = 1;
+  if (m->C > GZ_MAX_C || P > GZ_MAX_P || m->C < 1) {
+    if (required) fail(LMS_E_ARG, "GZ schedule: needs 1 <= colours <= 15 and 1 <= sweeps per pass <= 8");
+    return false;
+  }
+  int cap = 0, nsm = 0;
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  const int maxw = (m->dim == 2 ? 640 : 384) / 32;  // the kernel's launch bounds
+  const int nw = env_int("LMS_GZ_WORKERS", maxw - 2, 1, maxw - 2);  // + region producer + record loader
+  const int want_nb = env_int("LMS_GZ_BUFFERS", 0, 0, 8);
+  const int dim = m->dim, C = m->C;
+  GzNeeds nd;
+  Schedule& S = m->sched;
+  for (int t = T; t >= 32; t = t * 5 / 8) {
+    // tiles per CTA is bounded by the tile count, known after the build; use
+    // an upper bound from the mesh size
+    auto fits = [&](const GzNeeds& q) {
+      const int64_t K = (m->V + t - 1) / t * 2 + 16;
+      const int cap_t = (int)std::min<int64_t>(K / nsm + 2, 1 << 20);
+      GzLayout L;
+      return plan_layout(q, dim, C, P, cap, want_nb, nw, cap_t, &L) <= cap;
+    };
+    if (build_gz_once(m, t, P, s, &nd, fits)) {
+      const int tiles_cap = (int)((S.gz_ntiles + nsm - 1) / nsm) + 1;
+      const int64_t total = plan_layout(nd, dim, C, P, cap, want_nb, nw, tiles_cap, &S.gz_L);
+      if (total > cap) continue;
+      S.gz_smem = (int)total;
+      S.gz_threads = 32 * (2 + S.gz_L.NW);
+      if (getenv("LMS_GZ_VERBOSE"))
+        fprintf(stderr, "[gz] T=%d P=%d tiles=%lld items=%lld NB=%d RR=%d NW=%d smem=%d buf=%d slots<=%lld "
+                "items/tile<=%lld regions=%lld updates=%lld blob=%lld B\n", t, P, (long long)S.gz_ntiles,
+                (long long)S.gz_items, S.gz_L.NB, S.gz_L.RR, S.gz_L.NW, S.gz_smem, S.gz_L.buf_bytes,
+                (long long)nd.max_slots, (long long)nd.max_items, (long long)S.gz_nreg, (long long)S.gz_nupd,
+                (long long)S.gz_bytes);
+      return true;
+    }
+  }
+  if (required)
+    fail(LMS_E_STATE, "GZ schedule: no tile size fits a region in shared memory (region " +
+                          std::to_string(nd.max_slots) + " slots, have " + std::to_string(cap) + " B)");
+  return false;
+}
+
+template <int DIM, int RMAX>
+static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
+  Schedule& S = m->sched;
+  auto kern = k_sweep_gz<DIM, RMAX>;
+  LMS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S.gz_smem));
+  int nsm = 0;
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  const int grid = (int)(S.gz_ntiles < nsm ? S.gz_ntiles : nsm);
+  if (grid <= 0) return;
+  static unsigned long long* stats = nullptr;
+  const bool want_stats = getenv("LMS_GZ_STATS") != nullptr;
+  if (want_stats) {
+    if (!stats) LMS_TRY_CUDA(cudaMalloc(&stats, 8 * sizeof(unsigned long long)));
+    LMS_TRY_CUDA(cudaMemsetAsync(stats, 0, 8 * sizeof(unsigned long long), s));
+  }
+  const double2* a0 = DIM == 2 ? reinterpret_cast<const double2*>(m->xy[m->xy_cur].p) : nullptr;
+  double2* a1 = DIM == 2 ? reinterpret_cast<double2*>(m->xy[1 - m->xy_cur].p) : nullptr;
+  kern<<<grid, S.gz_threads, S.gz_smem, s>>>(
+      S.gz_tiles.p, (int)S.gz_ntiles, S.gz_tab.p, S.gz_item_sweep.p, S.gz_meta.p, S.gz_rec.p, a0, a1, m->x[0].p,
+      m->x[1].p, DIM == 3 ? m->x[2].p : nullptr, DIM == 3 ? m->xalt[0].p : nullptr,
+      DIM == 3 ? m->xalt[1].p : nullptr, DIM == 3 ? m->xalt[2].p : nullptr, m->C, S.gz_P, j0, S.gz_L,
+      want_stats ? stats : nullptr);
+  LMS_CHECK_LAUNCH();
+  if (want_stats) {
+    unsigned long long h[8];
+    LMS_TRY_CUDA(cudaMemcpyAsync(h, stats, sizeof(h), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    const double it = h[3] ? (double)h[3] : 1.0;
+    fprintf(stderr, "[gz stats] per item cycles: wait_tile=%.0f wait_deps=%.0f compute=%.0f (items=%.0f)\n",
+            h[0] / it, h[1] / it, h[2] / it, it);
+  }
+}
+
+__global__ void k_soa_to_aos(const double* __restrict__ x, const double* __restrict__ y, int64_t V, double2* a,
+                             double2* b) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = make_double2(x[v], y[v]);
+    a[v] = p;
+    b[v] = p;
+  }
+}
+
+__global__ void k_aos_to_soa(const double2* __restrict__ a, int64_t V, double* x, double* y) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = a[v];
+    x[v] = p.x;
+    y[v] = p.y;
+  }
+}
+
+void soa_changed(lms_mesh_s* m) {
+  m->aos_state = 0;
+  ++m->coord_gen;
+}
+
+void sync_soa(lms_mesh_s* m, cudaStream_t s) {
+  if (m->aos_state != 1) return;
+  k_aos_to_soa<<<gsz(m->V), 256, 0, s>>>(reinterpret_cast<const double2*>(m->xy[m->xy_cur].p), m->V, m->x[0].p,
+                                          m->x[1].p);
+  LMS_CHECK_LAUNCH();
+  m->aos_state = 2;
+}
+
+void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s) {
+  Schedule& S = m->sched;
+  const int64_t V = m->V;
+  if (m->dim == 2) {
+    // interleaved ping-pong pair; both copies carry the fixed vertices (the
+    // kernel never writes them), so they are refreshed from x[] whenever x[]
+    // was written outside a sweep
+    if (m->aos_state == 0) {
+      for (int i = 0; i < 2; ++i)
+        if (!m->xy[i].p || m->xy[i].n != (size_t)(2 * V)) m->xy[i].alloc(2 * V, s);
+      k_soa_to_aos<<<gsz(V), 256, 0, s>>>(m->x[0].p, m->x[1].p, V, reinterpret_cast<double2*>(m->xy[0].p),
+                                          reinterpret_cast<double2*>(m->xy[1].p));
+      LMS_CHECK_LAUNCH();
+      m->xy_cur = 0;
+      m->aos_state = 2;
+    }
+  } else if (m->alt_gen != m->coord_gen || !m->xalt[0].p) {
+    // X' holds the fixed vertices too (never written by the kernel): sync it
+    // whenever the coordinates were changed outside a sweep
+    for (int a = 0; a < m->dim; ++a) {
+      if (!m->xalt[a].p || m->xalt[a].n != (size_t)V) m->xalt[a].alloc(V, s);
+      LMS_TRY_CUDA(cudaMemcpyAsync(m->xalt[a].p, m->x[a].p, V * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    m->alt_gen = m->coord_gen;
+  }
+  int left = sweeps;
+  while (left > 0) {
+    const int r = left < S.gz_P ? left : S.gz_P;
+    const int j0 = S.gz_P - r;  // the last r sweeps of a P-sweep pass are an exact r-sweep pass
+    if (m->dim == 2) {
+      launch_gz_t<2, 8>(m, j0, s);
+      m->xy_cur = 1 - m->xy_cur;
+      m->aos_state = 1;
+    } else {
+      launch_gz_t<3, 16>(m, j0, s);
+      for (int a = 0; a < m->dim; ++a) std::swap(m->x[a], m->xalt[a]);
+    }
+    left -= r;
+  }
+}
+
+}  // namespace lms

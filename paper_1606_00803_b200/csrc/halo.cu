@@ -41,6 +41,7 @@ lms_status lms_smooth_colour(lms_mesh_t m, int32_t colour, lms_stream_t stream) 
     if (colour < 0 || colour >= m->C) fail(LMS_E_ARG, "colour out of range");
     if (m->n_free == 0) return LMS_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    sync_soa(m, s);
     if (!m->sched.valid) build_schedule(m, s);
     run_colour_stage(m, colour, s);
     return LMS_OK;
@@ -55,6 +56,7 @@ lms_status lms_gather_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, doub
     if (!m || (n > 0 && (!d_idx || !d_out)) || n < 0) fail(LMS_E_ARG, "bad argument");
     if (n == 0) return LMS_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    sync_soa(m, s);
     k_gather_coords<<<grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256), 256, 0, s>>>(
         m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_out);
     LMS_CHECK_LAUNCH();
@@ -71,9 +73,11 @@ lms_status lms_scatter_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, con
     if (!m || (n > 0 && (!d_idx || !d_in)) || n < 0) fail(LMS_E_ARG, "bad argument");
     if (n == 0) return LMS_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    sync_soa(m, s);
     k_scatter_coords<<<grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256), 256, 0, s>>>(
         m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_in);
     LMS_CHECK_LAUNCH();
+    soa_changed(m);
     return LMS_OK;
   } catch (const Err& e) {
     set_error(e.msg);

@@ -74,6 +74,25 @@ struct DBuf {
   T* get() const { return p; }
 };
 
+// ----------------------------------------------------------------- GZ kernel tables
+// per tile: record base, meta base (16-byte units), sizes (gz.cu)
+struct __align__(16) GzTile {
+  long long rec_base;
+  long long meta_base;
+  uint32_t meta16, rec16, n_items, n_slots;
+  uint32_t R, pad0, pad1, pad2;
+};
+// shared-memory plan of the GZ kernel (gz.cu plan_layout)
+struct GzLayout {
+  int NB = 0, NPW = 0, NW = 0;  // region buffers, producer warps, worker warps
+  int RR = 0, rec_bytes = 0, off_rec = 0;  // record ring: slots, bytes per slot, offset
+  int hdr_bytes = 0;            // per buffer header copy
+  int flag_off = 0, cnt_off = 0, coord_off = 0, buf_bytes = 0;  // inside a buffer
+  int stage_bytes = 0;          // producer staging (largest meta block)
+  int tiles_cap = 0;            // tiles per CTA (table size)
+  int off_tab = 0, off_stage = 0, off_ring = 0;  // region offsets
+};
+
 // ----------------------------------------------------------------- schedule
 // Sweep schedule: free vertices grouped into work items
 // (tile k, colour c), tile = T consecutive storage positions; inside an item
@@ -102,6 +121,27 @@ struct Schedule {
   DBuf<int32_t> slab;       // S3 slab: per chunk 32 vertex ids + W x 32 neighbour ids
   DBuf<int32_t> irec;       // [K*C*32] S3 128-byte item records (see smooth.cu)
   DBuf<unsigned long long> ticket;  // [1] S3 work counter
+  // GZ (ghost-zone tiled sweep, gz.cu): per tile a region = owned free vertices
+  // plus every vertex within C*P hops; a persistent kernel stages regions in
+  // shared memory and runs P whole sweeps there, reading X and writing the
+  // owned vertices to X'.
+  int gz_P = 0;             // sweeps per pass
+  int64_t gz_K = 0;         // tiles of the spatial tiling
+  int gz_T = 0;             // target owned vertices per tile
+  int gz_smem = 0;          // dynamic shared memory per CTA (bytes)
+  int gz_threads = 0;       // threads per CTA
+  GzLayout gz_L;            // shared-memory plan of the kernel
+  int64_t gz_nreg = 0;      // sum of region sizes
+  int64_t gz_nupd = 0;      // sum over tiles of first-sweep updates
+  int64_t gz_items = 0;     // work items (32 updates of one stage of one tile)
+  int64_t gz_bytes = 0;     // schedule bytes (records + meta)
+  int gz_max_reg = 0;       // largest region
+  int64_t gz_ntiles = 0;    // non-empty tiles
+  DBuf<int32_t> gz_tiles;   // [gz_ntiles] non-empty tile ids, ascending
+  DBuf<GzTile> gz_tab;      // [K] per-tile table
+  DBuf<int32_t> gz_item_sweep;  // [K*(P+1)] first item of each sweep, per tile
+  DBuf<uint4> gz_meta;      // per tile: header + region ids
+  DBuf<uint4> gz_rec;       // per item: rows, slots/flags/deps, ids, descriptor
   // S1 CUDA graphs: [0] one sweep, [1] eight sweeps (C kernel nodes per sweep)
   cudaGraphExec_t graphs[2] = {nullptr, nullptr};
   ~Schedule() {
@@ -120,6 +160,15 @@ struct lms_mesh_s {
   int device = 0;
   cudaStream_t s0 = nullptr;   // stream used for allocations
   lms::DBuf<double> x[3];
+  lms::DBuf<double> xalt[3];   // second coordinate buffer of the GZ sweep (ping-pong)
+  // 2D GZ sweeps run on interleaved (x, y) pairs: xy[xy_cur] is a double2[V]
+  // copy, xy[1 - xy_cur] its ping-pong partner.  aos_state says which copy
+  // is current: 0 = SoA x[] only, 1 = xy only (x[] stale), 2 = both.
+  lms::DBuf<double> xy[2];
+  int xy_cur = 0;
+  int aos_state = 0;
+  int64_t coord_gen = 1;       // bumped whenever x is (re)written outside a sweep
+  int64_t alt_gen = 0;         // coord_gen at which xalt's fixed vertices were synced
   lms::DBuf<uint8_t> fixed;
   lms::DBuf<int32_t> row_ptr, col;
   lms::DBuf<int8_t> colour;
@@ -155,6 +204,11 @@ void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s);
 void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s);
 void permute_mesh(lms_mesh_s* m, const int32_t* d_perm, cudaStream_t s);
 void build_schedule(lms_mesh_s* m, cudaStream_t s);
+int64_t spatial_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s);
+bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s);  // gz.cu
+void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s);                     // gz.cu
+void sync_soa(lms_mesh_s* m, cudaStream_t s);   // make x[] current (gz.cu)
+void soa_changed(lms_mesh_s* m);                // x[] was written outside a sweep
 void run_sweeps(lms_mesh_s* m, int sweeps, cudaStream_t s);
 void segmented_sort_rows(int32_t* d_col, const int32_t* d_row_ptr, int64_t V, int64_t nnz, cudaStream_t s);
 int64_t count_free(lms_mesh_s* m, cudaStream_t s);

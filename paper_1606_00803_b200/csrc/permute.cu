@@ -48,6 +48,7 @@ __global__ void k_remap(int32_t* __restrict__ a, int64_t n, const int32_t* __res
 }
 
 void permute_mesh(lms_mesh_s* m, const int32_t* d_perm, cudaStream_t s) {
+  sync_soa(m, s);
   const int64_t V = m->V, nnz = m->nnz;
   const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
   DBuf<int32_t> inv(V, s);
@@ -106,6 +107,7 @@ void permute_mesh(lms_mesh_s* m, const int32_t* d_perm, cudaStream_t s) {
     LMS_CHECK_LAUNCH();
   }
   m->sched.valid = false;
+  soa_changed(m);
 }
 
 }  // namespace lms

@@ -243,34 +243,14 @@ __global__ void k_item_records(const int32_t* __restrict__ item_ptr, const long 
   }
 }
 
-static int s3_ctas(int dev) {
-  int nsm = 0;
-  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  int per = 1;  // 1024-thread CTAs per SM (LMS_S3_CTAS_PER_SM overrides, for tuning)
-  if (const char* e = getenv("LMS_S3_CTAS_PER_SM")) per = atoi(e) > 0 ? atoi(e) : per;
-  return nsm * per;
-}
-
-void build_schedule(lms_mesh_s* m, cudaStream_t s) {
-  Schedule& S = m->sched;
-  S.valid = false;
-  for (int i = 0; i < 2; ++i)
-    if (S.graphs[i]) { cudaGraphExecDestroy(S.graphs[i]); S.graphs[i] = nullptr; }
+// Spatial tiling: tile = cell of a regular grid of bins over the bounding box
+// of the current coordinates, ~T vertices per cell, numbered row-major
+// (x fastest).  Returns the number of cells K.
+int64_t spatial_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) {
+  sync_soa(m, s);
   const int64_t V = m->V;
-  const int C = m->C > 0 ? m->C : 1;
-  const bool want_s3 = (m->sched_req == LMS_SCHED_S3 || m->sched_req == LMS_SCHED_AUTO);
-  // tiling: S3 defaults to spatial cells of ~4096 vertices; S1 to storage tiles
-  // of ~256*C vertices (one vertex per thread of a 256-thread CTA per item)
-  int tiling = m->tiling_req;
-  if (tiling == LMS_TILING_AUTO) tiling = want_s3 ? LMS_TILING_SPATIAL : LMS_TILING_STORAGE;
-  int T = m->tile_req;
-  if (T == 0) T = want_s3 ? 4096 : 256 * C;
-  if (T > V) T = (int)((V + 31) / 32 * 32);
-  if (T < 32) T = 32;
   const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
-  DBuf<int32_t> tile_of(V, s);
   int64_t K = 0;
-  if (tiling == LMS_TILING_SPATIAL) {
     double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     {
       DBuf<double> r(2, s);
@@ -304,8 +284,40 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
     K = (int64_t)nb[0] * nb[1] * nb[2];
     k_tile_spatial<<<Gv, 256, 0, s>>>(V, m->dim, m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, lo[0],
                                       lo[1], lo[2], nb[0] / w[0], nb[1] / w[1], nb[2] / w[2], nb[0], nb[1], nb[2],
-                                      tile_of.p);
+                                      tile_of);
     LMS_CHECK_LAUNCH();
+  return K;
+}
+
+static int s3_ctas(int dev) {
+  int nsm = 0;
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  int per = 1;  // 1024-thread CTAs per SM (LMS_S3_CTAS_PER_SM overrides, for tuning)
+  if (const char* e = getenv("LMS_S3_CTAS_PER_SM")) per = atoi(e) > 0 ? atoi(e) : per;
+  return nsm * per;
+}
+
+void build_schedule(lms_mesh_s* m, cudaStream_t s) {
+  Schedule& S = m->sched;
+  S.valid = false;
+  for (int i = 0; i < 2; ++i)
+    if (S.graphs[i]) { cudaGraphExecDestroy(S.graphs[i]); S.graphs[i] = nullptr; }
+  const int64_t V = m->V;
+  const int C = m->C > 0 ? m->C : 1;
+  const bool want_s3 = (m->sched_req == LMS_SCHED_S3 || (m->sched_req == LMS_SCHED_AUTO && !(m->dim == 2 && m->C <= 8)));
+  // tiling: S3 defaults to spatial cells of ~4096 vertices; S1 to storage tiles
+  // of ~256*C vertices (one vertex per thread of a 256-thread CTA per item)
+  int tiling = m->tiling_req;
+  if (tiling == LMS_TILING_AUTO) tiling = want_s3 ? LMS_TILING_SPATIAL : LMS_TILING_STORAGE;
+  int T = m->tile_req;
+  if (T == 0) T = want_s3 ? 4096 : 256 * C;
+  if (T > V) T = (int)((V + 31) / 32 * 32);
+  if (T < 32) T = 32;
+  const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
+  DBuf<int32_t> tile_of(V, s);
+  int64_t K = 0;
+  if (tiling == LMS_TILING_SPATIAL) {
+    K = spatial_tiles(m, T, tile_of.p, s);
   } else {
     K = (V + T - 1) / T;
     k_tile_storage<<<Gv, 256, 0, s>>>(V, T, tile_of.p);
@@ -454,6 +466,18 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   LMS_TRY_CUDA(cudaMemcpyAsync(&hr, reach.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   LMS_TRY_CUDA(cudaStreamSynchronize(s));
   S.max_reach = hr;
+  // GZ (gz.cu): the default for 2D meshes with few colours, where the
+  // C-hop ghost zone of a tile is a small fraction of it
+  if (m->sched_req == LMS_SCHED_GZ || (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->C <= 8)) {
+    const int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 900 : 512);
+    const int P = (m->sched_req == LMS_SCHED_GZ && m->lag_req > 0) ? m->lag_req : 1;
+    if (build_gz(m, Tg, P, m->sched_req == LMS_SCHED_GZ, s)) {
+      S.kind = LMS_SCHED_GZ;
+      S.lag = 0;
+      S.valid = true;
+      return;
+    }
+  }
   // resolve the kernel: S3 pays off when the tile graph is banded (small reach)
   int kind = m->sched_req;
   if (kind == LMS_SCHED_AUTO) kind = (K >= 16 && hr * 8 <= K) ? LMS_SCHED_S3 : LMS_SCHED_S1;
@@ -1356,6 +1380,8 @@ static cudaGraphExec_t get_graph(lms_mesh_s* m, int which) {
 // one colour stage with the S1 kernel (used by the multi-GPU sweep, which
 // exchanges halos between stages)
 void run_colour_stage(lms_mesh_s* m, int c, cudaStream_t s) {
+  sync_soa(m, s);
+  soa_changed(m);
   const unsigned G = (unsigned)(m->sched.K < 65535 * 16 ? m->sched.K : 65535 * 16);
   if (m->dim == 2)
     launch_s1_t<2, OPT_DEFAULT>(m, s, c, G);
@@ -1366,6 +1392,12 @@ void run_colour_stage(lms_mesh_s* m, int c, cudaStream_t s) {
 
 void run_sweeps(lms_mesh_s* m, int sweeps, cudaStream_t s) {
   Schedule& S = m->sched;
+  if (S.kind == LMS_SCHED_GZ) {
+    run_gz(m, sweeps, s);
+    return;
+  }
+  sync_soa(m, s);
+  soa_changed(m);  // S1/S3 update x[] in place
   if (S.kind == LMS_SCHED_S1) {
     int left = sweeps;
     while (left >= 8) {

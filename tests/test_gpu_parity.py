@@ -75,7 +75,9 @@ def test_bfs_other_seed(pair):
     assert np.array_equal(np_(gm.order("bfs", s)), oracle.order_bfs(om["row_ptr"], om["col"], s))
 
 
-@pytest.mark.parametrize("sched", [("s1", 0), ("s3", 0), ("s3", 64), ("s3", 96)])
+@pytest.mark.parametrize("sched", [("s1", 0, 0), ("s3", 0, 0), ("s3", 64, 0), ("s3", 96, 0),
+                                   ("gz", 0, 1), ("gz", 64, 1), ("gz", 200, 2), ("gz", 0, 3)],
+                         ids=lambda s: "%s-T%d-P%d" % s)
 def test_sweeps_bit_exact_all_orderings(pair, sched):
     m, om, gm0 = pair
     for kind in ["original", "random", "bfs", "rdr"]:
@@ -85,7 +87,7 @@ def test_sweeps_bit_exact_all_orderings(pair, sched):
         want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 7)
         with gpu_mesh(m) as gm:
             gm.permute(cuda(perm))
-            gm.set_schedule(sched[0], tile=sched[1])
+            gm.set_schedule(sched[0], tile=sched[1], lag=sched[2])
             gm.smooth(3)
             gm.smooth(4)
             got = gpu_coords(gm)
@@ -95,6 +97,38 @@ def test_sweeps_bit_exact_all_orderings(pair, sched):
             assert np.array_equal(rp, pm["row_ptr"]) and np.array_equal(col, pm["col"])
             assert np.array_equal(np_(gm.colour()), pm["colour"])
             assert np.array_equal(np_(gm.orig_id()), pm["orig_id"])
+
+
+def test_gz_coordinate_updates_between_calls(pair):
+    """GZ ping-pongs two coordinate buffers; coordinates imported between calls
+    (and odd sweep counts) must still give the sequential colour schedule."""
+    m, om, gm0 = pair
+    rng = np.random.default_rng(7)
+    with gpu_mesh(m) as gm:
+        gm.set_schedule("gz", tile=128, lag=2)
+        gm.smooth(1)
+        X = gpu_coords(gm)
+        # move the free vertices a little (fixed ones stay) and import
+        free = om["fixed"] == 0
+        X2 = [x.copy() for x in X]
+        for a in range(len(X2)):
+            X2[a][free] += rng.uniform(-1e-3, 1e-3, free.sum())
+        gm.import_coords([cuda(x) for x in X2])
+        gm.smooth(3)
+        want = oracle.smooth(X2, om["row_ptr"], om["col"], om["colour"], om["C"], 3)
+        assert bits_equal(gpu_coords(gm), want)
+        gm.smooth(2)
+        want = oracle.smooth(want, om["row_ptr"], om["col"], om["colour"], om["C"], 2)
+        assert bits_equal(gpu_coords(gm), want)
+        # switching kernels between calls continues from the current coordinates
+        gm.set_schedule("s1")
+        gm.smooth(2)
+        gm.set_schedule("gz", tile=96, lag=1)
+        gm.smooth(3)
+        gm.set_schedule("s3")
+        gm.smooth(1)
+        want = oracle.smooth(want, om["row_ptr"], om["col"], om["colour"], om["C"], 6)
+        assert bits_equal(gpu_coords(gm), want)
 
 
 def test_cross_ordering_tolerance(pair):
@@ -239,7 +273,7 @@ def test_C3_full_bfs_rdr():
 
 def test_C4_full_bench_config():
     """BASELINE.json configs[3] (the bench workload), original ordering, the
-    launch configuration bench.py times (AUTO -> S3), 3 sweeps bit-exact."""
+    launch configuration bench.py times (AUTO -> GZ), 3 sweeps bit-exact."""
     m = meshgen.make_config("C4")
     om = oracle.prepare(m)
     gm = gpu_mesh(m)
@@ -247,6 +281,7 @@ def test_C4_full_bench_config():
     assert np.array_equal(rp, om["row_ptr"]) and np.array_equal(col, om["col"])
     assert np.array_equal(np_(gm.colour()), om["colour"])
     gm.smooth(3)
+    assert gm.schedule_info()["kind"] == "gz"
     want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 3)
     assert bits_equal(gpu_coords(gm), want), gm.schedule_info()
     gm.close()
