@@ -274,19 +274,30 @@ def run_ours(args):
         t_ms = float(tt.item())
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kernel_ms = statistics.mean(step_ms)  # one sweep kernel launch (S3) / the graph of colour kernels (S1)
+    step_mean = statistics.mean(step_ms)
     value = vfree * sweeps * args.steps / (t_ms / 1e3) * world
     peak, peak_src = peaks()
-    achieved = bsw * sweeps / (kernel_ms / 1e3) / 1e9
-    kname = "k_sweep_s3" if sinfo["kind"] == "s3" else "k_sweep_s1"
+    # the dominant kernel and its launches per step: GZ = one launch per pass of
+    # P sweeps; S3 = one persistent launch per step; S1 = C launches per sweep
+    kind = sinfo["kind"]
+    if kind == "gz":
+        kname, per_launch_sweeps = "k_sweep_gz", max(1, sinfo["lag"])
+    elif kind == "s3":
+        kname, per_launch_sweeps = "k_sweep_s3", sweeps
+    else:
+        kname, per_launch_sweeps = "k_sweep_s1", 1
+    n_launch = max(1, -(-sweeps // per_launch_sweeps))
+    launch_ms = step_mean / n_launch
+    achieved = bsw * sweeps / (step_mean / 1e3) / 1e9  # = bytes per launch / launch time
     tr = load_traffic(args.config, args.ordering, kname)
     traffic = None
     if tr is not None and tr.get("sweeps"):
-        traffic = tr["dram_bytes"] / tr["sweeps"] * sweeps
+        traffic = tr["dram_bytes"] / tr["sweeps"] * per_launch_sweeps
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src, "kernel": kname,
-            "bytes_per_launch": bsw * sweeps, "launch_ms": kernel_ms,
-            "b_sweep": bsw, "frac_of_8TBs_nominal": achieved / 8000.0}
+            "bytes_per_launch": bsw * per_launch_sweeps, "launch_ms": launch_ms, "launches_per_step": n_launch,
+            "b_sweep": bsw, "frac_of_8TBs_nominal": achieved / 8000.0,
+            "traffic_source": tr.get("source") if tr else None}
 
     # ---------------- e2e: whole path from pinned host buffers, every step
     e2e = None

@@ -574,14 +574,87 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
   }
 }
 
+// Two updates per lane (2D): the lane's update of item A and of item B, with
+// all sixteen gathers issued before the two ordered sums (more loads in flight
+// per warp, two independent FP64 add chains per axis).
+template <int RMAX>
+__device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const GzRec<RMAX>& rb, bool vb, int R,
+                                           const uint4* __restrict__ rowgA, const uint4* __restrict__ rowgB,
+                                           double* sc, double2& oa, double2& ob) {
+  double2* s2 = reinterpret_cast<double2*>(sc);
+  uint16_t ua[RMAX], ub[RMAX];
+#pragma unroll
+  for (int p = 0; p < RMAX / 8; ++p) {
+    unpack8(ra.row[p], ua + 8 * p);
+    unpack8(rb.row[p], ub + 8 * p);
+  }
+#pragma unroll
+  for (int w = 0; w < RMAX; ++w) {
+    if (!va) ua[w] = GZ_PAD;
+    if (!vb) ub[w] = GZ_PAD;
+  }
+  double2 ga[RMAX], gb[RMAX];
+#pragma unroll
+  for (int w = 0; w < RMAX; ++w) {
+    ga[w] = (ua[w] != GZ_PAD) ? s2[ua[w]] : make_double2(0.0, 0.0);
+    gb[w] = (ub[w] != GZ_PAD) ? s2[ub[w]] : make_double2(0.0, 0.0);
+  }
+  double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+  int da = 0, db = 0;
+#pragma unroll
+  for (int w = 0; w < RMAX; ++w) {
+    if (ua[w] != GZ_PAD) {
+      if (w == 0) { ax = ga[w].x; ay = ga[w].y; }
+      else { ax = __dadd_rn(ax, ga[w].x); ay = __dadd_rn(ay, ga[w].y); }
+      ++da;
+    }
+    if (ub[w] != GZ_PAD) {
+      if (w == 0) { bx = gb[w].x; by = gb[w].y; }
+      else { bx = __dadd_rn(bx, gb[w].x); by = __dadd_rn(by, gb[w].y); }
+      ++db;
+    }
+  }
+  for (int p = RMAX / 8; p * 8 < R; ++p) {  // rows longer than RMAX: ordered tails
+    uint16_t t[8];
+    if (va) {
+      unpack8(rowgA[p], t);
+      for (int q = 0; q < 8 && t[q] != GZ_PAD; ++q) {
+        const double2 e = s2[t[q]];
+        ax = __dadd_rn(ax, e.x);
+        ay = __dadd_rn(ay, e.y);
+        ++da;
+      }
+    }
+    if (vb) {
+      unpack8(rowgB[p], t);
+      for (int q = 0; q < 8 && t[q] != GZ_PAD; ++q) {
+        const double2 e = s2[t[q]];
+        bx = __dadd_rn(bx, e.x);
+        by = __dadd_rn(by, e.y);
+        ++db;
+      }
+    }
+  }
+  if (va) {
+    const double dd = (double)da;
+    oa = make_double2(__ddiv_rn(ax, dd), __ddiv_rn(ay, dd));
+    s2[ra.pb & 0x7fffu] = oa;
+  }
+  if (vb) {
+    const double dd = (double)db;
+    ob = make_double2(__ddiv_rn(bx, dd), __ddiv_rn(by, dd));
+    s2[rb.pb & 0x7fffu] = ob;
+  }
+}
+
 // Shared-memory layout of k_sweep_gz: see GzLayout (lms_internal.cuh) and plan_layout.
 
 // Warp roles: warp 0 stages tile regions into the coordinate ring (TMA bulk
 // copies of id runs, or 16-byte cp.async gathers), warp 1 streams item
 // records into the record ring (one TMA bulk copy per record, in claim
 // order), warps 2.. are workers (one claimed item at a time).
-template <int DIM, int RMAX>
-__global__ void __launch_bounds__(DIM == 2 ? 640 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
+template <int DIM, int RMAX, bool PAIR>
+__global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
                                                                       const GzTile* __restrict__ tab,
                                                                       const int32_t* __restrict__ item_sweep,
                                                                       const uint4* __restrict__ meta,
@@ -610,6 +683,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 640 : 384, 1) k_sweep_gz(const int3
   int* t_R = t_rec16 + L.tiles_cap;
   int* t_item0 = t_R + L.tiles_cap;
   int* t_pre = t_item0 + L.tiles_cap;  // [n_my + 1]
+  int* t_buf = t_pre + L.tiles_cap + 1;  // buffer | (phase parity << 16) of the CTA's i-th tile
   unsigned char* stg = sm + L.off_stage;
   unsigned char* rring = sm + L.off_rec;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -647,6 +721,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 640 : 384, 1) k_sweep_gz(const int3
     const int a = item_sweep[k * (P + 1) + j0];
     t_item0[i] = a;
     t_pre[i + 1] = (int)t.n_items - a;
+    t_buf[i] = (i % NB) | (((i / NB) & 1) << 16);
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // prefix of the items this CTA runs, in tile order
@@ -727,8 +802,8 @@ __global__ void __launch_bounds__(DIM == 2 ? 640 : 384, 1) k_sweep_gz(const int3
       int ti = 0;
       const int nbat = (total + GZ_BS - 1) / GZ_BS;
       for (int g = 0; g < nbat; ++g) {
-        const int slot = g % RR;
-        if (g >= RR) mbar_wait(rempty + slot, ((uint32_t)(g / RR) & 1u) ^ 1u);
+        const int slot = g & (RR - 1);  // RR is a power of two
+        if (g >= RR) mbar_wait(rempty + slot, ((uint32_t)(g >> L.RR_log2) & 1u) ^ 1u);
         const int k0 = g * GZ_BS, k1 = min(total, k0 + GZ_BS);
         uint32_t bytes = 0;
         for (int kc = k0, tj = ti; kc < k1;) {  // pass 1: bytes of the batch
@@ -761,99 +836,141 @@ __global__ void __launch_bounds__(DIM == 2 ? 640 : 384, 1) k_sweep_gz(const int3
   if (warp >= 2 + L.NW) return;
   // ------------------------------------------------------------------- workers
   const unsigned FULL = 0xffffffffu;
-  int ti = 0;  // this warp's position in the tile list (claims are increasing)
+  // the current tile's parameters, refreshed when a claim crosses into the next tile
+  int ti = -1, pre_lo = 0, pre_hi = 0, item0 = 0, R = 8, rec16 = 0, tb = 0;
+  unsigned char* buf = nullptr;
+  auto enter_tile = [&](int kc) {
+    while (kc >= pre_hi) {
+      ++ti;
+      pre_lo = pre_hi;
+      pre_hi = t_pre[ti + 1];
+    }
+    item0 = t_item0[ti];
+    R = t_R[ti];
+    rec16 = t_rec16[ti];
+    tb = t_buf[ti];
+    buf = sm + L.off_ring + (size_t)(tb & 0xffff) * L.buf_bytes;
+  };
   unsigned long long w_wait = 0, w_dep = 0, w_comp = 0, w_items = 0;
-  for (;;) {
-    int kc = 0;
-    if (lane == 0) kc = atomicAdd(ctl, 1);
-    kc = __shfl_sync(FULL, kc, 0);
-    if (kc >= total) break;
-    while (kc >= t_pre[ti + 1]) ++ti;
-    const int i = ti;
-    const int t = t_item0[i] + (kc - t_pre[i]);
-    const int R = t_R[i];
-    const long long c0 = stats ? clock64() : 0;
-    // the item's record, from the record ring
-    const int bat = kc / GZ_BS;
-    const int slot = bat % RR;
-    if (lane == 0) mbar_wait(rfull + slot, (uint32_t)(bat / RR) & 1u);
+  bool tile_ready = false;
+  constexpr int G = (DIM == 2 && PAIR) ? 2 : 1;  // items claimed together (PAIR: two updates per lane)
+  auto load_rec = [&](int kc, GzRec<RMAX>& r) -> const unsigned char* {
+    const int bat = kc >> 3;
+    const int slot = bat & (RR - 1);
+    if (lane == 0) mbar_wait(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u);
     __syncwarp();
-    const unsigned char* rbase = rring + ((size_t)slot * GZ_BS + (kc - bat * GZ_BS)) * L.rec_bytes;
-    GzRec<RMAX> r;
-    {
-      const unsigned char* rb = rbase;
-      const uint4* rows = reinterpret_cast<const uint4*>(rb) + lane * (R >> 3);
+    const unsigned char* rbase = rring + ((size_t)slot * GZ_BS + (kc & 7)) * L.rec_bytes;
+    const uint4* rows = reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3);
 #pragma unroll
-      for (int p = 0; p < RMAX / 8; ++p) r.row[p] = (p * 8 < R) ? rows[p] : make_uint4(~0u, ~0u, ~0u, ~0u);
-      const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rb + 64 * R);
-      r.pb = pbs[lane];
-      r.gid = (int32_t)pbs[32 + lane];
-      r.desc = *reinterpret_cast<const uint4*>(rb + 64 * R + 256);
-      r.tile = i;
-      r.t = t;
-    }
-    const uint4* rowtail = reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3);
-    // the region of the item's tile
-    const int b = i % NB;
-    unsigned char* buf = sm + L.off_ring + (size_t)b * L.buf_bytes;
-    if (lane == 0) {
-      while (buf_tile[b] != i) __nanosleep(32);
-      mbar_wait(full + b, (uint32_t)(i / NB) & 1u);
-    }
-    __syncwarp();
-    const long long c1 = stats ? clock64() : 0;
-    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(buf);
+    for (int p = 0; p < RMAX / 8; ++p) r.row[p] = (p * 8 < R) ? rows[p] : make_uint4(~0u, ~0u, ~0u, ~0u);
+    const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rbase + 64 * R);
+    r.pb = pbs[lane];
+    r.gid = (int32_t)pbs[32 + lane];
+    r.desc = *reinterpret_cast<const uint4*>(rbase + 64 * R + 256);
+    return rbase;
+  };
+  auto wait_deps = [&](const GzRec<RMAX>& r, int i) {
     volatile int* flags = reinterpret_cast<volatile int*>(buf + L.flag_off);
-    int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
-    const int n = (int)(r.desc.x & 0xffu);
-    const int j = (int)((r.desc.x >> 8) & 0xffu);
     const int sg = (int)(r.desc.x >> 16);
-    const int item0 = t_item0[i];
-    // this item's dependencies
     if (r.desc.y == 0) {
       const int dep = (int)(r.pb >> 16);
       if (dep != 0xffff && dep >= item0)
         while (flags[dep] != i + 1) __nanosleep(20);
     } else if (lane == 0) {
+      const uint32_t* hdr = reinterpret_cast<const uint32_t*>(buf);
+      int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
       const int s0 = max(sg - C, j0 * C);
       for (int s2 = s0; s2 < sg; ++s2) {
         const int need = (int)(hdr[4 + s2 + 1] - hdr[4 + s2]);
         while (*(volatile int*)(cnt + s2) != need) __nanosleep(20);
       }
     }
-    __syncwarp();
-    __threadfence_block();
-    const long long c2 = stats ? clock64() : 0;
-    if (lane < n) {
-      const int nr4 = (int)r4(hdr[1]);
-      double* sc = reinterpret_cast<double*>(buf + L.coord_off);
-      double ox, oy, oz;
-      gz_update<DIM, RMAX>(r, R, rowtail, sc, nr4, ox, oy, oz);
-      if (j == P - 1 && (r.pb & 0x8000u)) {  // owned vertex, final value of the pass
-        if (DIM == 2) {
-          a1[r.gid] = make_double2(ox, oy);
-        } else {
-          x1[r.gid] = ox;
-          y1[r.gid] = oy;
-          z1[r.gid] = oz;
-        }
+  };
+  auto store_owned = [&](const GzRec<RMAX>& r, double ox, double oy, double oz) {
+    if ((int)((r.desc.x >> 8) & 0xffu) == P - 1 && (r.pb & 0x8000u)) {  // owned vertex, final value of the pass
+      if (DIM == 2) {
+        a1[r.gid] = make_double2(ox, oy);
+      } else {
+        x1[r.gid] = ox;
+        y1[r.gid] = oy;
+        z1[r.gid] = oz;
       }
     }
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(rempty + slot);  // one of the batch's records consumed (rows > RMAX were read in gz_update)
+  };
+  auto finish = [&](const GzRec<RMAX>& r, int kc, int t, int i) {  // lane 0, after __syncwarp
+    volatile int* flags = reinterpret_cast<volatile int*>(buf + L.flag_off);
+    int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
+    mbar_arrive(rempty + ((kc >> 3) & (RR - 1)));  // one of the batch's records consumed
+    __threadfence_block();
+    flags[t] = i + 1;
+    atomicAdd(cnt + (int)(r.desc.x >> 16), 1);
+    if (atomicAdd(ndone + (tb & 0xffff), 1) == pre_hi - pre_lo - 1) mbar_arrive(empty + (tb & 0xffff));
+  };
+  for (;;) {
+    int kc0 = 0;
+    if (lane == 0) kc0 = atomicAdd(ctl, G);
+    kc0 = __shfl_sync(FULL, kc0, 0);
+    if (kc0 >= total) break;
+    const int nclaim = min(G, total - kc0);
+    for (int q = 0; q < nclaim;) {
+      const int kc = kc0 + q;
+      if (kc >= pre_hi) {
+        enter_tile(kc);
+        tile_ready = false;
+      }
+      const int i = ti;
+      const long long c0 = stats ? clock64() : 0;
+      GzRec<RMAX> ra, rb;
+      const unsigned char* basea = load_rec(kc, ra);
+      const int ta = item0 + (kc - pre_lo);
+      // pair with the next claimed item if it is in the same tile and does not wait for this one
+      bool pair = false;
+      const unsigned char* baseb = basea;
+      if (G == 2 && q + 1 < nclaim && kc + 1 < pre_hi) {
+        baseb = load_rec(kc + 1, rb);
+        pair = rb.desc.y == 0 && !__any_sync(FULL, (int)(rb.pb >> 16) == ta);
+      }
+      if (lane == 0 && !tile_ready) {  // the region of the item's tile
+        while (buf_tile[tb & 0xffff] != i) __nanosleep(32);
+        mbar_wait(full + (tb & 0xffff), (uint32_t)(tb >> 16));
+      }
+      tile_ready = true;
+      __syncwarp();
+      const long long c1 = stats ? clock64() : 0;
+      wait_deps(ra, i);
+      if (pair) wait_deps(rb, i);
+      __syncwarp();
       __threadfence_block();
-      flags[t] = i + 1;
-      atomicAdd(cnt + sg, 1);
-      const int n_eff = t_pre[i + 1] - t_pre[i];
-      if (atomicAdd(ndone + b, 1) == n_eff - 1) mbar_arrive(empty + b);
-    }
-    if (stats) {
-      const long long c3 = clock64();
-      w_wait += c1 - c0;
-      w_dep += c2 - c1;
-      w_comp += c3 - c2;
-      w_items += 1;
+      const long long c2 = stats ? clock64() : 0;
+      double* sc = reinterpret_cast<double*>(buf + L.coord_off);
+      const int na = (int)(ra.desc.x & 0xffu);
+      if (DIM == 2 && pair) {
+        const int nb = (int)(rb.desc.x & 0xffu);
+        double2 oa, ob;
+        gz_update2<RMAX>(ra, lane < na, rb, lane < nb, R,
+                         reinterpret_cast<const uint4*>(basea) + lane * (R >> 3),
+                         reinterpret_cast<const uint4*>(baseb) + lane * (R >> 3), sc, oa, ob);
+        if (lane < na) store_owned(ra, oa.x, oa.y, 0.0);
+        if (lane < nb) store_owned(rb, ob.x, ob.y, 0.0);
+      } else if (lane < na) {
+        const int nr4 = DIM == 3 ? (int)r4(reinterpret_cast<const uint32_t*>(buf)[1]) : 0;
+        double ox, oy, oz;
+        gz_update<DIM, RMAX>(ra, R, reinterpret_cast<const uint4*>(basea) + lane * (R >> 3), sc, nr4, ox, oy, oz);
+        store_owned(ra, ox, oy, oz);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        finish(ra, kc, ta, i);
+        if (pair) finish(rb, kc + 1, ta + 1, i);
+      }
+      q += pair ? 2 : 1;
+      if (stats) {
+        const long long c3 = clock64();
+        w_wait += c1 - c0;
+        w_dep += c2 - c1;
+        w_comp += c3 - c2;
+        w_items += pair ? 2 : 1;
+      }
     }
   }
   if (stats && lane == 0) {
@@ -1181,7 +1298,10 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int cap, in
   L->NW = nw;
   // record ring: RR batches of GZ_BS records; RR * GZ_BS - GZ_BS >= workers keeps
   // every mbarrier phase unambiguous (a claim is never a full ring ahead)
-  L->RR = std::max(8, (nw + GZ_BS - 1) / GZ_BS + 2);
+  L->RR = 8;
+  while (L->RR * GZ_BS - GZ_BS < nw + GZ_BS) L->RR *= 2;  // a power of two
+  L->RR_log2 = 0;
+  while ((1 << L->RR_log2) < L->RR) ++L->RR_log2;
   L->rec_bytes = gz_rec16(nd.max_row > 0 ? (int)((nd.max_row + 7) & ~7) : 8) * 16;
   const int HW = gz_hdr_words(C, P);
   L->hdr_bytes = r16i(4 * (int64_t)HW);
@@ -1196,7 +1316,7 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int cap, in
     L->NB = nb;
     const int ctl = (2 * nb + 2 * L->RR + 1) * 8 + (1 + 2 * nb) * 4;
     L->off_tab = r16i(ctl);
-    const int tab_bytes = r16i((int64_t)tiles_cap * (8 + 4 + 4 + 4) + 4 * ((int64_t)tiles_cap + 1));
+    const int tab_bytes = r16i((int64_t)tiles_cap * (8 + 4 + 4 + 4 + 4) + 4 * ((int64_t)tiles_cap + 1));
     L->off_stage = L->off_tab + tab_bytes;
     L->off_rec = L->off_stage + L->stage_bytes;
     L->off_ring = (L->off_rec + L->RR * GZ_BS * L->rec_bytes + 127) & ~127;
@@ -1216,8 +1336,10 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   int cap = 0, nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
-  const int maxw = (m->dim == 2 ? 640 : 384) / 32;  // the kernel's launch bounds
-  const int nw = env_int("LMS_GZ_WORKERS", maxw - 2, 1, maxw - 2);  // + region producer + record loader
+  const int maxw = (m->dim == 2 ? 1024 : 384) / 32;  // the kernel's launch bounds
+  // 18 workers measured best on C4 (more warps only lengthen every item: the
+  // shared-memory pipe is the shared resource); + region producer + record loader
+  const int nw = env_int("LMS_GZ_WORKERS", std::min(maxw - 2, m->dim == 2 ? 18 : 10), 1, maxw - 2);
   const int want_nb = env_int("LMS_GZ_BUFFERS", 0, 0, 8);
   const int dim = m->dim, C = m->C;
   GzNeeds nd;
@@ -1252,10 +1374,10 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   return false;
 }
 
-template <int DIM, int RMAX>
+template <int DIM, int RMAX, bool PAIR>
 static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
   Schedule& S = m->sched;
-  auto kern = k_sweep_gz<DIM, RMAX>;
+  auto kern = k_sweep_gz<DIM, RMAX, PAIR>;
   LMS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S.gz_smem));
   int nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
@@ -1345,11 +1467,14 @@ void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s) {
     const int r = left < S.gz_P ? left : S.gz_P;
     const int j0 = S.gz_P - r;  // the last r sweeps of a P-sweep pass are an exact r-sweep pass
     if (m->dim == 2) {
-      launch_gz_t<2, 8>(m, j0, s);
+      if (getenv("LMS_GZ_PAIR"))  // tuning: two items per warp
+        launch_gz_t<2, 8, true>(m, j0, s);
+      else
+        launch_gz_t<2, 8, false>(m, j0, s);
       m->xy_cur = 1 - m->xy_cur;
       m->aos_state = 1;
     } else {
-      launch_gz_t<3, 16>(m, j0, s);
+      launch_gz_t<3, 16, false>(m, j0, s);
       for (int a = 0; a < m->dim; ++a) std::swap(m->x[a], m->xalt[a]);
     }
     left -= r;

@@ -85,7 +85,7 @@ struct __align__(16) GzTile {
 // shared-memory plan of the GZ kernel (gz.cu plan_layout)
 struct GzLayout {
   int NB = 0, NPW = 0, NW = 0;  // region buffers, producer warps, worker warps
-  int RR = 0, rec_bytes = 0, off_rec = 0;  // record ring: slots, bytes per slot, offset
+  int RR = 0, RR_log2 = 0, rec_bytes = 0, off_rec = 0;  // record ring: batches (power of 2), bytes per record
   int hdr_bytes = 0;            // per buffer header copy
   int flag_off = 0, cnt_off = 0, coord_off = 0, buf_bytes = 0;  // inside a buffer
   int stage_bytes = 0;          // producer staging (largest meta block)

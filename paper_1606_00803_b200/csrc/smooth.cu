@@ -469,7 +469,7 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   // GZ (gz.cu): the default for 2D meshes with few colours, where the
   // C-hop ghost zone of a tile is a small fraction of it
   if (m->sched_req == LMS_SCHED_GZ || (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->C <= 8)) {
-    const int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 900 : 512);
+    const int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 3600 : 512);
     const int P = (m->sched_req == LMS_SCHED_GZ && m->lag_req > 0) ? m->lag_req : 1;
     if (build_gz(m, Tg, P, m->sched_req == LMS_SCHED_GZ, s)) {
       S.kind = LMS_SCHED_GZ;

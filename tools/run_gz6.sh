@@ -1,10 +1,10 @@
 #!/bin/bash
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gz or C4" > gpurun_out/gz9_tests.log 2>&1
-echo rc=$? >> gpurun_out/gz9_tests.log
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gz or C4" > gpurun_out/gz12_tests.log 2>&1
+echo rc=$? >> gpurun_out/gz12_tests.log
 export LMS_GZ_VERBOSE=1
-for w in 18 12; do
+for w in 18 14; do
   LMS_GZ_WORKERS=$w timeout 300 python tools/explore.py --config C4 --sweeps 12 --reps 2 \
-    --variants gz:1600:1,gz:2500:1,gz:3600:1,gz:900:1 > gpurun_out/gz9_explore_$w.log 2>&1
+    --variants gz:1600:1,gz:2500:1,gz:3600:1,gz:4500:1 > gpurun_out/gz12_explore_$w.log 2>&1
 done
-LMS_GZ_STATS=1 timeout 300 python tools/explore.py --config C4 --sweeps 2 --reps 1 --variants gz:2500:1 > gpurun_out/gz9_stats.log 2>&1
+LMS_GZ_STATS=1 timeout 300 python tools/explore.py --config C4 --sweeps 2 --reps 1 --variants gz:3600:1 > gpurun_out/gz12_stats.log 2>&1
 echo done
