@@ -322,6 +322,30 @@ def run_ours(args):
             torch.cuda.synchronize()
             g.close()
         e2e_step()
+        # phase breakdown of one more e2e step (CUDA events; informational)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+        evs[0].record(stream)
+        dc = [t.to(dev, non_blocking=True) for t in hc]
+        de = he.to(dev, non_blocking=True)
+        evs[1].record(stream)
+        g = lms.Mesh.build_csr(dc, de)
+        evs[2].record(stream)
+        p = g.order(args.ordering, meshgen.RANDOM_ORDER_SEED if args.ordering == "random" else 0)
+        g.permute(p)
+        evs[3].record(stream)
+        g.set_schedule(args.schedule, args.tile, args.lag)
+        g.smooth(1)
+        evs[4].record(stream)
+        g.smooth(sweeps - 1)
+        evs[5].record(stream)
+        out = g.coords()
+        for o, h in zip(out, hout):
+            h.copy_(o, non_blocking=True)
+        evs[6].record(stream)
+        torch.cuda.synchronize()
+        g.close()
+        names = ["h2d", "build_csr+colour", "order+permute", "schedule+1sweep", "sweeps", "d2h"]
+        e2e_phases = {nm: evs[i].elapsed_time(evs[i + 1]) for i, nm in enumerate(names)}
         n_e2e = max(1, min(args.steps, 3))
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
@@ -333,7 +357,7 @@ def run_ours(args):
         e_ms = a.elapsed_time(b) / n_e2e
         e2e = {"value": vfree * sweeps / (e_ms / 1e3) * world, "unit": "vertex-updates/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
-               "steps": n_e2e,
+               "steps": n_e2e, "phases_ms": e2e_phases,
                "path": "H2D coords+elems -> build_csr -> order -> permute -> smooth(%d) -> D2H coords" % sweeps}
 
     cpu = None

@@ -71,12 +71,30 @@ static void check_coords(int dim, const double* const* d) {
     if (!d[a]) fail(LMS_E_ARG, "coordinate pointer is NULL");
 }
 
+// The library allocates stream-ordered (cudaMallocAsync) and synchronises
+// between build phases; with the default release threshold of 0 every sync
+// hands the freed pool memory back to the driver, so the next large
+// allocation maps pages again.  Keep up to LMS_POOL_KEEP_GB (default 64 GB,
+// of 180 GB) reserved in the device's default pool.
+static void keep_pool_memory(int dev) {
+  static int done_for = -1;
+  if (done_for == dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+  double gb = 64.0;
+  if (const char* e = getenv("LMS_POOL_KEEP_GB")) gb = atof(e);
+  uint64_t keep = (uint64_t)(gb * 1073741824.0);
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  done_for = dev;
+}
+
 static lms_mesh_s* new_mesh(int dim, int64_t V, cudaStream_t s) {
   auto* m = new lms_mesh_s();
   m->dim = dim;
   m->V = V;
   m->s0 = s;
   LMS_TRY_CUDA(cudaGetDevice(&m->device));
+  keep_pool_memory(m->device);
   m->err.alloc(1, s);
   LMS_TRY_CUDA(cudaMemsetAsync(m->err.p, 0, sizeof(int), s));
   return m;

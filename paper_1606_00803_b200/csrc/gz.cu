@@ -57,6 +57,7 @@
 #include <cub/device/device_select.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
@@ -1068,6 +1069,16 @@ struct GzNeeds {
 // tile, `fits`: the shared-memory plan) are not met.
 template <typename Fits>
 static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* out, Fits fits) {
+  // LMS_GZ_VERBOSE=2: host-side phase timings (synchronising)
+  const bool tv = getenv("LMS_GZ_VERBOSE") && atoi(getenv("LMS_GZ_VERBOSE")) >= 2;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!tv) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[gz build] %-18s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
 
   Schedule& S = m->sched;
   const int64_t V = m->V;
@@ -1078,6 +1089,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   const int kbits = bits_for(K + 1);
   const int end_bit = 32 + kbits;
 
+  mark("tiling");
   // level 0: the owned free vertices of every tile, sorted by (tile, id)
   std::vector<DBuf<uint64_t>> lev(D);
   std::vector<int64_t> nlev(D, 0);
@@ -1096,6 +1108,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
     }
   }
   nlev[0] = m->n_free;
+  mark("level0");
   // levels 1..D-1: breadth-first rings through free vertices, per tile
   for (int L = 1; L < D; ++L) {
     DBuf<uint64_t> cand;
@@ -1119,6 +1132,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
     }
     nlev[L] = read_i64(nsel.p, false, s);
   }
+  mark("levels");
   // update set U: free entries with L + colour <= D - 1
   int64_t ntot = 0;
   for (int L = 0; L < D; ++L) ntot += nlev[L];
@@ -1134,6 +1148,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
     }
   const int64_t nU = read_i64(nu.p, true, s);
   for (int L = 1; L < D; ++L) lev[L].release();
+  mark("update set");
   // region = U and its neighbours, sorted by (tile, id)
   DBuf<uint64_t> reg;
   int64_t nreg_all = expand(ukey, nU, m, 1, reg, s);
@@ -1145,6 +1160,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   DBuf<int64_t> own_off(K + 1, s);
   k_gz_tile_off<<<gsz(K + 1), 256, 0, s>>>(lev[0].p, nlev[0], K, own_off.p);
   LMS_CHECK_LAUNCH();
+  mark("region");
   // updates sorted by (tile, colour, sweeps needed desc, local index)
   DBuf<uint64_t> ck(nU > 0 ? nU : 1, s), ck2(nU > 0 ? nU : 1, s);
   DBuf<int32_t> cv(nU > 0 ? nU : 1, s), cv2(nU > 0 ? nU : 1, s);
@@ -1166,6 +1182,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   LMS_CHECK_LAUNCH();
   nch.release();
   own_off.release();
+  mark("update sort");
   // items: per (tile, stage) ceil(updates / 32), tile-major then stage-major
   const int64_t nks = K * PC;
   DBuf<int64_t> ns(nks > 0 ? nks : 1, s), sfirst(nks + 1, s);
@@ -1184,6 +1201,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
     k_gzd_tile_r<<<gsz(nU), 256, 0, s>>>(ck2.p, cv2.p, nU, m->row_ptr.p, tR.p);
     LMS_CHECK_LAUNCH();
   }
+  mark("items");
   // runs of consecutive ids in each region: rs = exclusive scan of run starts
   DBuf<int64_t> rs(nreg_all + 1, s);
   {
@@ -1228,6 +1246,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   out->max_row = mx[3];
   if (mx[0] > GZ_MAX_REGION || mx[1] > 65534) return false;
   if (!fits(*out)) return false;
+  mark("sizes");
   // the blobs
   DBuf<GzTile> tab(K > 0 ? K : 1, s);
   DBuf<int32_t> item_sweep(K * (P + 1) > 0 ? K * (P + 1) : 1, s);
@@ -1249,6 +1268,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
     k_gzd_deps<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, tab.p, sfirst.p, it_lo.p, it_hi.p, rec.p);
     LMS_CHECK_LAUNCH();
   }
+  mark("records+deps");
   // the non-empty tiles, in tile order
   DBuf<int32_t> tiles(K > 0 ? K : 1, s);
   int64_t nt = 0;
@@ -1265,6 +1285,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
     nt = read_i64(nsel.p, false, s);
     tiles = std::move(o);
   }
+  mark("tile list");
   S.gz_tiles = std::move(tiles);
   S.gz_ntiles = nt;
   S.gz_tab = std::move(tab);

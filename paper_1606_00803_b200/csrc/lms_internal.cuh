@@ -100,6 +100,7 @@ struct GzLayout {
 // ("colour-sliced CSR"), so each item streams its own rows contiguously.
 struct Schedule {
   bool valid = false;
+  bool base_valid = false;  // S1/S3 lists built (GZ builds them only on demand)
   int kind = 0;          // LMS_SCHED_S1 or LMS_SCHED_S3 (resolved)
   int tile = 0;          // T
   int lag = 0;           // S3 tile lag L

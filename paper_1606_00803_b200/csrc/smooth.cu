@@ -297,14 +297,16 @@ static int s3_ctas(int dev) {
   return nsm * per;
 }
 
-void build_schedule(lms_mesh_s* m, cudaStream_t s) {
+// The S1/S3 schedule (item lists, slab, dependency records).  With gz_base the
+// kernel choice stays GZ and only the S1 lists that lms_smooth_colour uses are
+// (re)built.
+static void build_base(lms_mesh_s* m, cudaStream_t s, bool gz_base) {
   Schedule& S = m->sched;
-  S.valid = false;
   for (int i = 0; i < 2; ++i)
     if (S.graphs[i]) { cudaGraphExecDestroy(S.graphs[i]); S.graphs[i] = nullptr; }
   const int64_t V = m->V;
   const int C = m->C > 0 ? m->C : 1;
-  const bool want_s3 = (m->sched_req == LMS_SCHED_S3 || (m->sched_req == LMS_SCHED_AUTO && !(m->dim == 2 && m->C <= 8)));
+  const bool want_s3 = !gz_base && (m->sched_req == LMS_SCHED_S3 || m->sched_req == LMS_SCHED_AUTO);
   // tiling: S3 defaults to spatial cells of ~4096 vertices; S1 to storage tiles
   // of ~256*C vertices (one vertex per thread of a 256-thread CTA per item)
   int tiling = m->tiling_req;
@@ -466,18 +468,8 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   LMS_TRY_CUDA(cudaMemcpyAsync(&hr, reach.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   LMS_TRY_CUDA(cudaStreamSynchronize(s));
   S.max_reach = hr;
-  // GZ (gz.cu): the default for 2D meshes with few colours, where the
-  // C-hop ghost zone of a tile is a small fraction of it
-  if (m->sched_req == LMS_SCHED_GZ || (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->C <= 8)) {
-    const int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 3600 : 512);
-    const int P = (m->sched_req == LMS_SCHED_GZ && m->lag_req > 0) ? m->lag_req : 1;
-    if (build_gz(m, Tg, P, m->sched_req == LMS_SCHED_GZ, s)) {
-      S.kind = LMS_SCHED_GZ;
-      S.lag = 0;
-      S.valid = true;
-      return;
-    }
-  }
+  S.base_valid = true;
+  if (gz_base) return;
   // resolve the kernel: S3 pays off when the tile graph is banded (small reach)
   int kind = m->sched_req;
   if (kind == LMS_SCHED_AUTO) kind = (K >= 16 && hr * 8 <= K) ? LMS_SCHED_S3 : LMS_SCHED_S1;
@@ -493,6 +485,25 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
     S.lag = 0;
   }
   S.valid = true;
+}
+
+void build_schedule(lms_mesh_s* m, cudaStream_t s) {
+  Schedule& S = m->sched;
+  S.valid = false;
+  S.base_valid = false;
+  // GZ (gz.cu): the default for 2D meshes with few colours, where the
+  // C-hop ghost zone of a tile is a small fraction of it
+  if (m->sched_req == LMS_SCHED_GZ || (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->C <= 8)) {
+    const int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 3600 : 512);
+    const int P = (m->sched_req == LMS_SCHED_GZ && m->lag_req > 0) ? m->lag_req : 1;
+    if (build_gz(m, Tg, P, m->sched_req == LMS_SCHED_GZ, s)) {
+      S.kind = LMS_SCHED_GZ;
+      S.lag = 0;
+      S.valid = true;
+      return;
+    }
+  }
+  build_base(m, s, false);
 }
 
 // ---------------------------------------------------------------- sweep kernels
@@ -1381,6 +1392,7 @@ static cudaGraphExec_t get_graph(lms_mesh_s* m, int which) {
 // exchanges halos between stages)
 void run_colour_stage(lms_mesh_s* m, int c, cudaStream_t s) {
   sync_soa(m, s);
+  if (!m->sched.base_valid) build_base(m, s, true);  // GZ schedules skip the S1 lists
   soa_changed(m);
   const unsigned G = (unsigned)(m->sched.K < 65535 * 16 ? m->sched.K : 65535 * 16);
   if (m->dim == 2)
