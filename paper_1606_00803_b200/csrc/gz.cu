@@ -46,7 +46,10 @@
 //   record blob, per item (rec16 * 16 bytes, R = the tile's longest row
 //   rounded up to 8):
 //       u16 rows[32][R]   lane l's neighbour slots in CSR order (0xFFFF pad)
-//       u32 pb[32]        slot of lane l's vertex | owned << 15 | dep_l << 16
+//       u32 pb[32]        slot of lane l's vertex (0x7FFF: empty lane) | owned << 15
+//                         | dep_l << 16.  The item's updates are placed on lanes
+//                         by a greedy bank-aware assignment to quarter-warps
+//                         (2D), which cuts shared-memory bank conflicts
 //                         (dep_l: l-th item this one waits for, 0xFFFF none)
 //       i32 gid[32]       global id of lane l's vertex
 //       u32 desc[4]       {n | sweep << 8 | stage << 16, mode, n_deps, 0};
@@ -317,13 +320,16 @@ __global__ void k_gzd_region(const uint64_t* __restrict__ reg, int64_t n, int C,
 
 // one warp per item: the record (rows, slots + owned flags, ids, descriptor)
 // and the item's touched slot interval [lo, hi]
-__global__ void k_gzd_records(const int32_t* __restrict__ it_ks, const int32_t* __restrict__ it_q, int64_t NI,
+__global__ void __launch_bounds__(256) k_gzd_records(const int32_t* __restrict__ it_ks,
+                                                     const int32_t* __restrict__ it_q, int64_t NI,
                               int C, int P, const int64_t* __restrict__ kc_off, const int32_t* __restrict__ cntj,
                               const uint64_t* __restrict__ ck, const int32_t* __restrict__ cv,
                               const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
                               const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                               const int32_t* __restrict__ tile_of, const uint64_t* __restrict__ reg,
                               const int64_t* __restrict__ reg_off, uint4* rec, int32_t* it_lo, int32_t* it_hi) {
+  __shared__ uint8_t gz_banks[8 * 32 * 9];
+  __shared__ uint8_t gz_pos[8 * 32];
   const int lane = threadIdx.x & 31;
   const int PC = P * C;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -346,10 +352,11 @@ __global__ void k_gzd_records(const int32_t* __restrict__ it_ks, const int32_t* 
     int32_t* gid = reinterpret_cast<int32_t*>(base + 64 * R + 128);
     uint32_t* desc = reinterpret_cast<uint32_t*>(base + 64 * R + 256);
     int lo = 0x7fffffff, hi = -1;
-    uint32_t p = 0xffff0000u | 0x7fffu;
+    uint32_t p = 0xffff0000u | 0x7fffu;  // slot 0x7fff = empty lane
     int32_t g = -1;
     const uint64_t kh = (uint64_t)k << 32;
     const int64_t ra = reg_off[k], rb = reg_off[k + 1];
+    int d = 0;
     if (lane < n) {
       const int64_t u = kc_off[kc] + 32 * q + lane;
       const int32_t v = cv[u];
@@ -357,7 +364,61 @@ __global__ void k_gzd_records(const int32_t* __restrict__ it_ks, const int32_t* 
       g = v;
       p = 0xffff0000u | (uint32_t)lv | (tile_of[v] == (int32_t)k ? 0x8000u : 0u);
       lo = hi = lv;
-      const int32_t b = rp[v], d = rp[v + 1] - b;
+      const int32_t b = rp[v];
+      d = rp[v + 1] - b;
+    }
+    // lane position in the record: 2D rows of 8 get a greedy bank-aware
+    // assignment to quarter-warps (the 16-byte shared-memory gathers and the
+    // result store are processed 8 lanes at a time; lanes of one quarter that
+    // hit the same bank group serialise), everything else keeps its lane
+    int pos = lane;
+    if (R == 8) {
+      uint8_t* bk = gz_banks + (threadIdx.x >> 5) * 32 * 9;
+      for (int w = 0; w < 9; ++w) bk[lane * 9 + w] = 0xff;
+      if (lane < n) {
+        bk[lane * 9] = (uint8_t)((p & 0x7fffu) & 7u);
+        const int32_t b = rp[g];
+        for (int w = 0; w < d && w < 8; ++w) {
+          const int sl = (int)(lower_bound_u64(reg, ra, rb, kh | (uint32_t)col[b + w]) - ra);
+          bk[lane * 9 + 1 + w] = (uint8_t)(sl & 7);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        uint8_t qm[4][9];
+        int qn[4] = {0, 0, 0, 0};
+        for (int a = 0; a < 4; ++a)
+          for (int w = 0; w < 9; ++w) qm[a][w] = 0;
+        int posv[32];
+        for (int dd = 9; dd >= 0; --dd)  // most neighbours first; empty lanes (9 x 0xff) last
+          for (int l = 0; l < 32; ++l) {
+            int cntl = 0;
+            for (int w = 0; w < 9; ++w) cntl += bk[l * 9 + w] != 0xff;
+            if (cntl != dd) continue;
+            int best = -1, bp = 1 << 30;
+            for (int a = 0; a < 4; ++a) {
+              if (qn[a] >= 8) continue;
+              int pen = 0;
+              for (int w = 0; w < 9; ++w) {
+                const int bb = bk[l * 9 + w];
+                if (bb != 0xff) pen += (qm[a][w] >> bb) & 1;
+              }
+              if (pen < bp) { bp = pen; best = a; }
+            }
+            posv[l] = 8 * best + qn[best]++;
+            for (int w = 0; w < 9; ++w) {
+              const int bb = bk[l * 9 + w];
+              if (bb != 0xff) qm[best][w] |= (uint8_t)(1u << bb);
+            }
+          }
+        for (int l = 0; l < 32; ++l) gz_pos[(threadIdx.x >> 5) * 32 + l] = (uint8_t)posv[l];
+      }
+      __syncwarp();
+      pos = gz_pos[(threadIdx.x >> 5) * 32 + lane];
+      __syncwarp();
+    }
+    if (lane < n) {
+      const int32_t b = rp[g];
       for (int w = 0; w < R; ++w) {
         uint16_t li = GZ_PAD;
         if (w < d) {
@@ -366,13 +427,13 @@ __global__ void k_gzd_records(const int32_t* __restrict__ it_ks, const int32_t* 
           lo = min(lo, sl);
           hi = max(hi, sl);
         }
-        rows[lane * R + w] = li;
+        rows[pos * R + w] = li;
       }
     } else {
-      for (int w = 0; w < R; ++w) rows[lane * R + w] = GZ_PAD;
+      for (int w = 0; w < R; ++w) rows[pos * R + w] = GZ_PAD;
     }
-    pb[lane] = p;
-    gid[lane] = g;
+    pb[pos] = p;
+    gid[pos] = g;
     for (int o = 16; o; o >>= 1) {
       lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
@@ -944,16 +1005,14 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
       __threadfence_block();
       const long long c2 = stats ? clock64() : 0;
       double* sc = reinterpret_cast<double*>(buf + L.coord_off);
-      const int na = (int)(ra.desc.x & 0xffu);
       if (DIM == 2 && pair) {
-        const int nb = (int)(rb.desc.x & 0xffu);
         double2 oa, ob;
-        gz_update2<RMAX>(ra, lane < na, rb, lane < nb, R,
+        gz_update2<RMAX>(ra, (ra.pb & 0x7fffu) != 0x7fffu, rb, (rb.pb & 0x7fffu) != 0x7fffu, R,
                          reinterpret_cast<const uint4*>(basea) + lane * (R >> 3),
                          reinterpret_cast<const uint4*>(baseb) + lane * (R >> 3), sc, oa, ob);
-        if (lane < na) store_owned(ra, oa.x, oa.y, 0.0);
-        if (lane < nb) store_owned(rb, ob.x, ob.y, 0.0);
-      } else if (lane < na) {
+        if ((ra.pb & 0x7fffu) != 0x7fffu) store_owned(ra, oa.x, oa.y, 0.0);
+        if ((rb.pb & 0x7fffu) != 0x7fffu) store_owned(rb, ob.x, ob.y, 0.0);
+      } else if ((ra.pb & 0x7fffu) != 0x7fffu) {
         const int nr4 = DIM == 3 ? (int)r4(reinterpret_cast<const uint32_t*>(buf)[1]) : 0;
         double ox, oy, oz;
         gz_update<DIM, RMAX>(ra, R, reinterpret_cast<const uint4*>(basea) + lane * (R >> 3), sc, nr4, ox, oy, oz);
@@ -1317,10 +1376,14 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int cap, in
                            GzLayout* L) {
   L->NPW = 1;
   L->NW = nw;
-  // record ring: RR batches of GZ_BS records; RR * GZ_BS - GZ_BS >= workers keeps
-  // every mbarrier phase unambiguous (a claim is never a full ring ahead)
+  // A worker waits for the record batch of its claim; that batch's slot could
+  // only be two phases behind if every claim of the RR batches before it were
+  // outstanding too, i.e. RR * GZ_BS < NW; RR * GZ_BS >= NW + GZ_BS keeps each
+  // wait unambiguous.  The ring is also the record prefetch depth: about 45
+  // records are consumed per TMA latency on C4, so at least 8 batches (64
+  // records; 4 batches measured 1.7x slower).  RR is a power of two.
   L->RR = 8;
-  while (L->RR * GZ_BS - GZ_BS < nw + GZ_BS) L->RR *= 2;  // a power of two
+  while (L->RR * GZ_BS < nw + GZ_BS) L->RR *= 2;
   L->RR_log2 = 0;
   while ((1 << L->RR_log2) < L->RR) ++L->RR_log2;
   L->rec_bytes = gz_rec16(nd.max_row > 0 ? (int)((nd.max_row + 7) & ~7) : 8) * 16;
@@ -1358,9 +1421,9 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
   const int maxw = (m->dim == 2 ? 1024 : 384) / 32;  // the kernel's launch bounds
-  // 18 workers measured best on C4 (more warps only lengthen every item: the
+  // 22 workers measured best on C4 (more warps only lengthen every item: the
   // shared-memory pipe is the shared resource); + region producer + record loader
-  const int nw = env_int("LMS_GZ_WORKERS", std::min(maxw - 2, m->dim == 2 ? 18 : 10), 1, maxw - 2);
+  const int nw = env_int("LMS_GZ_WORKERS", std::min(maxw - 2, m->dim == 2 ? 22 : 10), 1, maxw - 2);
   const int want_nb = env_int("LMS_GZ_BUFFERS", 0, 0, 8);
   const int dim = m->dim, C = m->C;
   GzNeeds nd;

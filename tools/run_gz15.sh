@@ -1,0 +1,9 @@
+#!/bin/bash
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gz or C4" > gpurun_out/gz15_tests.log 2>&1
+echo rc=$? >> gpurun_out/gz15_tests.log
+export LMS_GZ_VERBOSE=1
+for w in 22 26 30; do
+  LMS_GZ_WORKERS=$w timeout 300 python tools/explore.py --config C4 --sweeps 12 --reps 2 \
+    --variants gz:3000:1,gz:3600:1,gz:4096:1,gz:5000:1 > gpurun_out/gz15_explore_$w.log 2>&1
+done
+echo done
