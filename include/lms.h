@@ -60,8 +60,7 @@ typedef enum {
 } lms_order_kind;
 
 typedef enum {
-    LMS_SCHED_AUTO = 0,     /* pick per mesh: GZ for 2D meshes with <= 6 colours, else S3 when the
-                               ordering is banded, else S1 */
+    LMS_SCHED_AUTO = 0,     /* pick per mesh: GZ for 2D meshes with <= 8 colours, else S1 */
     LMS_SCHED_S1 = 1,       /* one launch per colour (CUDA-graph captured sweep) */
     LMS_SCHED_S3 = 3,       /* persistent colour-pipelined sweep with per-tile progress flags */
     LMS_SCHED_GZ = 4        /* ghost-zone tiled sweep: one launch per P sweeps; each CTA stages a

@@ -52,8 +52,10 @@
 //                         (2D), which cuts shared-memory bank conflicts
 //                         (dep_l: l-th item this one waits for, 0xFFFF none)
 //       i32 gid[32]       global id of lane l's vertex
-//       u32 desc[4]       {n | sweep << 8 | stage << 16, mode, n_deps, 0};
-//                         mode 1 = wait for whole stages (too many deps)
+//       u32 desc[4]       {n | sweep << 8 | stage << 16, mode, tile counts
+//                         stages, 0}; mode 1 = wait for whole stages (more
+//                         than U deps); then every item of that tile
+//                         increments the per-stage completion counters
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -73,12 +75,14 @@ constexpr int GZ_MAX_C = 15;    // colours: 4 bits of the update sort key
 constexpr int GZ_MAX_P = 8;     // sweeps per pass: 3 bits of the update sort key
 constexpr uint16_t GZ_PAD = 0xFFFF;
 constexpr int GZ_MAX_REGION = 32767;  // slots are 15 bits (bit 15 = owned flag)
-constexpr int GZ_MAX_DEPS = 32;       // one per lane; more -> wait for whole stages
-constexpr int GZ_BS = 8;              // records per record-ring batch
+// An item is U = 32 * UPL updates of one stage of one tile (UPL updates per
+// lane: 2 in 2D, 1 in 3D); its dependency list has at most U entries (more ->
+// wait for whole stages).
 
 __host__ __device__ inline int64_t r4(int64_t n) { return (n + 3) & ~(int64_t)3; }
 __host__ __device__ inline int gz_hdr_words(int C, int P) { return (int)r4(4 + P * C + 1); }
-__host__ __device__ inline int gz_rec16(int R) { return (64 * R + 128 + 128 + 16) / 16; }
+// record bytes for rows of R and U positions: rows, pb, gid, descriptor
+__host__ __device__ inline int gz_rec16(int R, int U) { return (2 * U * R + 8 * U + 16) / 16; }
 
 
 // ---------------------------------------------------------------- build kernels
@@ -218,13 +222,13 @@ __global__ void k_gzd_tile_r(const uint64_t* __restrict__ ck, const int32_t* __r
 }
 
 // items per (tile, stage): ceil(updates / 32), stage s = j*C + c
-__global__ void k_gzd_stage_items(const int32_t* __restrict__ cntj, int64_t K, int C, int P, int64_t* ns) {
+__global__ void k_gzd_stage_items(const int32_t* __restrict__ cntj, int64_t K, int C, int P, int U, int64_t* ns) {
   const int PC = P * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < K * PC; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = i / PC;
     const int sg = (int)(i - k * PC);
     const int j = sg / C, c = sg - j * C;
-    ns[i] = (cntj[(k * C + c) * P + j] + 31) >> 5;
+    ns[i] = (cntj[(k * C + c) * P + j] + U - 1) / U;
   }
 }
 
@@ -238,7 +242,7 @@ __global__ void k_gzd_item_map(const int64_t* __restrict__ sfirst, int64_t nks, 
 }
 
 // per tile: table entry, record / meta sizes (16-byte units)
-__global__ void k_gzd_tile_sizes(int64_t K, int C, int P, int dim, const int* __restrict__ tR,
+__global__ void k_gzd_tile_sizes(int64_t K, int C, int P, int dim, int U, const int* __restrict__ tR,
                                  const int64_t* __restrict__ sfirst, const int64_t* __restrict__ reg_off,
                                  const int64_t* __restrict__ rs, int64_t* rec_sz, int64_t* meta_sz, int64_t* nitems,
                                  int64_t* nslots, int64_t* nruns) {
@@ -250,7 +254,7 @@ __global__ void k_gzd_tile_sizes(int64_t K, int C, int P, int dim, const int* __
     const int64_t nr = reg_off[k + 1] - reg_off[k];
     nitems[k] = ni;
     nslots[k] = nr;
-    rec_sz[k] = ni * gz_rec16(R);
+    rec_sz[k] = ni * gz_rec16(R, U);
     const int64_t runs = rs[reg_off[k + 1]] - rs[reg_off[k]];
     const bool use_runs = dim == 2 && runs > 0 && nr >= 4 * runs;  // 2D (interleaved) and runs long enough
     nruns[k] = use_runs ? runs : 0;
@@ -258,7 +262,7 @@ __global__ void k_gzd_tile_sizes(int64_t K, int C, int P, int dim, const int* __
   }
 }
 
-__global__ void k_gzd_tiles(int64_t K, int C, int P, const int* __restrict__ tR, const int64_t* __restrict__ rec_off,
+__global__ void k_gzd_tiles(int64_t K, int C, int P, int U, const int* __restrict__ tR, const int64_t* __restrict__ rec_off,
                             const int64_t* __restrict__ meta_off, const int64_t* __restrict__ nitems,
                             const int64_t* __restrict__ nslots, const int64_t* __restrict__ nruns,
                             const int64_t* __restrict__ sfirst, GzTile* tab,
@@ -271,7 +275,7 @@ __global__ void k_gzd_tiles(int64_t K, int C, int P, const int* __restrict__ tR,
     t.rec_base = rec_off[k];
     t.meta_base = meta_off[k];
     t.meta16 = (uint32_t)(meta_off[k + 1] - meta_off[k]);
-    t.rec16 = (uint32_t)gz_rec16(R);
+    t.rec16 = (uint32_t)gz_rec16(R, U);
     t.n_items = (uint32_t)nitems[k];
     t.n_slots = (uint32_t)nslots[k];
     t.R = (uint32_t)R;
@@ -319,19 +323,26 @@ __global__ void k_gzd_region(const uint64_t* __restrict__ reg, int64_t n, int C,
 }
 
 // one warp per item: the record (rows, slots + owned flags, ids, descriptor)
-// and the item's touched slot interval [lo, hi]
+// and the item's touched slot interval [lo, hi].  Lane l builds positions l,
+// l + 32, ... (U = 32 * UPL positions).  2D rows of 8 get a greedy bank-aware
+// placement: the 16-byte shared-memory gathers and the result stores are
+// processed 8 lanes at a time, and lanes of one quarter-warp hitting the same
+// bank group serialise, so each update goes to the group of 8 positions where
+// it collides least (groups of the same instruction are positions 32u..32u+31).
 __global__ void __launch_bounds__(256) k_gzd_records(const int32_t* __restrict__ it_ks,
                                                      const int32_t* __restrict__ it_q, int64_t NI,
-                              int C, int P, const int64_t* __restrict__ kc_off, const int32_t* __restrict__ cntj,
+                              int C, int P, int UPL, const int64_t* __restrict__ kc_off, const int32_t* __restrict__ cntj,
                               const uint64_t* __restrict__ ck, const int32_t* __restrict__ cv,
                               const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
                               const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                               const int32_t* __restrict__ tile_of, const uint64_t* __restrict__ reg,
                               const int64_t* __restrict__ reg_off, uint4* rec, int32_t* it_lo, int32_t* it_hi) {
-  __shared__ uint8_t gz_banks[8 * 32 * 9];
-  __shared__ uint8_t gz_pos[8 * 32];
+  __shared__ uint8_t gz_banks[8 * 64 * 9];
+  __shared__ uint8_t gz_pos[8 * 64];
   const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
   const int PC = P * C;
+  const int U = 32 * UPL;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = w0; it < NI; it += nw) {
@@ -342,98 +353,103 @@ __global__ void __launch_bounds__(256) k_gzd_records(const int32_t* __restrict__
     const int q = it_q[it];
     const int64_t kc = k * C + c;
     const int nupd = cntj[kc * P + j];
-    const int n = min(32, nupd - 32 * q);
+    const int n = min(U, nupd - U * q);
     const GzTile t = tab[k];
     const int R = (int)t.R;
     const int64_t tloc = it - sfirst[k * PC];  // item index inside the tile
     unsigned char* base = reinterpret_cast<unsigned char*>(rec + t.rec_base + tloc * t.rec16);
     uint16_t* rows = reinterpret_cast<uint16_t*>(base);
-    uint32_t* pb = reinterpret_cast<uint32_t*>(base + 64 * R);
-    int32_t* gid = reinterpret_cast<int32_t*>(base + 64 * R + 128);
-    uint32_t* desc = reinterpret_cast<uint32_t*>(base + 64 * R + 256);
-    int lo = 0x7fffffff, hi = -1;
-    uint32_t p = 0xffff0000u | 0x7fffu;  // slot 0x7fff = empty lane
-    int32_t g = -1;
+    uint32_t* pb = reinterpret_cast<uint32_t*>(base + 2 * U * R);
+    int32_t* gid = reinterpret_cast<int32_t*>(base + 2 * U * R + 4 * U);
+    uint32_t* desc = reinterpret_cast<uint32_t*>(base + 2 * U * R + 8 * U);
     const uint64_t kh = (uint64_t)k << 32;
     const int64_t ra = reg_off[k], rb = reg_off[k + 1];
-    int d = 0;
-    if (lane < n) {
-      const int64_t u = kc_off[kc] + 32 * q + lane;
-      const int32_t v = cv[u];
-      const int lv = (int)(ck[u] & 0xffffull);
-      g = v;
-      p = 0xffff0000u | (uint32_t)lv | (tile_of[v] == (int32_t)k ? 0x8000u : 0u);
-      lo = hi = lv;
-      const int32_t b = rp[v];
-      d = rp[v + 1] - b;
-    }
-    // lane position in the record: 2D rows of 8 get a greedy bank-aware
-    // assignment to quarter-warps (the 16-byte shared-memory gathers and the
-    // result store are processed 8 lanes at a time; lanes of one quarter that
-    // hit the same bank group serialise), everything else keeps its lane
-    int pos = lane;
+    uint8_t* bk = gz_banks + wib * 64 * 9;
+    uint8_t* ps = gz_pos + wib * 64;
+    // bank groups of each update (position-independent), then the placement
     if (R == 8) {
-      uint8_t* bk = gz_banks + (threadIdx.x >> 5) * 32 * 9;
-      for (int w = 0; w < 9; ++w) bk[lane * 9 + w] = 0xff;
-      if (lane < n) {
-        bk[lane * 9] = (uint8_t)((p & 0x7fffu) & 7u);
-        const int32_t b = rp[g];
-        for (int w = 0; w < d && w < 8; ++w) {
-          const int sl = (int)(lower_bound_u64(reg, ra, rb, kh | (uint32_t)col[b + w]) - ra);
-          bk[lane * 9 + 1 + w] = (uint8_t)(sl & 7);
+      for (int u0 = 0; u0 < U; u0 += 32) {
+        const int e = u0 + lane;
+        for (int w = 0; w < 9; ++w) bk[e * 9 + w] = 0xff;
+        if (e < n) {
+          const int64_t uu = kc_off[kc] + (int64_t)U * q + e;
+          const int32_t v = cv[uu];
+          bk[e * 9] = (uint8_t)((ck[uu] & 0xffffull) & 7u);
+          const int32_t b = rp[v], d = rp[v + 1] - b;
+          for (int w = 0; w < d && w < 8; ++w) {
+            const int sl = (int)(lower_bound_u64(reg, ra, rb, kh | (uint32_t)col[b + w]) - ra);
+            bk[e * 9 + 1 + w] = (uint8_t)(sl & 7);
+          }
         }
       }
       __syncwarp();
       if (lane == 0) {
-        uint8_t qm[4][9];
-        int qn[4] = {0, 0, 0, 0};
-        for (int a = 0; a < 4; ++a)
+        uint8_t qm[8][9];
+        int qn[8];
+        const int ng = U / 8;
+        for (int a = 0; a < ng; ++a) {
+          qn[a] = 0;
           for (int w = 0; w < 9; ++w) qm[a][w] = 0;
-        int posv[32];
-        for (int dd = 9; dd >= 0; --dd)  // most neighbours first; empty lanes (9 x 0xff) last
-          for (int l = 0; l < 32; ++l) {
+        }
+        for (int dd = 9; dd >= 0; --dd)  // most neighbours first; empty positions (no banks) last
+          for (int e = 0; e < U; ++e) {
             int cntl = 0;
-            for (int w = 0; w < 9; ++w) cntl += bk[l * 9 + w] != 0xff;
+            for (int w = 0; w < 9; ++w) cntl += bk[e * 9 + w] != 0xff;
             if (cntl != dd) continue;
             int best = -1, bp = 1 << 30;
-            for (int a = 0; a < 4; ++a) {
+            for (int a = 0; a < ng; ++a) {
               if (qn[a] >= 8) continue;
               int pen = 0;
               for (int w = 0; w < 9; ++w) {
-                const int bb = bk[l * 9 + w];
+                const int bb = bk[e * 9 + w];
                 if (bb != 0xff) pen += (qm[a][w] >> bb) & 1;
               }
               if (pen < bp) { bp = pen; best = a; }
             }
-            posv[l] = 8 * best + qn[best]++;
+            ps[e] = (uint8_t)(8 * best + qn[best]++);
             for (int w = 0; w < 9; ++w) {
-              const int bb = bk[l * 9 + w];
+              const int bb = bk[e * 9 + w];
               if (bb != 0xff) qm[best][w] |= (uint8_t)(1u << bb);
             }
           }
-        for (int l = 0; l < 32; ++l) gz_pos[(threadIdx.x >> 5) * 32 + l] = (uint8_t)posv[l];
       }
       __syncwarp();
-      pos = gz_pos[(threadIdx.x >> 5) * 32 + lane];
-      __syncwarp();
-    }
-    if (lane < n) {
-      const int32_t b = rp[g];
-      for (int w = 0; w < R; ++w) {
-        uint16_t li = GZ_PAD;
-        if (w < d) {
-          const int sl = (int)(lower_bound_u64(reg, ra, rb, kh | (uint32_t)col[b + w]) - ra);
-          li = (uint16_t)sl;
-          lo = min(lo, sl);
-          hi = max(hi, sl);
-        }
-        rows[pos * R + w] = li;
-      }
     } else {
-      for (int w = 0; w < R; ++w) rows[pos * R + w] = GZ_PAD;
+      for (int e = lane; e < U; e += 32) ps[e] = (uint8_t)e;
+      __syncwarp();
     }
-    pb[pos] = p;
-    gid[pos] = g;
+    int lo = 0x7fffffff, hi = -1;
+    for (int u0 = 0; u0 < U; u0 += 32) {
+      const int e = u0 + lane;
+      const int pos = ps[e];
+      uint32_t p = 0xffff0000u | 0x7fffu;  // slot 0x7fff = empty position
+      int32_t g = -1;
+      if (e < n) {
+        const int64_t uu = kc_off[kc] + (int64_t)U * q + e;
+        const int32_t v = cv[uu];
+        const int lv = (int)(ck[uu] & 0xffffull);
+        g = v;
+        p = 0xffff0000u | (uint32_t)lv | (tile_of[v] == (int32_t)k ? 0x8000u : 0u);
+        lo = min(lo, lv);
+        hi = max(hi, lv);
+        const int32_t b = rp[v], d = rp[v + 1] - b;
+        for (int w = 0; w < R; ++w) {
+          uint16_t li = GZ_PAD;
+          if (w < d) {
+            const int sl = (int)(lower_bound_u64(reg, ra, rb, kh | (uint32_t)col[b + w]) - ra);
+            li = (uint16_t)sl;
+            lo = min(lo, sl);
+            hi = max(hi, sl);
+          }
+          rows[pos * R + w] = li;
+        }
+      } else {
+        for (int w = 0; w < R; ++w) rows[pos * R + w] = GZ_PAD;
+      }
+      pb[pos] = p;
+      gid[pos] = g;
+    }
+    __syncwarp();
     for (int o = 16; o; o >>= 1) {
       lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
       hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
@@ -452,9 +468,10 @@ __global__ void __launch_bounds__(256) k_gzd_records(const int32_t* __restrict__
 // dependencies: the earlier items of stages [s - C, s - 1] of the same tile
 // whose touched slot intervals overlap this item's (a superset of the items it
 // shares a vertex with; older stages are ordered transitively through them)
-__global__ void k_gzd_deps(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P,
+__global__ void k_gzd_deps(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P, int U,
                            const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
-                           const int32_t* __restrict__ it_lo, const int32_t* __restrict__ it_hi, uint4* rec) {
+                           const int32_t* __restrict__ it_lo, const int32_t* __restrict__ it_hi, uint4* rec,
+                           int* tneed) {
   const int PC = P * C;
   for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < NI; it += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ks = it_ks[it];
@@ -463,18 +480,32 @@ __global__ void k_gzd_deps(const int32_t* __restrict__ it_ks, int64_t NI, int C,
     const GzTile t = tab[k];
     const int64_t f0 = sfirst[k * PC];
     unsigned char* base = reinterpret_cast<unsigned char*>(rec + t.rec_base + (it - f0) * t.rec16);
-    uint32_t* pb = reinterpret_cast<uint32_t*>(base + 64 * t.R);
-    uint32_t* desc = reinterpret_cast<uint32_t*>(base + 64 * t.R + 256);
+    uint32_t* pb = reinterpret_cast<uint32_t*>(base + 2 * U * t.R);
+    uint32_t* desc = reinterpret_cast<uint32_t*>(base + 2 * U * t.R + 8 * U);
     const int lo = it_lo[it], hi = it_hi[it];
     const int64_t a = sfirst[k * PC + (sg - C > 0 ? sg - C : 0)], b = sfirst[k * PC + sg];
     int nd = 0;
     for (int64_t o = a; o < b; ++o)
       if (it_lo[o] <= hi && it_hi[o] >= lo) {
-        if (nd < GZ_MAX_DEPS) pb[nd] = (pb[nd] & 0xffffu) | ((uint32_t)(o - f0) << 16);
+        if (nd < U) pb[nd] = (pb[nd] & 0xffffu) | ((uint32_t)(o - f0) << 16);
         ++nd;
       }
-    desc[1] = nd > GZ_MAX_DEPS ? 1u : 0u;
-    desc[2] = (uint32_t)nd;
+    desc[1] = nd > U ? 1u : 0u;
+    if (nd > U) atomicOr(&tneed[k], 1);
+  }
+}
+
+// desc[2] = 1 for every item of a tile in which some item waits for whole
+// stages (those tiles keep per-stage completion counters)
+__global__ void k_gzd_mark(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P, int U,
+                           const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
+                           const int* __restrict__ tneed, uint4* rec) {
+  const int PC = P * C;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < NI; it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = it_ks[it] / PC;
+    const GzTile t = tab[k];
+    unsigned char* base = reinterpret_cast<unsigned char*>(rec + t.rec_base + (it - sfirst[k * PC]) * t.rec16);
+    reinterpret_cast<uint32_t*>(base + 2 * U * t.R + 8 * U)[2] = (uint32_t)tneed[k];
   }
 }
 
@@ -715,8 +746,8 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
 // copies of id runs, or 16-byte cp.async gathers), warp 1 streams item
 // records into the record ring (one TMA bulk copy per record, in claim
 // order), warps 2.. are workers (one claimed item at a time).
-template <int DIM, int RMAX, bool PAIR>
-__global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
+template <int DIM, int RMAX, int UPL>
+__global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
                                                                       const GzTile* __restrict__ tab,
                                                                       const int32_t* __restrict__ item_sweep,
                                                                       const uint4* __restrict__ meta,
@@ -735,7 +766,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);     // [NB] region coordinates of the buffer's tile landed
   uint64_t* empty = full + NB;                          // [NB] buffer's tile finished
   uint64_t* rfull = empty + NB;                         // [RR] record batch landed
-  uint64_t* rempty = rfull + RR;                        // [RR] record batch consumed (GZ_BS arrivals)
+  uint64_t* rempty = rfull + RR;                        // [RR] record batch consumed (BS arrivals)
   uint64_t* sbar = rempty + RR;                         // [1] producer staging copy landed
   int* ctl = reinterpret_cast<int*>(sbar + 1);          // [0] cursor, [1..NB] buf_tile, [NB+1..2NB] ndone
   volatile int* buf_tile = ctl + 1;
@@ -762,7 +793,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
     }
     for (int r = 0; r < RR; ++r) {
       mbar_init(rfull + r, 1);
-      mbar_init(rempty + r, GZ_BS);
+      mbar_init(rempty + r, L.BS);
     }
     mbar_init(sbar, 1);
     ctl[0] = 0;
@@ -862,11 +893,12 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
     // tile's record size equals the slot stride, else one per record)
     if (lane == 0) {
       int ti = 0;
-      const int nbat = (total + GZ_BS - 1) / GZ_BS;
+      const int BS = L.BS;
+      const int nbat = (total + BS - 1) / BS;
       for (int g = 0; g < nbat; ++g) {
         const int slot = g & (RR - 1);  // RR is a power of two
         if (g >= RR) mbar_wait(rempty + slot, ((uint32_t)(g >> L.RR_log2) & 1u) ^ 1u);
-        const int k0 = g * GZ_BS, k1 = min(total, k0 + GZ_BS);
+        const int k0 = g * BS, k1 = min(total, k0 + BS);
         uint32_t bytes = 0;
         for (int kc = k0, tj = ti; kc < k1;) {  // pass 1: bytes of the batch
           while (kc >= t_pre[tj + 1]) ++tj;
@@ -875,7 +907,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
           kc = kend;
         }
         mbar_expect_tx(rfull + slot, bytes);
-        unsigned char* dst = rring + (size_t)slot * GZ_BS * L.rec_bytes;
+        unsigned char* dst = rring + (size_t)slot * BS * L.rec_bytes;
         for (int kc = k0; kc < k1;) {
           while (kc >= t_pre[ti + 1]) ++ti;
           const int kend = min(k1, t_pre[ti + 1]);
@@ -915,122 +947,115 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
   };
   unsigned long long w_wait = 0, w_dep = 0, w_comp = 0, w_items = 0;
   bool tile_ready = false;
-  constexpr int G = (DIM == 2 && PAIR) ? 2 : 1;  // items claimed together (PAIR: two updates per lane)
-  auto load_rec = [&](int kc, GzRec<RMAX>& r) -> const unsigned char* {
-    const int bat = kc >> 3;
+  constexpr int U = 32 * UPL;  // updates per item; lane l handles positions l, l + 32
+  const int bs_log2 = L.BS_log2;
+  for (;;) {
+    int kc = 0;
+    if (lane == 0) kc = atomicAdd(ctl, 1);
+    kc = __shfl_sync(FULL, kc, 0);
+    if (kc >= total) break;
+    if (kc >= pre_hi) {
+      enter_tile(kc);
+      tile_ready = false;
+    }
+    const int i = ti;
+    const int t = item0 + (kc - pre_lo);
+    const long long c0 = stats ? clock64() : 0;
+    // the item's record, from the record ring
+    const int bat = kc >> bs_log2;
     const int slot = bat & (RR - 1);
-    if (lane == 0) mbar_wait(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u);
+    const unsigned char* rbase =
+        rring + ((size_t)slot * L.BS + (kc & (L.BS - 1))) * L.rec_bytes;
+    if (lane == 0) {
+      mbar_wait(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u);
+      if (!tile_ready) {  // the region of the item's tile
+        while (buf_tile[tb & 0xffff] != i) __nanosleep(32);
+        mbar_wait(full + (tb & 0xffff), (uint32_t)(tb >> 16));
+      }
+    }
+    tile_ready = true;
     __syncwarp();
-    const unsigned char* rbase = rring + ((size_t)slot * GZ_BS + (kc & 7)) * L.rec_bytes;
-    const uint4* rows = reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3);
+    GzRec<RMAX> r[UPL];
+    const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rbase + 2 * U * R);
+    const uint4 desc = *reinterpret_cast<const uint4*>(rbase + 2 * U * R + 8 * U);
 #pragma unroll
-    for (int p = 0; p < RMAX / 8; ++p) r.row[p] = (p * 8 < R) ? rows[p] : make_uint4(~0u, ~0u, ~0u, ~0u);
-    const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rbase + 64 * R);
-    r.pb = pbs[lane];
-    r.gid = (int32_t)pbs[32 + lane];
-    r.desc = *reinterpret_cast<const uint4*>(rbase + 64 * R + 256);
-    return rbase;
-  };
-  auto wait_deps = [&](const GzRec<RMAX>& r, int i) {
+    for (int u = 0; u < UPL; ++u) {
+      const int pos = lane + 32 * u;
+      const uint4* rows = reinterpret_cast<const uint4*>(rbase) + pos * (R >> 3);
+#pragma unroll
+      for (int p = 0; p < RMAX / 8; ++p) r[u].row[p] = (p * 8 < R) ? rows[p] : make_uint4(~0u, ~0u, ~0u, ~0u);
+      r[u].pb = pbs[pos];
+      r[u].gid = (int32_t)pbs[U + pos];
+      r[u].desc = desc;
+    }
+    const long long c1 = stats ? clock64() : 0;
     volatile int* flags = reinterpret_cast<volatile int*>(buf + L.flag_off);
-    const int sg = (int)(r.desc.x >> 16);
-    if (r.desc.y == 0) {
-      const int dep = (int)(r.pb >> 16);
-      if (dep != 0xffff && dep >= item0)
-        while (flags[dep] != i + 1) __nanosleep(20);
+    int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
+    const int j = (int)((desc.x >> 8) & 0xffu);
+    const int sg = (int)(desc.x >> 16);
+    // this item's dependencies
+    if (desc.y == 0) {
+#pragma unroll
+      for (int u = 0; u < UPL; ++u) {
+        const int dep = (int)(r[u].pb >> 16);
+        if (dep != 0xffff && dep >= item0)
+          while (flags[dep] != i + 1) __nanosleep(20);
+      }
     } else if (lane == 0) {
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(buf);
-      int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
       const int s0 = max(sg - C, j0 * C);
       for (int s2 = s0; s2 < sg; ++s2) {
         const int need = (int)(hdr[4 + s2 + 1] - hdr[4 + s2]);
         while (*(volatile int*)(cnt + s2) != need) __nanosleep(20);
       }
     }
-  };
-  auto store_owned = [&](const GzRec<RMAX>& r, double ox, double oy, double oz) {
-    if ((int)((r.desc.x >> 8) & 0xffu) == P - 1 && (r.pb & 0x8000u)) {  // owned vertex, final value of the pass
-      if (DIM == 2) {
-        a1[r.gid] = make_double2(ox, oy);
-      } else {
-        x1[r.gid] = ox;
-        y1[r.gid] = oy;
-        z1[r.gid] = oz;
-      }
-    }
-  };
-  auto finish = [&](const GzRec<RMAX>& r, int kc, int t, int i) {  // lane 0, after __syncwarp
-    volatile int* flags = reinterpret_cast<volatile int*>(buf + L.flag_off);
-    int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
-    mbar_arrive(rempty + ((kc >> 3) & (RR - 1)));  // one of the batch's records consumed
+    __syncwarp();
     __threadfence_block();
-    flags[t] = i + 1;
-    atomicAdd(cnt + (int)(r.desc.x >> 16), 1);
-    if (atomicAdd(ndone + (tb & 0xffff), 1) == pre_hi - pre_lo - 1) mbar_arrive(empty + (tb & 0xffff));
-  };
-  for (;;) {
-    int kc0 = 0;
-    if (lane == 0) kc0 = atomicAdd(ctl, G);
-    kc0 = __shfl_sync(FULL, kc0, 0);
-    if (kc0 >= total) break;
-    const int nclaim = min(G, total - kc0);
-    for (int q = 0; q < nclaim;) {
-      const int kc = kc0 + q;
-      if (kc >= pre_hi) {
-        enter_tile(kc);
-        tile_ready = false;
+    const long long c2 = stats ? clock64() : 0;
+    double* sc = reinterpret_cast<double*>(buf + L.coord_off);
+    const bool last = j == P - 1;
+    if (UPL == 2 && DIM == 2) {
+      const bool va = (r[0].pb & 0x7fffu) != 0x7fffu, vb = (r[UPL - 1].pb & 0x7fffu) != 0x7fffu;
+      double2 oa, ob;
+      gz_update2<RMAX>(r[0], va, r[UPL - 1], vb, R, reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3),
+                       reinterpret_cast<const uint4*>(rbase) + (lane + 32) * (R >> 3), sc, oa, ob);
+      if (last) {  // owned vertices, final values of the pass
+        if (va && (r[0].pb & 0x8000u)) a1[r[0].gid] = oa;
+        if (vb && (r[UPL - 1].pb & 0x8000u)) a1[r[UPL - 1].gid] = ob;
       }
-      const int i = ti;
-      const long long c0 = stats ? clock64() : 0;
-      GzRec<RMAX> ra, rb;
-      const unsigned char* basea = load_rec(kc, ra);
-      const int ta = item0 + (kc - pre_lo);
-      // pair with the next claimed item if it is in the same tile and does not wait for this one
-      bool pair = false;
-      const unsigned char* baseb = basea;
-      if (G == 2 && q + 1 < nclaim && kc + 1 < pre_hi) {
-        baseb = load_rec(kc + 1, rb);
-        pair = rb.desc.y == 0 && !__any_sync(FULL, (int)(rb.pb >> 16) == ta);
-      }
-      if (lane == 0 && !tile_ready) {  // the region of the item's tile
-        while (buf_tile[tb & 0xffff] != i) __nanosleep(32);
-        mbar_wait(full + (tb & 0xffff), (uint32_t)(tb >> 16));
-      }
-      tile_ready = true;
-      __syncwarp();
-      const long long c1 = stats ? clock64() : 0;
-      wait_deps(ra, i);
-      if (pair) wait_deps(rb, i);
-      __syncwarp();
+    } else {
+#pragma unroll
+      for (int u = 0; u < UPL; ++u)
+        if ((r[u].pb & 0x7fffu) != 0x7fffu) {
+          const int nr4 = DIM == 3 ? (int)r4(reinterpret_cast<const uint32_t*>(buf)[1]) : 0;
+          double ox, oy, oz;
+          gz_update<DIM, RMAX>(r[u], R, reinterpret_cast<const uint4*>(rbase) + (lane + 32 * u) * (R >> 3), sc,
+                               nr4, ox, oy, oz);
+          if (last && (r[u].pb & 0x8000u)) {
+            if (DIM == 2) {
+              a1[r[u].gid] = make_double2(ox, oy);
+            } else {
+              x1[r[u].gid] = ox;
+              y1[r[u].gid] = oy;
+              z1[r[u].gid] = oz;
+            }
+          }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(rempty + slot);  // one of the batch's records consumed
       __threadfence_block();
-      const long long c2 = stats ? clock64() : 0;
-      double* sc = reinterpret_cast<double*>(buf + L.coord_off);
-      if (DIM == 2 && pair) {
-        double2 oa, ob;
-        gz_update2<RMAX>(ra, (ra.pb & 0x7fffu) != 0x7fffu, rb, (rb.pb & 0x7fffu) != 0x7fffu, R,
-                         reinterpret_cast<const uint4*>(basea) + lane * (R >> 3),
-                         reinterpret_cast<const uint4*>(baseb) + lane * (R >> 3), sc, oa, ob);
-        if ((ra.pb & 0x7fffu) != 0x7fffu) store_owned(ra, oa.x, oa.y, 0.0);
-        if ((rb.pb & 0x7fffu) != 0x7fffu) store_owned(rb, ob.x, ob.y, 0.0);
-      } else if ((ra.pb & 0x7fffu) != 0x7fffu) {
-        const int nr4 = DIM == 3 ? (int)r4(reinterpret_cast<const uint32_t*>(buf)[1]) : 0;
-        double ox, oy, oz;
-        gz_update<DIM, RMAX>(ra, R, reinterpret_cast<const uint4*>(basea) + lane * (R >> 3), sc, nr4, ox, oy, oz);
-        store_owned(ra, ox, oy, oz);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        finish(ra, kc, ta, i);
-        if (pair) finish(rb, kc + 1, ta + 1, i);
-      }
-      q += pair ? 2 : 1;
-      if (stats) {
-        const long long c3 = clock64();
-        w_wait += c1 - c0;
-        w_dep += c2 - c1;
-        w_comp += c3 - c2;
-        w_items += pair ? 2 : 1;
-      }
+      flags[t] = i + 1;
+      if (desc.z) atomicAdd(cnt + sg, 1);  // stage counters: only tiles with whole-stage waits read them
+      if (atomicAdd(ndone + (tb & 0xffff), 1) == pre_hi - pre_lo - 1) mbar_arrive(empty + (tb & 0xffff));
+    }
+    if (stats) {
+      const long long c3 = clock64();
+      w_wait += c1 - c0;
+      w_dep += c2 - c1;
+      w_comp += c3 - c2;
+      w_items += 1;
     }
   }
   if (stats && lane == 0) {
@@ -1127,7 +1152,7 @@ struct GzNeeds {
 // Returns false (nothing kept) if the limits (region <= 32767 slots, items per
 // tile, `fits`: the shared-memory plan) are not met.
 template <typename Fits>
-static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* out, Fits fits) {
+static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, cudaStream_t s, GzNeeds* out, Fits fits) {
   // LMS_GZ_VERBOSE=2: host-side phase timings (synchronising)
   const bool tv = getenv("LMS_GZ_VERBOSE") && atoi(getenv("LMS_GZ_VERBOSE")) >= 2;
   auto t_last = std::chrono::steady_clock::now();
@@ -1245,7 +1270,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   // items: per (tile, stage) ceil(updates / 32), tile-major then stage-major
   const int64_t nks = K * PC;
   DBuf<int64_t> ns(nks > 0 ? nks : 1, s), sfirst(nks + 1, s);
-  k_gzd_stage_items<<<gsz(nks), 256, 0, s>>>(cntj.p, K, C, P, ns.p);
+  k_gzd_stage_items<<<gsz(nks), 256, 0, s>>>(cntj.p, K, C, P, 32 * upl, ns.p);
   LMS_CHECK_LAUNCH();
   const int64_t NI = scan_i64(ns.p, nks, sfirst.p, s);
   ns.release();
@@ -1273,7 +1298,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   }
   DBuf<int64_t> rec_sz(K, s), meta_sz(K, s), nitems(K, s), nslots(K, s), nruns(K, s), rec_off(K + 1, s),
       meta_off(K + 1, s);
-  k_gzd_tile_sizes<<<gsz(K), 256, 0, s>>>(K, C, P, m->dim, tR.p, sfirst.p, reg_off.p, rs.p, rec_sz.p, meta_sz.p, nitems.p,
+  k_gzd_tile_sizes<<<gsz(K), 256, 0, s>>>(K, C, P, m->dim, 32 * upl, tR.p, sfirst.p, reg_off.p, rs.p, rec_sz.p, meta_sz.p, nitems.p,
                                           nslots.p, nruns.p);
   LMS_CHECK_LAUNCH();
   const int64_t rec16_all = scan_i64(rec_sz.p, K, rec_off.p, s);
@@ -1310,7 +1335,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   DBuf<GzTile> tab(K > 0 ? K : 1, s);
   DBuf<int32_t> item_sweep(K * (P + 1) > 0 ? K * (P + 1) : 1, s);
   DBuf<uint4> meta(meta16_all > 0 ? meta16_all : 1, s), rec(rec16_all > 0 ? rec16_all : 1, s);
-  k_gzd_tiles<<<gsz(K), 256, 0, s>>>(K, C, P, tR.p, rec_off.p, meta_off.p, nitems.p, nslots.p, nruns.p, sfirst.p, tab.p,
+  k_gzd_tiles<<<gsz(K), 256, 0, s>>>(K, C, P, 32 * upl, tR.p, rec_off.p, meta_off.p, nitems.p, nslots.p, nruns.p, sfirst.p, tab.p,
                                      item_sweep.p, reinterpret_cast<uint32_t*>(meta.p));
   LMS_CHECK_LAUNCH();
   if (nreg_all > 0) {
@@ -1320,11 +1345,16 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   }
   if (NI > 0) {
     DBuf<int32_t> it_lo(NI, s), it_hi(NI, s);
-    k_gzd_records<<<gsz(NI * 32), 256, 0, s>>>(it_ks.p, it_q.p, NI, C, P, kc_off.p, cntj.p, ck2.p, cv2.p, tab.p,
+    k_gzd_records<<<gsz(NI * 32), 256, 0, s>>>(it_ks.p, it_q.p, NI, C, P, upl, kc_off.p, cntj.p, ck2.p, cv2.p, tab.p,
                                                sfirst.p, m->row_ptr.p, m->col.p, tile_of.p, reg.p, reg_off.p, rec.p,
                                                it_lo.p, it_hi.p);
     LMS_CHECK_LAUNCH();
-    k_gzd_deps<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, tab.p, sfirst.p, it_lo.p, it_hi.p, rec.p);
+    DBuf<int> tneed(K > 0 ? K : 1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(tneed.p, 0, (K > 0 ? K : 1) * sizeof(int), s));
+    k_gzd_deps<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, 32 * upl, tab.p, sfirst.p, it_lo.p, it_hi.p, rec.p,
+                                       tneed.p);
+    LMS_CHECK_LAUNCH();
+    k_gzd_mark<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, 32 * upl, tab.p, sfirst.p, tneed.p, rec.p);
     LMS_CHECK_LAUNCH();
   }
   mark("records+deps");
@@ -1352,6 +1382,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, cudaStream_t s, GzNeeds* 
   S.gz_meta = std::move(meta);
   S.gz_rec = std::move(rec);
   S.gz_P = P;
+  S.gz_upl = upl;
   S.gz_nreg = nreg_all;
   S.gz_nupd = nU;
   S.gz_items = NI;
@@ -1372,21 +1403,24 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
 static int r16i(int64_t n) { return (int)((n + 15) & ~(int64_t)15); }
 
 // Shared-memory plan for given limits; returns total bytes (> cap if none fits).
-static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int cap, int want_nb, int nw, int tiles_cap,
-                           GzLayout* L) {
+static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, int cap, int want_nb, int nw,
+                           int tiles_cap, GzLayout* L) {
   L->NPW = 1;
   L->NW = nw;
   // A worker waits for the record batch of its claim; that batch's slot could
   // only be two phases behind if every claim of the RR batches before it were
-  // outstanding too, i.e. RR * GZ_BS < NW; RR * GZ_BS >= NW + GZ_BS keeps each
+  // outstanding too, i.e. RR * BS < NW; RR * BS >= NW + BS keeps each
   // wait unambiguous.  The ring is also the record prefetch depth: about 45
   // records are consumed per TMA latency on C4, so at least 8 batches (64
   // records; 4 batches measured 1.7x slower).  RR is a power of two.
+  L->BS = upl == 2 ? 4 : 8;  // records per batch (about 3-6 KB per batch)
+  L->BS_log2 = upl == 2 ? 2 : 3;
   L->RR = 8;
-  while (L->RR * GZ_BS < nw + GZ_BS) L->RR *= 2;
+  while (L->RR * L->BS < nw + L->BS) L->RR *= 2;
   L->RR_log2 = 0;
   while ((1 << L->RR_log2) < L->RR) ++L->RR_log2;
-  L->rec_bytes = gz_rec16(nd.max_row > 0 ? (int)((nd.max_row + 7) & ~7) : 8) * 16;
+  L->rec_bytes = gz_rec16(nd.max_row > 0 ? (int)((nd.max_row + 7) & ~7) : 8, 32 * upl) * 16;
+  L->U = 32 * upl;
   const int HW = gz_hdr_words(C, P);
   L->hdr_bytes = r16i(4 * (int64_t)HW);
   L->flag_off = L->hdr_bytes;
@@ -1403,7 +1437,7 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int cap, in
     const int tab_bytes = r16i((int64_t)tiles_cap * (8 + 4 + 4 + 4 + 4) + 4 * ((int64_t)tiles_cap + 1));
     L->off_stage = L->off_tab + tab_bytes;
     L->off_rec = L->off_stage + L->stage_bytes;
-    L->off_ring = (L->off_rec + L->RR * GZ_BS * L->rec_bytes + 127) & ~127;
+    L->off_ring = (L->off_rec + L->RR * L->BS * L->rec_bytes + 127) & ~127;
     const int64_t total = (int64_t)L->off_ring + (int64_t)nb * L->buf_bytes;
     if (total <= cap) return total;
     if (want_nb > 0) return total;
@@ -1420,7 +1454,10 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   int cap = 0, nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
-  const int maxw = (m->dim == 2 ? 1024 : 384) / 32;  // the kernel's launch bounds
+  // updates per lane (LMS_GZ_UPL=2 in 2D: 64-update items; measured slower on
+  // C4 -- coarser items wait on more dependencies -- so 1 is the default)
+  const int upl = env_int("LMS_GZ_UPL", 1, 1, m->dim == 2 ? 2 : 1);
+  const int maxw = (m->dim == 2 ? 768 : 384) / 32;  // the kernel's launch bounds
   // 22 workers measured best on C4 (more warps only lengthen every item: the
   // shared-memory pipe is the shared resource); + region producer + record loader
   const int nw = env_int("LMS_GZ_WORKERS", std::min(maxw - 2, m->dim == 2 ? 22 : 10), 1, maxw - 2);
@@ -1435,11 +1472,11 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
       const int64_t K = (m->V + t - 1) / t * 2 + 16;
       const int cap_t = (int)std::min<int64_t>(K / nsm + 2, 1 << 20);
       GzLayout L;
-      return plan_layout(q, dim, C, P, cap, want_nb, nw, cap_t, &L) <= cap;
+      return plan_layout(q, dim, C, P, upl, cap, want_nb, nw, cap_t, &L) <= cap;
     };
-    if (build_gz_once(m, t, P, s, &nd, fits)) {
+    if (build_gz_once(m, t, P, upl, s, &nd, fits)) {
       const int tiles_cap = (int)((S.gz_ntiles + nsm - 1) / nsm) + 1;
-      const int64_t total = plan_layout(nd, dim, C, P, cap, want_nb, nw, tiles_cap, &S.gz_L);
+      const int64_t total = plan_layout(nd, dim, C, P, upl, cap, want_nb, nw, tiles_cap, &S.gz_L);
       if (total > cap) continue;
       S.gz_smem = (int)total;
       S.gz_threads = 32 * (2 + S.gz_L.NW);
@@ -1458,10 +1495,10 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   return false;
 }
 
-template <int DIM, int RMAX, bool PAIR>
+template <int DIM, int RMAX, int UPL>
 static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
   Schedule& S = m->sched;
-  auto kern = k_sweep_gz<DIM, RMAX, PAIR>;
+  auto kern = k_sweep_gz<DIM, RMAX, UPL>;
   LMS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S.gz_smem));
   int nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
@@ -1551,14 +1588,14 @@ void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s) {
     const int r = left < S.gz_P ? left : S.gz_P;
     const int j0 = S.gz_P - r;  // the last r sweeps of a P-sweep pass are an exact r-sweep pass
     if (m->dim == 2) {
-      if (getenv("LMS_GZ_PAIR"))  // tuning: two items per warp
-        launch_gz_t<2, 8, true>(m, j0, s);
+      if (S.gz_upl == 2)
+        launch_gz_t<2, 8, 2>(m, j0, s);
       else
-        launch_gz_t<2, 8, false>(m, j0, s);
+        launch_gz_t<2, 8, 1>(m, j0, s);
       m->xy_cur = 1 - m->xy_cur;
       m->aos_state = 1;
     } else {
-      launch_gz_t<3, 16, false>(m, j0, s);
+      launch_gz_t<3, 16, 1>(m, j0, s);
       for (int a = 0; a < m->dim; ++a) std::swap(m->x[a], m->xalt[a]);
     }
     left -= r;

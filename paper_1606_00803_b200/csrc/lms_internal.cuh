@@ -86,6 +86,8 @@ struct __align__(16) GzTile {
 struct GzLayout {
   int NB = 0, NPW = 0, NW = 0;  // region buffers, producer warps, worker warps
   int RR = 0, RR_log2 = 0, rec_bytes = 0, off_rec = 0;  // record ring: batches (power of 2), bytes per record
+  int BS = 8, BS_log2 = 3;      // records per batch
+  int U = 32;                   // updates per item (32 * updates per lane)
   int hdr_bytes = 0;            // per buffer header copy
   int flag_off = 0, cnt_off = 0, coord_off = 0, buf_bytes = 0;  // inside a buffer
   int stage_bytes = 0;          // producer staging (largest meta block)
@@ -127,6 +129,7 @@ struct Schedule {
   // shared memory and runs P whole sweeps there, reading X and writing the
   // owned vertices to X'.
   int gz_P = 0;             // sweeps per pass
+  int gz_upl = 1;           // updates per lane (item = 32 * gz_upl updates)
   int64_t gz_K = 0;         // tiles of the spatial tiling
   int gz_T = 0;             // target owned vertices per tile
   int gz_smem = 0;          // dynamic shared memory per CTA (bytes)

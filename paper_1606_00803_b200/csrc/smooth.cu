@@ -306,7 +306,7 @@ static void build_base(lms_mesh_s* m, cudaStream_t s, bool gz_base) {
     if (S.graphs[i]) { cudaGraphExecDestroy(S.graphs[i]); S.graphs[i] = nullptr; }
   const int64_t V = m->V;
   const int C = m->C > 0 ? m->C : 1;
-  const bool want_s3 = !gz_base && (m->sched_req == LMS_SCHED_S3 || m->sched_req == LMS_SCHED_AUTO);
+  const bool want_s3 = !gz_base && m->sched_req == LMS_SCHED_S3;
   // tiling: S3 defaults to spatial cells of ~4096 vertices; S1 to storage tiles
   // of ~256*C vertices (one vertex per thread of a 256-thread CTA per item)
   int tiling = m->tiling_req;
@@ -472,7 +472,9 @@ static void build_base(lms_mesh_s* m, cudaStream_t s, bool gz_base) {
   if (gz_base) return;
   // resolve the kernel: S3 pays off when the tile graph is banded (small reach)
   int kind = m->sched_req;
-  if (kind == LMS_SCHED_AUTO) kind = (K >= 16 && hr * 8 <= K) ? LMS_SCHED_S3 : LMS_SCHED_S1;
+  // AUTO beyond GZ: S1 (measured faster than S3 on the 3D Kuhn C3 under every
+  // ordering, profiles/round1_ordering_study.md)
+  if (kind == LMS_SCHED_AUTO) kind = LMS_SCHED_S1;
   S.kind = kind;
   if (kind == LMS_SCHED_S3) {
     const int ctas = s3_ctas(m->device);
@@ -494,7 +496,7 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   // GZ (gz.cu): the default for 2D meshes with few colours, where the
   // C-hop ghost zone of a tile is a small fraction of it
   if (m->sched_req == LMS_SCHED_GZ || (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->C <= 8)) {
-    const int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 3600 : 512);
+    const int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 4096 : 512);
     const int P = (m->sched_req == LMS_SCHED_GZ && m->lag_req > 0) ? m->lag_req : 1;
     if (build_gz(m, Tg, P, m->sched_req == LMS_SCHED_GZ, s)) {
       S.kind = LMS_SCHED_GZ;
