@@ -65,6 +65,8 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
+#include <cstring>
 #include <utility>
 
 #include "lms_internal.cuh"
@@ -1144,6 +1146,64 @@ static int bits_for(int64_t n) {
   return b;
 }
 
+// ---------------------------------------------------------------- equal-count tiling
+// Tiles of ~T vertices for meshes whose density varies (C5's x -> x^2 grading
+// packs many grid columns into a uniform bin near x = 0): sort the vertices by
+// x and cut equal-count strips, sort each strip by y and cut it into tiles of
+// T.  Tiles are numbered strip-major.  A scheduling device only: results do
+// not depend on the tiling.
+__device__ __forceinline__ uint64_t orderable(double d) {
+  const uint64_t u = (uint64_t)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__global__ void k_kd_xkey(const double* __restrict__ x, int64_t V, uint64_t* key, int32_t* ids) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    key[v] = orderable(x[v]);
+    ids[v] = (int32_t)v;
+  }
+}
+// sorted position p -> strip; key (strip, y)
+__global__ void k_kd_ykey(const int32_t* __restrict__ sorted_ids, const double* __restrict__ y, int64_t V,
+                          int64_t per_strip, uint64_t* key, int32_t* ids) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < V; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = sorted_ids[p];
+    const uint64_t strip = (uint64_t)(p / per_strip);
+    key[p] = (strip << 44) | (orderable(y[v]) >> 20);
+    ids[p] = v;
+  }
+}
+__global__ void k_kd_tile(const int32_t* __restrict__ sorted_ids, int64_t V, int64_t per_strip, int T, int64_t tps,
+                          int32_t* tile_of) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < V; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t strip = p / per_strip;
+    tile_of[sorted_ids[p]] = (int32_t)(strip * tps + (p - strip * per_strip) / T);
+  }
+}
+
+static int64_t kd_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) {
+  sync_soa(m, s);
+  const int64_t V = m->V;
+  const int64_t K0 = std::max<int64_t>(1, (V + T - 1) / T);
+  int64_t nbx = std::max<int64_t>(1, (int64_t)std::llround(std::sqrt((double)K0)));
+  if (nbx > (1 << 19)) nbx = 1 << 19;
+  const int64_t per_strip = (V + nbx - 1) / nbx;
+  const int64_t tps = (per_strip + T - 1) / T;
+  DBuf<uint64_t> k1(V, s), k2(V, s);
+  DBuf<int32_t> i1(V, s), i2(V, s);
+  k_kd_xkey<<<gsz(V), 256, 0, s>>>(m->x[0].p, V, k1.p, i1.p);
+  LMS_CHECK_LAUNCH();
+  size_t tb = 0;
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 64, s));
+  DBuf<char> tmp(tb, s);
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 64, s));
+  k_kd_ykey<<<gsz(V), 256, 0, s>>>(i2.p, m->x[1].p, V, per_strip, k1.p, i1.p);
+  LMS_CHECK_LAUNCH();
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 64, s));
+  k_kd_tile<<<gsz(V), 256, 0, s>>>(i2.p, V, per_strip, T, tps, tile_of);
+  LMS_CHECK_LAUNCH();
+  return nbx * tps;
+}
+
 struct GzNeeds {
   int64_t max_slots = 0, max_items = 0, max_meta16 = 0, max_row = 0;
 };
@@ -1152,7 +1212,7 @@ struct GzNeeds {
 // Returns false (nothing kept) if the limits (region <= 32767 slots, items per
 // tile, `fits`: the shared-memory plan) are not met.
 template <typename Fits>
-static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, cudaStream_t s, GzNeeds* out, Fits fits) {
+static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStream_t s, GzNeeds* out, Fits fits) {
   // LMS_GZ_VERBOSE=2: host-side phase timings (synchronising)
   const bool tv = getenv("LMS_GZ_VERBOSE") && atoi(getenv("LMS_GZ_VERBOSE")) >= 2;
   auto t_last = std::chrono::steady_clock::now();
@@ -1169,7 +1229,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, cudaStream_t s, 
   const int C = m->C;
   const int D = C * P;
   DBuf<int32_t> tile_of(V, s);
-  const int64_t K = spatial_tiles(m, T, tile_of.p, s);
+  const int64_t K = kd ? kd_tiles(m, T, tile_of.p, s) : spatial_tiles(m, T, tile_of.p, s);
   const int kbits = bits_for(K + 1);
   const int end_bit = 32 + kbits;
 
@@ -1465,24 +1525,39 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   const int dim = m->dim, C = m->C;
   GzNeeds nd;
   Schedule& S = m->sched;
-  for (int t = T; t >= 32; t = t * 5 / 8) {
+  // uniform spatial bins first; equal-count (kd) tiles for 2D meshes whose
+  // density varies too much for bins (or LMS_GZ_TILING=kd)
+  const char* te = getenv("LMS_GZ_TILING");
+  const bool kd_only = te && !strcmp(te, "kd");
+  // attempts: bins at T, then (2D) equal-count tiles at T, 4T/5, ...; 3D: bins
+  // at shrinking T
+  std::vector<std::pair<int, int>> tries;
+  if (!kd_only) tries.push_back({0, T});
+  for (int t = T; t >= 32; t = t * 4 / 5)
+    if (dim == 2) tries.push_back({1, t});
+    else if (t != T) tries.push_back({0, t});
+  // two region buffers (load of the next tile overlapping the current one)
+  // are worth a smaller tile; one buffer only as the last resort
+  for (int min_nb = 2; min_nb >= 1; --min_nb)
+  for (const auto& tr : tries) {
+    const int kd = tr.first, t = tr.second;
     // tiles per CTA is bounded by the tile count, known after the build; use
     // an upper bound from the mesh size
     auto fits = [&](const GzNeeds& q) {
       const int64_t K = (m->V + t - 1) / t * 2 + 16;
       const int cap_t = (int)std::min<int64_t>(K / nsm + 2, 1 << 20);
       GzLayout L;
-      return plan_layout(q, dim, C, P, upl, cap, want_nb, nw, cap_t, &L) <= cap;
+      return plan_layout(q, dim, C, P, upl, cap, want_nb, nw, cap_t, &L) <= cap && (want_nb > 0 || L.NB >= min_nb);
     };
-    if (build_gz_once(m, t, P, upl, s, &nd, fits)) {
+    if (build_gz_once(m, t, P, upl, kd != 0, s, &nd, fits)) {
       const int tiles_cap = (int)((S.gz_ntiles + nsm - 1) / nsm) + 1;
       const int64_t total = plan_layout(nd, dim, C, P, upl, cap, want_nb, nw, tiles_cap, &S.gz_L);
-      if (total > cap) continue;
+      if (total > cap || (want_nb == 0 && S.gz_L.NB < min_nb)) continue;
       S.gz_smem = (int)total;
       S.gz_threads = 32 * (2 + S.gz_L.NW);
       if (getenv("LMS_GZ_VERBOSE"))
-        fprintf(stderr, "[gz] T=%d P=%d tiles=%lld items=%lld NB=%d RR=%d NW=%d smem=%d buf=%d slots<=%lld "
-                "items/tile<=%lld regions=%lld updates=%lld blob=%lld B\n", t, P, (long long)S.gz_ntiles,
+        fprintf(stderr, "[gz] %s T=%d P=%d tiles=%lld items=%lld NB=%d RR=%d NW=%d smem=%d buf=%d slots<=%lld "
+                "items/tile<=%lld regions=%lld updates=%lld blob=%lld B\n", kd ? "kd" : "bins", t, P, (long long)S.gz_ntiles,
                 (long long)S.gz_items, S.gz_L.NB, S.gz_L.RR, S.gz_L.NW, S.gz_smem, S.gz_L.buf_bytes,
                 (long long)nd.max_slots, (long long)nd.max_items, (long long)S.gz_nreg, (long long)S.gz_nupd,
                 (long long)S.gz_bytes);

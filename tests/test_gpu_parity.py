@@ -131,6 +131,39 @@ def test_gz_coordinate_updates_between_calls(pair):
         assert bits_equal(gpu_coords(gm), want)
 
 
+def test_gz_equal_count_tiling(pair, monkeypatch):
+    """LMS_GZ_TILING=kd: equal-count strip tiles (the fallback for graded
+    meshes) give the same bit-exact sweeps."""
+    m, om, gm0 = pair
+    if m["dim"] != 2:
+        pytest.skip("equal-count tiling is 2D")
+    monkeypatch.setenv("LMS_GZ_TILING", "kd")
+    want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 4)
+    with gpu_mesh(m) as gm:
+        gm.set_schedule("gz", tile=100, lag=2)
+        gm.smooth(4)
+        assert bits_equal(gpu_coords(gm), want)
+
+
+@pytest.mark.parametrize("upl", [2])
+def test_gz_two_updates_per_lane(pair, upl, monkeypatch):
+    """LMS_GZ_UPL=2: 64-update items (two updates per lane) -- the optional
+    item size of the GZ kernel -- bit-exact under two orderings, P = 1 and 2."""
+    m, om, gm0 = pair
+    if m["dim"] != 2:
+        pytest.skip("two updates per lane is a 2D option")
+    monkeypatch.setenv("LMS_GZ_UPL", str(upl))
+    for kind, P in [("original", 1), ("random", 2)]:
+        perm = oracle.order(om, kind, 803)
+        pm = oracle.permute_mesh(om, perm)
+        want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 5)
+        with gpu_mesh(m) as gm:
+            gm.permute(cuda(perm))
+            gm.set_schedule("gz", tile=128, lag=P)
+            gm.smooth(5)
+            assert bits_equal(gpu_coords(gm), want), (kind, P)
+
+
 def test_cross_ordering_tolerance(pair):
     m, om, gm = pair
     X = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 10)
