@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sweeps", type=int, default=2)
+    p.add_argument("--dist", default="auto", choices=["auto", "deep", "colour"],
+                   help="N>1: deep halo + GZ (2D default) or per-colour exchange + S1")
     return p.parse_args()
 
 
@@ -391,13 +393,16 @@ def run_ours(args):
 
 
 def run_ours_dist(args, m, cfg, sweeps, world, rank, dev):
-    """N > 1: contiguous vertex ranges of the relabelled mesh, one rank per GPU,
-    per-colour halo exchange over NCCL (paper_1606_00803_b200.dist)."""
+    """N > 1: contiguous vertex ranges of the relabelled mesh, one rank per GPU.
+    2D (default): deep halo -- C*P-hop ghost zones, one ghost exchange per
+    pass of P sweeps (NCCL send/recv over NVLink), the GZ kernel on each
+    rank's local mesh.  3D / --dist colour: per-colour exchange + S1 stages."""
     import torch
     import torch.distributed as dist
 
     import paper_1606_00803_b200 as lms
-    from paper_1606_00803_b200.dist import CudaLocal, Plan, smooth_dist
+    from paper_1606_00803_b200.dist import (CudaLocal, CudaLocalDeep, DeepPlan, Plan, smooth_dist,
+                                            smooth_dist_deep)
     stream = torch.cuda.current_stream()
     dim, V = m["dim"], m.V
     gm = lms.Mesh.build_csr([torch.from_numpy(c).to(dev) for c in m["coords"]], torch.from_numpy(m["elems"]).to(dev))
@@ -407,13 +412,26 @@ def run_ours_dist(args, m, cfg, sweeps, world, rank, dev):
     coords = [c.cpu().numpy() for c in gm.coords()]
     info = gm.info()
     gm.close()
-    plan = Plan(rp.cpu().numpy(), col.cpu().numpy(), fixed, colour, world)
-    rplan = plan.rank_plan(rank)
-    local = CudaLocal(rplan, coords, dev)
+    deep = args.dist == "deep" or (args.dist == "auto" and dim == 2)
+    P = max(1, args.lag) if deep else 0
+    if deep:
+        plan = DeepPlan(rp.cpu().numpy(), col.cpu().numpy(), fixed, colour, world, info["C"] * P)
+        rplan = plan.rank_plan(rank)
+        local = CudaLocalDeep(rplan, coords, dev, P=P, tile=args.tile)
+        step = lambda: smooth_dist_deep(local, rplan, sweeps, P)  # noqa: E731
+        how = f"contiguous vertex ranges x{world}, deep halo ({info['C'] * P} hops), one exchange per {P}-sweep pass"
+        kname = "k_sweep_gz + halo pack/unpack"
+    else:
+        plan = Plan(rp.cpu().numpy(), col.cpu().numpy(), fixed, colour, world)
+        rplan = plan.rank_plan(rank)
+        local = CudaLocal(rplan, coords, dev)
+        step = lambda: smooth_dist(local, rplan, plan.C, sweeps)  # noqa: E731
+        how = f"contiguous vertex ranges x{world}, per-colour halo exchange (NCCL p2p)"
+        kname = "k_sweep_s1 (per colour) + halo pack/unpack"
     vfree = int((fixed == 0).sum())
     bsw = b_sweep(dim, V, info["nnz"], vfree)
     for _ in range(args.warmup):
-        smooth_dist(local, rplan, plan.C, sweeps)
+        step()
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
@@ -422,7 +440,7 @@ def run_ours_dist(args, m, cfg, sweeps, world, rank, dev):
         a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.steps):
-            smooth_dist(local, rplan, plan.C, sweeps)
+            step()
         b.record(stream)
         torch.cuda.synchronize()
     launches = lms.kernel_launches() - launches0
@@ -442,11 +460,10 @@ def run_ours_dist(args, m, cfg, sweeps, world, rank, dev):
             "config": {"workload": f"{args.config}: {cfg['args']}, {args.ordering} ordering, {sweeps} sweeps per step",
                        "config": args.config, "ordering": args.ordering, "sweeps_per_step": sweeps,
                        "V": V, "V_free": vfree, "nnz": info["nnz"], "colours": plan.C,
-                       "parallelism": f"contiguous vertex ranges x{world}, per-colour halo exchange (NCCL p2p)",
-                       "l2": "inputs larger than L2; no flush"},
+                       "parallelism": how, "l2": "inputs larger than L2; no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": "k_sweep_s1 (per colour) + halo pack/unpack", "per_gpu": True},
+                         "kernel": kname, "per_gpu": True},
             "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk.record(),
         }
         print(json.dumps(line), flush=True)

@@ -19,6 +19,27 @@ __global__ void k_gather_coords(const double* __restrict__ x, const double* __re
   }
 }
 
+// interleaved (x, y) copies of the 2D GZ path (see gz.cu): gather from the
+// current copy, scatter into both ping-pong copies (a scattered vertex may be
+// fixed for the kernel, which never rewrites it in the partner copy)
+__global__ void k_gather_aos(const double2* __restrict__ a, const int32_t* __restrict__ idx, int64_t n,
+                             double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = a[idx[i]];
+    out[i] = p.x;
+    out[n + i] = p.y;
+  }
+}
+
+__global__ void k_scatter_aos(double2* __restrict__ a, double2* __restrict__ b, const int32_t* __restrict__ idx,
+                              int64_t n, const double* __restrict__ in) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 p = make_double2(in[i], in[n + i]);
+    a[idx[i]] = p;
+    b[idx[i]] = p;
+  }
+}
+
 __global__ void k_scatter_coords(double* __restrict__ x, double* __restrict__ y, double* __restrict__ z,
                                  const int32_t* __restrict__ idx, int64_t n, const double* __restrict__ in) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -56,9 +77,12 @@ lms_status lms_gather_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, doub
     if (!m || (n > 0 && (!d_idx || !d_out)) || n < 0) fail(LMS_E_ARG, "bad argument");
     if (n == 0) return LMS_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    sync_soa(m, s);
-    k_gather_coords<<<grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256), 256, 0, s>>>(
-        m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_out);
+    const unsigned G = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
+    if (m->aos_state == 1) {  // the interleaved copy is current: no conversion of the whole mesh
+      k_gather_aos<<<G, 256, 0, s>>>(reinterpret_cast<const double2*>(m->xy[m->xy_cur].p), d_idx, n, d_out);
+    } else {
+      k_gather_coords<<<G, 256, 0, s>>>(m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_out);
+    }
     LMS_CHECK_LAUNCH();
     return LMS_OK;
   } catch (const Err& e) {
@@ -73,11 +97,17 @@ lms_status lms_scatter_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, con
     if (!m || (n > 0 && (!d_idx || !d_in)) || n < 0) fail(LMS_E_ARG, "bad argument");
     if (n == 0) return LMS_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    sync_soa(m, s);
-    k_scatter_coords<<<grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256), 256, 0, s>>>(
-        m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_in);
-    LMS_CHECK_LAUNCH();
-    soa_changed(m);
+    const unsigned G = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
+    if (m->aos_state != 0) {  // keep the interleaved ping-pong copies current
+      k_scatter_aos<<<G, 256, 0, s>>>(reinterpret_cast<double2*>(m->xy[0].p), reinterpret_cast<double2*>(m->xy[1].p),
+                                      d_idx, n, d_in);
+      LMS_CHECK_LAUNCH();
+    }
+    if (m->aos_state != 1) {
+      k_scatter_coords<<<G, 256, 0, s>>>(m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_in);
+      LMS_CHECK_LAUNCH();
+    }
+    if (m->aos_state == 0) soa_changed(m);
     return LMS_OK;
   } catch (const Err& e) {
     set_error(e.msg);

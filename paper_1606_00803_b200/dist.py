@@ -15,6 +15,15 @@ torch.distributed: NCCL over NVLink on GPUs, gloo on CPU in tests).
 `Plan` is pure host logic (numpy).  `CudaLocal` runs the local steps in the
 CUDA library; tests substitute a CPU implementation of the same three calls to
 check the plan and the exchange with gloo (world size 2) against the oracle.
+
+Deep halo (`DeepPlan`, `smooth_dist_deep`; the default on 2D meshes): the
+ghost zone is D = C * P hops deep (through free vertices), so one exchange per
+pass of P sweeps replaces the C exchanges per sweep, and each rank runs the
+ghost-zone kernel (GZ) on its local mesh.  After P sweeps an owned vertex
+depends on the pass-start values only within D hops (see csrc/gz.cu), all of
+which are local: owned values are exact, ghost values are refreshed by the
+next exchange.  Ghosts at distance exactly D are fixed locally (their rows
+would leave the local mesh); they are only ever read.
 """
 from __future__ import annotations
 
@@ -187,3 +196,121 @@ def smooth_dist(local, plan: RankPlan, C: int, sweeps: int, group=None):
                     req.wait()
             for idx, rb in rbufs:
                 local.unpack(idx, rb)
+
+
+class DeepPlan:
+    """Contiguous partition with a D-hop ghost zone per rank (deep halo)."""
+
+    def __init__(self, row_ptr, col, fixed, colour, parts: int, depth: int):
+        self.row_ptr = np.asarray(row_ptr, dtype=np.int64)
+        self.col = np.asarray(col, dtype=np.int64)
+        self.fixed = np.asarray(fixed, dtype=np.uint8)
+        self.colour = np.asarray(colour, dtype=np.int8)
+        self.parts = parts
+        self.depth = depth
+        self.V = self.row_ptr.shape[0] - 1
+        self.C = int(self.colour.max()) + 1 if (self.colour >= 0).any() else 0
+        self.bounds = partition_bounds(self.fixed, parts)
+        self._local = [self._local_of(r) for r in range(parts)]
+
+    def _neighbours(self, vs):
+        if vs.size == 0:
+            return np.zeros(0, dtype=np.int64)
+        starts, ends = self.row_ptr[vs], self.row_ptr[vs + 1]
+        lens = ends - starts
+        idx = np.repeat(starts - np.cumsum(np.r_[0, lens[:-1]]), lens) + np.arange(int(lens.sum()))
+        return self.col[idx]
+
+    def _local_of(self, r):
+        """(local global ids ascending, hop distance of each) for rank r."""
+        a, b = int(self.bounds[r]), int(self.bounds[r + 1])
+        dist_ = np.full(self.V, -1, dtype=np.int64)
+        owned = np.arange(a, b, dtype=np.int64)
+        dist_[owned] = 0
+        front = owned[self.fixed[owned] == 0]
+        for L in range(1, self.depth + 1):
+            nb = np.unique(self._neighbours(front))
+            new = nb[dist_[nb] < 0]
+            dist_[new] = L
+            front = new[self.fixed[new] == 0]
+        local = np.nonzero(dist_ >= 0)[0]
+        return local, dist_[local]
+
+    def rank_plan(self, r: int) -> RankPlan:
+        a, b = int(self.bounds[r]), int(self.bounds[r + 1])
+        local, dl = self._local[r]
+        n = local.shape[0]
+        # evaluated: free vertices closer than D (their rows stay inside the local mesh)
+        evaluated = (self.fixed[local] == 0) & (dl < self.depth)
+        deg = np.where(evaluated, self.row_ptr[local + 1] - self.row_ptr[local], 1)
+        rp = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(deg, out=rp[1:])
+        colm = np.empty(int(rp[-1]), dtype=np.int64)
+        ev = np.nonzero(evaluated)[0]
+        if ev.size:
+            gl = local[ev]
+            starts = self.row_ptr[gl]
+            lens = self.row_ptr[gl + 1] - starts
+            src = np.repeat(starts - np.cumsum(np.r_[0, lens[:-1]]), lens) + np.arange(int(lens.sum()))
+            dst = np.repeat(rp[ev] - np.cumsum(np.r_[0, lens[:-1]]), lens) + np.arange(int(lens.sum()))
+            colm[dst] = np.searchsorted(local, self.col[src])
+        oth = np.nonzero(~evaluated)[0]
+        if oth.size:
+            colm[rp[oth]] = np.where(oth + 1 < n, oth + 1, oth - 1) if n > 1 else 0
+        fixed = np.where(evaluated, 0, 1).astype(np.uint8)
+        colour = np.where(evaluated, self.colour[local], -1).astype(np.int8)
+        # one exchange per pass: every ghost, from its owner
+        send, recv = [dict()], [dict()]
+        ghosts = local[(local < a) | (local >= b)]
+        for q in range(self.parts):
+            if q == r:
+                continue
+            qa, qb = int(self.bounds[q]), int(self.bounds[q + 1])
+            ql = self._local[q][0]
+            mine = ql[(ql >= a) & (ql < b)]          # q's ghosts that r owns
+            if mine.size:
+                send[0][q] = np.searchsorted(local, mine).astype(np.int32)
+            theirs = ghosts[(ghosts >= qa) & (ghosts < qb)]
+            if theirs.size:
+                recv[0][q] = np.searchsorted(local, theirs).astype(np.int32)
+        return RankPlan(r, self.bounds, local, rp.astype(np.int32), colm.astype(np.int32), fixed, colour, send, recv)
+
+
+def exchange(local, plan: RankPlan, slot: int = 0, group=None):
+    """Send this rank's owned values that peers hold as ghosts; receive its own
+    ghosts (grouped send/recv over torch.distributed)."""
+    ops, rbufs = [], []
+    for q, ids in sorted(plan.send[slot].items()):
+        ops.append(dist.P2POp(dist.isend, local.pack(local.index(("s", slot, q), ids)), q, group))
+    for q, ids in sorted(plan.recv[slot].items()):
+        rb = local.empty(ids.shape[0])
+        rbufs.append((local.index(("r", slot, q), ids), rb))
+        ops.append(dist.P2POp(dist.irecv, rb, q, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for idx, rb in rbufs:
+        local.unpack(idx, rb)
+
+
+def smooth_dist_deep(local, plan: RankPlan, sweeps: int, P: int, group=None):
+    """`sweeps` colour-GS sweeps with a D = C * P deep halo: per pass of up to P
+    sweeps, one ghost exchange, then the local pass (`local.smooth(p)`).
+    Bit-identical to the 1-GPU sweep on the owned vertices."""
+    left = sweeps
+    while left > 0:
+        p = min(P, left)
+        exchange(local, plan, 0, group)
+        local.smooth(p)
+        left -= p
+
+
+class CudaLocalDeep(CudaLocal):
+    """A rank's deep-halo local mesh on its GPU, smoothed by the GZ kernel."""
+
+    def __init__(self, plan: RankPlan, coords, device, P: int = 1, tile: int = 0):
+        super().__init__(plan, coords, device)
+        self.mesh.set_schedule("gz", tile, P)
+
+    def smooth(self, p: int):
+        self.mesh.smooth(p)

@@ -18,7 +18,7 @@ import torch.multiprocessing as mp
 
 import meshgen
 import oracle
-from paper_1606_00803_b200.dist import Plan, partition_bounds, smooth_dist
+from paper_1606_00803_b200.dist import DeepPlan, Plan, partition_bounds, smooth_dist, smooth_dist_deep
 
 
 class NumpyLocal:
@@ -55,6 +55,20 @@ class NumpyLocal:
             self.X[a][i] = b[a * n:(a + 1) * n]
 
 
+class NumpyLocalDeep(NumpyLocal):
+    """Stand-in for the GZ pass on a deep-halo local mesh: p colour-GS sweeps
+    over the locally evaluated vertices (test infrastructure)."""
+
+    def __init__(self, plan, coords, C):
+        super().__init__(plan, coords)
+        self.C = C
+
+    def smooth(self, p):
+        for _ in range(p):
+            for c in range(self.C):
+                self.smooth_colour(c)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -63,7 +77,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, kind, sweeps, out_q):
+def _worker(rank, world, port, kind, sweeps, out_q, P=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     if kind == "grid":
@@ -73,23 +87,32 @@ def _worker(rank, world, port, kind, sweeps, out_q):
     om = oracle.prepare(m)
     perm = oracle.order(om, "bfs", 0)
     pm = oracle.permute_mesh(om, perm)
-    plan = Plan(pm["row_ptr"], pm["col"], pm["fixed"], pm["colour"], world)
-    rp = plan.rank_plan(rank)
-    local = NumpyLocal(rp, pm["coords"])
-    smooth_dist(local, rp, plan.C, sweeps)
+    if P == 0:  # per-colour exchange
+        plan = Plan(pm["row_ptr"], pm["col"], pm["fixed"], pm["colour"], world)
+        rp = plan.rank_plan(rank)
+        local = NumpyLocal(rp, pm["coords"])
+        smooth_dist(local, rp, plan.C, sweeps)
+    else:  # deep halo, one exchange per pass of P sweeps
+        plan = DeepPlan(pm["row_ptr"], pm["col"], pm["fixed"], pm["colour"], world, pm["C"] * P)
+        rp = plan.rank_plan(rank)
+        local = NumpyLocalDeep(rp, pm["coords"], plan.C)
+        smooth_dist_deep(local, rp, sweeps, P)
     owned = [x[rp.owned_local] for x in local.X]
     out_q.put((rank, [o.tolist() for o in owned], plan.bounds.tolist()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind", [(2, "grid"), (3, "grid"), (2, "kuhn")])
-def test_gloo_dist_equals_single_process(world, kind):
+@pytest.mark.parametrize("world,kind,P", [(2, "grid", 0), (3, "grid", 0), (2, "kuhn", 0),
+                                          (2, "grid", 1), (3, "grid", 2), (2, "kuhn", 1)])
+def test_gloo_dist_equals_single_process(world, kind, P):
+    """P = 0: per-colour halo exchange; P >= 1: deep halo (C*P hops), one
+    exchange per pass of P sweeps.  5 sweeps (P = 2: passes 2 + 2 + 1)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    sweeps = 3
-    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, sweeps, q)) for r in range(world)]
+    sweeps = 5 if P else 3
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, sweeps, q, P)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -140,3 +163,36 @@ def test_plan_ghosts_are_exactly_the_read_set():
                 g = rp.local[ids]
                 assert ((g >= plan.bounds[q]) & (g < plan.bounds[q + 1])).all()
                 assert (om["colour"][g] == c).all()
+
+
+def test_deep_plan_ghost_depth_and_rows():
+    """Deep-halo plan: the local mesh is every vertex within D hops (through
+    free vertices) of the owned range; vertices closer than D keep their full
+    global rows (relabelled monotonically), the D-hop ring is fixed locally."""
+    m = meshgen.grid2d(17, 13, 0.3, seed=2)
+    om = oracle.prepare(m)
+    D = 2 * om["C"]
+    plan = DeepPlan(om["row_ptr"], om["col"], om["fixed"], om["colour"], 3, D)
+    import scipy.sparse as sp
+    import scipy.sparse.csgraph as csg
+    V = m.V
+    free = om["fixed"] == 0
+    rows = np.repeat(np.arange(V), np.diff(om["row_ptr"]))
+    # hops are taken only out of free vertices
+    keep = free[rows]
+    A = sp.csr_matrix((np.ones(keep.sum()), (rows[keep], om["col"][keep])), shape=(V, V))
+    for r in range(3):
+        rp = plan.rank_plan(r)
+        a, b = plan.bounds[r], plan.bounds[r + 1]
+        src = [v for v in range(a, b) if free[v]]
+        d = csg.shortest_path(A, unweighted=True, indices=src, directed=True).min(axis=0)
+        d[a:b] = 0
+        want = np.nonzero(d <= D)[0]
+        assert np.array_equal(rp.local, want)
+        for i, g in enumerate(rp.local):
+            if rp.fixed[i] == 0:
+                assert d[g] < D and free[g]
+                row = rp.local[rp.col[rp.row_ptr[i]:rp.row_ptr[i + 1]]]
+                assert np.array_equal(row, om["col"][om["row_ptr"][g]:om["row_ptr"][g + 1]])
+            else:
+                assert d[g] == D or not free[g]
