@@ -18,6 +18,8 @@
 // the dependency chain (about nx + 2 ny vertices on a row-major grid) times a
 // few memory round trips, instead of one grid barrier per JP round.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -112,24 +114,27 @@ __global__ void k_jp_records(const int32_t* __restrict__ rp, const int32_t* __re
 // makes a dependent ready continues with it directly (no queue round trip);
 // other newly ready vertices are pushed.  A warp adds its coloured count to
 // sizes[64] only when it goes idle (before popping), so that counter is not
-// a per-vertex hot spot; the warp whose flush completes n_free writes the stop
-// value -3 into every unfilled slot (continuations consume none), and a
-// waiting warp polls only its own slot.
+// a per-vertex hot spot; the warp whose flush completes n_free raises the
+// done flag sizes[96], which a warp waiting on an unfilled slot (continuations
+// consume no slot, so some slots stay empty) polls besides its slot.
 __global__ void __launch_bounds__(256) k_jp_warp(const int32_t* __restrict__ rec, int RS, int32_t* cnt,
                                                  int8_t* colour, int32_t* Q, int* sizes, int n_free, int* maxc,
-                                                 int* err) {
+                                                 int* err, unsigned long long* stats) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   int mymax = -1, done = 0;
   int32_t v = -1;
+  unsigned long long t_idle = 0, t_work = 0, n_v = 0, n_pop = 0;
+  long long tc = clock64();
   for (;;) {
+    if (stats) { const long long t = clock64(); t_work += t - tc; tc = t; }
     if (v < 0) {  // idle: flush the count, then pop the next queue slot
+      if (stats) ++n_pop;
       int fin = 0;
       if (lane == 0 && done > 0) fin = atomicAdd(&sizes[64], done) + done == n_free;
       done = 0;
       if (__shfl_sync(FULL, fin, 0)) {  // everything coloured: release the waiting warps
-        const int pushed = *(volatile int*)&sizes[0];
-        for (int q = pushed + lane; q < n_free; q += 32) st_release(&Q[q], -3);
+        if (lane == 0) st_release(&sizes[96], 1);
         break;
       }
       int i = 0;
@@ -139,13 +144,16 @@ __global__ void __launch_bounds__(256) k_jp_warp(const int32_t* __restrict__ rec
       if (lane == 0) {
         long long spins = 0;
         while ((v = ld_acquire(&Q[i])) == -1) {  // acquire: pairs with the pusher's release
+          if (ld_acquire(&sizes[96])) { v = -3; break; }  // everything coloured
           if (++spins > (1ll << 31)) { raise_err(err, LMS_E_CUDA); v = -2; break; }  // cannot happen (acyclic)
           __nanosleep(32);
         }
       }
       v = __shfl_sync(FULL, v, 0);
       if (v < 0) break;  // -3: all coloured; -2: error
+      if (stats) { const long long t = clock64(); t_idle += t - tc; tc = t; }
     }
+    if (stats) ++n_v;
     // v's lower-orig_id neighbours' colours are visible (fences around the
     // colour stores and the counter decrements; see below)
     const int32_t* rv = rec + (int64_t)v * RS;
@@ -199,6 +207,12 @@ __global__ void __launch_bounds__(256) k_jp_warp(const int32_t* __restrict__ rec
     v = next;
   }
   if (lane == 0 && mymax >= 0) atomicMax(maxc, mymax);
+  if (stats && lane == 0) {
+    atomicAdd(stats + 0, t_idle);
+    atomicAdd(stats + 1, t_work);
+    atomicAdd(stats + 2, n_v);
+    atomicAdd(stats + 3, n_pop);
+  }
 }
 
 __global__ void k_max_deg(const int32_t* __restrict__ rp, int64_t V, int* out) {
@@ -239,8 +253,8 @@ void compute_colouring(lms_mesh_s* m, cudaStream_t s) {
   } else {
     m->colour.alloc(V, s);
     DBuf<int32_t> cnt(V, s), Q(V, s);
-    DBuf<int> sizes(96, s);
-    LMS_TRY_CUDA(cudaMemsetAsync(sizes.p, 0, 96 * sizeof(int), s));
+    DBuf<int> sizes(128, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(sizes.p, 0, 128 * sizeof(int), s));
     LMS_TRY_CUDA(cudaMemsetAsync(Q.p, 0xff, V * sizeof(int32_t), s));
     k_jp_init<<<Gv, 256, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, m->orig_id.p, V, cnt.p, m->colour.p, Q.p,
                                  sizes.p);
@@ -278,9 +292,25 @@ void compute_colouring(lms_mesh_s* m, cudaStream_t s) {
       int a_n = (int)n_free;
       int* a_max = maxc.p;
       int* a_err = m->err.p;
-      void* args[] = {&a_rec, &a_rs, &a_cnt, &a_colour, &a_q, &a_sizes, &a_n, &a_max, &a_err};
+      unsigned long long* a_stats = nullptr;
+      static unsigned long long* jst = nullptr;
+      if (getenv("LMS_JP_STATS")) {
+        if (!jst) LMS_TRY_CUDA(cudaMalloc(&jst, 4 * sizeof(unsigned long long)));
+        LMS_TRY_CUDA(cudaMemsetAsync(jst, 0, 4 * sizeof(unsigned long long), s));
+        a_stats = jst;
+      }
+      void* args[] = {&a_rec, &a_rs, &a_cnt, &a_colour, &a_q, &a_sizes, &a_n, &a_max, &a_err, &a_stats};
       LMS_TRY_CUDA(cudaLaunchCooperativeKernel((void*)k_jp_warp, dim3(blocks), dim3(threads), args, 0, s));
       LMS_CHECK_LAUNCH();
+      if (a_stats) {
+        unsigned long long h[4];
+        LMS_TRY_CUDA(cudaMemcpyAsync(h, a_stats, sizeof(h), cudaMemcpyDeviceToHost, s));
+        LMS_TRY_CUDA(cudaStreamSynchronize(s));
+        const double nv = h[2] ? (double)h[2] : 1.0;
+        fprintf(stderr, "[jp stats] warps=%d vertices=%llu pops=%llu (continuations %.1f%%) work=%.0f cyc/vertex "
+                "idle=%.0f cyc/warp\n", blocks * threads / 32, h[2], h[3], 100.0 * (1.0 - h[3] / nv), h[1] / nv,
+                h[0] / (blocks * threads / 32.0));
+      }
     }
     k_check_all_coloured<<<Gv, 256, 0, s>>>(m->colour.p, m->fixed.p, V, m->err.p);
     LMS_CHECK_LAUNCH();

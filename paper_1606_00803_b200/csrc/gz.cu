@@ -577,6 +577,10 @@ __device__ __forceinline__ uint32_t ld_stream4(const uint32_t* p, uint64_t pol) 
   return v;
 }
 
+// CTA-scope acquire/release ordering (lighter than __threadfence_block's
+// sequentially consistent fence)
+__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
+
 __device__ __forceinline__ void unpack8(const uint4 q, uint16_t* u) {
   u[0] = (uint16_t)(q.x & 0xffff); u[1] = (uint16_t)(q.x >> 16);
   u[2] = (uint16_t)(q.y & 0xffff); u[3] = (uint16_t)(q.y >> 16);
@@ -611,7 +615,8 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
     const double2* s2 = reinterpret_cast<const double2*>(sc);
     double2 g[RMAX];
 #pragma unroll
-    for (int w = 0; w < RMAX; ++w) g[w] = (u[w] != GZ_PAD) ? s2[u[w]] : make_double2(0.0, 0.0);
+    for (int w = 0; w < RMAX; ++w)
+      if (u[w] != GZ_PAD) g[w] = s2[u[w]];
 #pragma unroll
     for (int w = 0; w < RMAX; ++w)
       if (u[w] != GZ_PAD) {
@@ -691,8 +696,8 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
   double2 ga[RMAX], gb[RMAX];
 #pragma unroll
   for (int w = 0; w < RMAX; ++w) {
-    ga[w] = (ua[w] != GZ_PAD) ? s2[ua[w]] : make_double2(0.0, 0.0);
-    gb[w] = (ub[w] != GZ_PAD) ? s2[ub[w]] : make_double2(0.0, 0.0);
+    if (ua[w] != GZ_PAD) ga[w] = s2[ua[w]];
+    if (ub[w] != GZ_PAD) gb[w] = s2[ub[w]];
   }
   double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
   int da = 0, db = 0;
@@ -748,7 +753,7 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
 // copies of id runs, or 16-byte cp.async gathers), warp 1 streams item
 // records into the record ring (one TMA bulk copy per record, in claim
 // order), warps 2.. are workers (one claimed item at a time).
-template <int DIM, int RMAX, int UPL>
+template <int DIM, int RMAX, int UPL, bool STATS>
 __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
                                                                       const GzTile* __restrict__ tab,
                                                                       const int32_t* __restrict__ item_sweep,
@@ -881,7 +886,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
       __syncwarp();
       if (lane == 0) {
         ndone[b] = 0;
-        __threadfence_block();
+        fence_cta();
         buf_tile[b] = i;
       }
       __syncwarp();
@@ -962,7 +967,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
     }
     const int i = ti;
     const int t = item0 + (kc - pre_lo);
-    const long long c0 = stats ? clock64() : 0;
+    const long long c0 = STATS ? clock64() : 0;
     // the item's record, from the record ring
     const int bat = kc >> bs_log2;
     const int slot = bat & (RR - 1);
@@ -990,7 +995,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
       r[u].gid = (int32_t)pbs[U + pos];
       r[u].desc = desc;
     }
-    const long long c1 = stats ? clock64() : 0;
+    const long long c1 = STATS ? clock64() : 0;
     volatile int* flags = reinterpret_cast<volatile int*>(buf + L.flag_off);
     int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
     const int j = (int)((desc.x >> 8) & 0xffu);
@@ -1012,8 +1017,8 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
       }
     }
     __syncwarp();
-    __threadfence_block();
-    const long long c2 = stats ? clock64() : 0;
+    fence_cta();
+    const long long c2 = STATS ? clock64() : 0;
     double* sc = reinterpret_cast<double*>(buf + L.coord_off);
     const bool last = j == P - 1;
     if (UPL == 2 && DIM == 2) {
@@ -1047,12 +1052,12 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
     __syncwarp();
     if (lane == 0) {
       mbar_arrive(rempty + slot);  // one of the batch's records consumed
-      __threadfence_block();
+      fence_cta();
       flags[t] = i + 1;
       if (desc.z) atomicAdd(cnt + sg, 1);  // stage counters: only tiles with whole-stage waits read them
       if (atomicAdd(ndone + (tb & 0xffff), 1) == pre_hi - pre_lo - 1) mbar_arrive(empty + (tb & 0xffff));
     }
-    if (stats) {
+    if (STATS) {
       const long long c3 = clock64();
       w_wait += c1 - c0;
       w_dep += c2 - c1;
@@ -1060,7 +1065,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
       w_items += 1;
     }
   }
-  if (stats && lane == 0) {
+  if (STATS && lane == 0) {
     atomicAdd(stats + 0, w_wait);
     atomicAdd(stats + 1, w_dep);
     atomicAdd(stats + 2, w_comp);
@@ -1573,7 +1578,8 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
 template <int DIM, int RMAX, int UPL>
 static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
   Schedule& S = m->sched;
-  auto kern = k_sweep_gz<DIM, RMAX, UPL>;
+  const bool want_stats_t = getenv("LMS_GZ_STATS") != nullptr;
+  auto kern = want_stats_t ? k_sweep_gz<DIM, RMAX, UPL, true> : k_sweep_gz<DIM, RMAX, UPL, false>;
   LMS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S.gz_smem));
   int nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));

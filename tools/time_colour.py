@@ -10,7 +10,7 @@ m = meshgen.make_config(cfg)
 coords = [torch.from_numpy(c).cuda() for c in m["coords"]]
 elems = torch.from_numpy(m["elems"]).cuda()
 ts = []
-for r in range(8):
+for r in range(int(os.environ.get("REPS", "8"))):
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record(); g = lms.Mesh.build_csr(coords, elems); b.record(); torch.cuda.synchronize()
     ts.append(a.elapsed_time(b)); C = g.info()["C"]; g.close()
