@@ -53,9 +53,10 @@
 //                         (dep_l: l-th item this one waits for, 0xFFFF none)
 //       i32 gid[32]       global id of lane l's vertex
 //       u32 desc[4]       {n | sweep << 8 | stage << 16, mode, tile counts
-//                         stages, 0}; mode 1 = wait for whole stages (more
-//                         than U deps); then every item of that tile
-//                         increments the per-stage completion counters
+//                         stages, number of dependencies}; mode 1 = wait for
+//                         whole stages (more than 2U deps); then every item of
+//                         that tile increments the per-stage completion counters
+//       u16 dep2[32]      the dependencies beyond the first U
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -83,8 +84,10 @@ constexpr int GZ_MAX_REGION = 32767;  // slots are 15 bits (bit 15 = owned flag)
 
 __host__ __device__ inline int64_t r4(int64_t n) { return (n + 3) & ~(int64_t)3; }
 __host__ __device__ inline int gz_hdr_words(int C, int P) { return (int)r4(4 + P * C + 1); }
-// record bytes for rows of R and U positions: rows, pb, gid, descriptor
-__host__ __device__ inline int gz_rec16(int R, int U) { return (2 * U * R + 8 * U + 16) / 16; }
+// record bytes for rows of R and U positions: rows, pb, gid, descriptor,
+// second dependency slot per position (u16)
+__host__ __device__ inline int gz_rec16(int R, int U) { return (2 * U * R + 8 * U + 16 + 2 * U) / 16; }
+__host__ __device__ inline int gz_dep2_off(int R, int U) { return 2 * U * R + 8 * U + 16; }
 
 
 // ---------------------------------------------------------------- build kernels
@@ -486,14 +489,18 @@ __global__ void k_gzd_deps(const int32_t* __restrict__ it_ks, int64_t NI, int C,
     uint32_t* desc = reinterpret_cast<uint32_t*>(base + 2 * U * t.R + 8 * U);
     const int lo = it_lo[it], hi = it_hi[it];
     const int64_t a = sfirst[k * PC + (sg - C > 0 ? sg - C : 0)], b = sfirst[k * PC + sg];
+    uint16_t* dep2 = reinterpret_cast<uint16_t*>(base + gz_dep2_off(t.R, U));
+    for (int e = 0; e < U; ++e) dep2[e] = 0xffffu;
     int nd = 0;
     for (int64_t o = a; o < b; ++o)
       if (it_lo[o] <= hi && it_hi[o] >= lo) {
         if (nd < U) pb[nd] = (pb[nd] & 0xffffu) | ((uint32_t)(o - f0) << 16);
+        else if (nd < 2 * U) dep2[nd - U] = (uint16_t)(o - f0);
         ++nd;
       }
-    desc[1] = nd > U ? 1u : 0u;
-    if (nd > U) atomicOr(&tneed[k], 1);
+    desc[1] = nd > 2 * U ? 1u : 0u;
+    desc[3] = (uint32_t)nd;  // (informational: the number of overlapping earlier items)
+    if (nd > 2 * U) atomicOr(&tneed[k], 1);
   }
 }
 
@@ -509,6 +516,115 @@ __global__ void k_gzd_mark(const int32_t* __restrict__ it_ks, int64_t NI, int C,
     unsigned char* base = reinterpret_cast<unsigned char*>(rec + t.rec_base + (it - sfirst[k * PC]) * t.rec16);
     reinterpret_cast<uint32_t*>(base + 2 * U * t.R + 8 * U)[2] = (uint32_t)tneed[k];
   }
+}
+
+// Claim order inside a tile (skewed stages).  Stage-major claiming makes
+// every item of stage s wait for its still-running neighbours of stage s - 1;
+// ordering the items of a sweep by lo + c * L instead (lo = start of the
+// item's touched slot interval, c its colour, L = the tile's widest interval
+// + 1) interleaves the stages as a wavefront, so an item's dependencies were
+// claimed about L slots' worth of items earlier.  Still a topological order:
+// a dependency d of item i (earlier colour, overlapping interval) has
+// lo_d <= hi_i < lo_i + L, hence lo_d + c_d * L < lo_i + c_i * L.  Sweeps stay
+// contiguous (the partial passes skip whole sweeps).
+__global__ void k_gzd_span(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P,
+                           const int32_t* __restrict__ it_lo, const int32_t* __restrict__ it_hi, int* tspan) {
+  const int PC = P * C;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < NI; it += (int64_t)gridDim.x * blockDim.x)
+    atomicMax(&tspan[it_ks[it] / PC], it_hi[it] - it_lo[it] + 1);
+}
+
+__global__ void k_gzd_scale(int* v, int64_t n, int f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] *= f;
+}
+
+__global__ void k_gzd_order_key(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P,
+                                const int32_t* __restrict__ it_lo, const int* __restrict__ tspan,
+                                const int* __restrict__ tneed, const int64_t* __restrict__ sfirst, uint64_t* key,
+                                int32_t* val) {
+  const int PC = P * C;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < NI; it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = it_ks[it] / PC;
+    const int sg = (int)(it_ks[it] - k * PC);
+    const int j = sg / C, c = sg - j * C;
+    // tiles with whole-stage waits keep stage-major order (such a wait needs
+    // every item of the earlier stages claimed before it)
+    const uint64_t pos = tneed[k] ? ((uint64_t)c << 16) | (uint64_t)(it - sfirst[k * PC])
+                                  : (uint64_t)it_lo[it] + (uint64_t)c * (uint64_t)tspan[k];  // < 2^21
+    key[it] = ((uint64_t)k << 28) | ((uint64_t)j << 25) | pos;
+    val[it] = (int32_t)it;
+  }
+}
+
+// new[p] = record of old item val[p]; dependency ids remapped to the new order
+__global__ void k_gzd_permute(const int32_t* __restrict__ it_ks, const int32_t* __restrict__ val, int64_t NI,
+                              int C, int P, int U, const GzTile* __restrict__ tab,
+                              const int64_t* __restrict__ sfirst, const int32_t* __restrict__ newpos,
+                              const uint4* __restrict__ rec, uint4* out) {
+  const int PC = P * C;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = w0; p < NI; p += nw) {
+    const int64_t old = val[p];
+    const int64_t k = it_ks[old] / PC;
+    const GzTile t = tab[k];
+    const int64_t f0 = sfirst[k * PC];
+    const uint4* src = rec + t.rec_base + (old - f0) * t.rec16;
+    uint4* dst = out + t.rec_base + (p - f0) * t.rec16;
+    for (uint32_t q = lane; q < t.rec16; q += 32) dst[q] = src[q];
+    __syncwarp();
+    uint32_t* pb = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + 2 * U * t.R);
+    uint16_t* dep2 = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(dst) + gz_dep2_off(t.R, U));
+    for (int e = lane; e < U; e += 32) {
+      const uint32_t d = pb[e] >> 16;
+      if (d != 0xffffu) pb[e] = (pb[e] & 0xffffu) | ((uint32_t)(newpos[f0 + d] - f0) << 16);
+      const uint32_t d2 = dep2[e];
+      if (d2 != 0xffffu) dep2[e] = (uint16_t)(newpos[f0 + d2] - f0);
+    }
+  }
+}
+
+// every dependency of an item must precede it in claim order (else fall back)
+__global__ void k_gzd_check_order(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P, int U,
+                                  const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
+                                  const uint4* __restrict__ rec, unsigned long long* bad) {
+  const int PC = P * C;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < NI; it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = it_ks[it] / PC;
+    const GzTile t = tab[k];
+    const int64_t loc = it - sfirst[k * PC];
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(rec + t.rec_base + loc * t.rec16);
+    const uint32_t* pb = reinterpret_cast<const uint32_t*>(base + 2 * U * t.R);
+    const uint16_t* dep2 = reinterpret_cast<const uint16_t*>(base + gz_dep2_off(t.R, U));
+    for (int e = 0; e < U; ++e) {
+      const uint32_t d = pb[e] >> 16, d2 = dep2[e];
+      if (d != 0xffffu && (int64_t)d >= loc) atomicAdd(bad, 1ull);
+      if (d2 != 0xffffu && (int64_t)d2 >= loc) atomicAdd(bad, 1ull);
+    }
+  }
+}
+
+__global__ void k_gzd_dep_hist(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P, int U,
+                               const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
+                               const uint4* __restrict__ rec, unsigned long long* hist /*[8]*/) {
+  const int PC = P * C;
+  for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < NI; it += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = it_ks[it] / PC;
+    const GzTile t = tab[k];
+    const unsigned char* base =
+        reinterpret_cast<const unsigned char*>(rec + t.rec_base + (it - sfirst[k * PC]) * t.rec16);
+    const uint32_t nd = reinterpret_cast<const uint32_t*>(base + 2 * U * t.R + 8 * U)[3];
+    const int b = nd == 0 ? 0 : nd <= 8 ? 1 : nd <= 16 ? 2 : nd <= 32 ? 3 : nd <= 64 ? 4 : nd <= 128 ? 5 : 6;
+    atomicAdd(hist + b, 1ull);
+    atomicAdd(hist + 7, (unsigned long long)nd);
+  }
+}
+
+__global__ void k_gzd_inverse(const int32_t* __restrict__ val, int64_t NI, int32_t* newpos) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < NI; p += (int64_t)gridDim.x * blockDim.x)
+    newpos[val[p]] = (int32_t)p;
 }
 
 __global__ void k_gzd_nonempty(const int64_t* __restrict__ nslots, int64_t K, uint8_t* flag, int32_t* ids) {
@@ -551,6 +667,42 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
+}
+// Watchdog for every wait of k_sweep_gz: a wait that outlives ~2^25 polls
+// (seconds) raises LMS_E_CUDA in the handle's error flag and every waiter
+// then leaves the kernel, so a schedule bug surfaces as an error instead of a
+// hung GPU.
+struct GzGuard {
+  int* gabort;          // global error flag (the handle's)
+  volatile int* sabort; // CTA-local copy
+  long long n = 0;
+  __device__ bool ok() {
+    ++n;
+    if ((n & 255) == 0 && (*sabort || *(volatile int*)gabort)) {
+      *sabort = 1;
+      return false;
+    }
+    if (n > (1ll << 25)) {
+      atomicCAS(gabort, 0, (int)LMS_E_CUDA);
+      *sabort = 1;
+      return false;
+    }
+    __nanosleep(n < 64 ? 20 : 128);
+    return true;
+  }
+};
+__device__ __forceinline__ bool mbar_wait_g(uint64_t* b, uint32_t parity, GzGuard& g) {
+  const uint32_t a = smem_u32(b);
+  for (;;) {
+    uint32_t done = 0;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) return true;
+    if (!g.ok()) return false;
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -767,8 +919,10 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
                                                                       double* __restrict__ x1,
                                                                       double* __restrict__ y1,
                                                                       double* __restrict__ z1, int C, int P, int j0,
-                                                                      GzLayout L, unsigned long long* stats) {
+                                                                      GzLayout L, unsigned long long* stats,
+                                                                      int* gabort) {
   extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ int s_abort;
   const int NB = L.NB, RR = L.RR;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);     // [NB] region coordinates of the buffer's tile landed
   uint64_t* empty = full + NB;                          // [NB] buffer's tile finished
@@ -792,6 +946,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
   const int HW = gz_hdr_words(C, P);
 
   if (threadIdx.x == 0) {
+    s_abort = 0;
     for (int b = 0; b < NB; ++b) {
       mbar_init(full + b, 32);
       mbar_init(empty + b, 1);
@@ -830,12 +985,13 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
   }
   __syncthreads();
   const int total = t_pre[n_my];
+  GzGuard guard{gabort, &s_abort};
 
   if (warp == 0) {  // -------------------------------------------- region producer
     for (int i = 0; i < n_my; ++i) {
       const int b = i % NB;
       const uint32_t ph = (uint32_t)(i / NB) & 1u;
-      if (i >= NB) mbar_wait(empty + b, ph ^ 1u);
+      if (i >= NB && !mbar_wait_g(empty + b, ph ^ 1u, guard)) return;
       const int k = tiles[blockIdx.x + (long long)i * gridDim.x];
       const GzTile t = tab[k];
       const uint32_t bytes = t.meta16 * 16u;
@@ -847,7 +1003,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
         for (uint32_t o = 0; o < bytes; o += PIECE)
           bulk_g2s(stg + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, sbar);
       }
-      mbar_wait(sbar, (uint32_t)i & 1u);
+      if (!mbar_wait_g(sbar, (uint32_t)i & 1u, guard)) return;
       unsigned char* buf = sm + L.off_ring + (size_t)b * L.buf_bytes;
       const uint32_t* hsrc = reinterpret_cast<const uint32_t*>(stg);
       uint32_t* hdst = reinterpret_cast<uint32_t*>(buf);
@@ -904,7 +1060,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
       const int nbat = (total + BS - 1) / BS;
       for (int g = 0; g < nbat; ++g) {
         const int slot = g & (RR - 1);  // RR is a power of two
-        if (g >= RR) mbar_wait(rempty + slot, ((uint32_t)(g >> L.RR_log2) & 1u) ^ 1u);
+        if (g >= RR && !mbar_wait_g(rempty + slot, ((uint32_t)(g >> L.RR_log2) & 1u) ^ 1u, guard)) return;
         const int k0 = g * BS, k1 = min(total, k0 + BS);
         uint32_t bytes = 0;
         for (int kc = k0, tj = ti; kc < k1;) {  // pass 1: bytes of the batch
@@ -973,15 +1129,16 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
     const int slot = bat & (RR - 1);
     const unsigned char* rbase =
         rring + ((size_t)slot * L.BS + (kc & (L.BS - 1))) * L.rec_bytes;
+    int alive = 1;
     if (lane == 0) {
-      mbar_wait(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u);
-      if (!tile_ready) {  // the region of the item's tile
-        while (buf_tile[tb & 0xffff] != i) __nanosleep(32);
-        mbar_wait(full + (tb & 0xffff), (uint32_t)(tb >> 16));
+      alive = mbar_wait_g(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u, guard);
+      if (alive && !tile_ready) {  // the region of the item's tile
+        while (alive && buf_tile[tb & 0xffff] != i) alive = guard.ok();
+        alive = alive && mbar_wait_g(full + (tb & 0xffff), (uint32_t)(tb >> 16), guard);
       }
     }
+    if (!__shfl_sync(FULL, alive, 0)) return;
     tile_ready = true;
-    __syncwarp();
     GzRec<RMAX> r[UPL];
     const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rbase + 2 * U * R);
     const uint4 desc = *reinterpret_cast<const uint4*>(rbase + 2 * U * R + 8 * U);
@@ -1001,22 +1158,27 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
     const int j = (int)((desc.x >> 8) & 0xffu);
     const int sg = (int)(desc.x >> 16);
     // this item's dependencies
+    alive = 1;
     if (desc.y == 0) {
+      const uint16_t* dep2 = reinterpret_cast<const uint16_t*>(rbase + gz_dep2_off(R, U));
 #pragma unroll
       for (int u = 0; u < UPL; ++u) {
         const int dep = (int)(r[u].pb >> 16);
         if (dep != 0xffff && dep >= item0)
-          while (flags[dep] != i + 1) __nanosleep(20);
+          while (alive && flags[dep] != i + 1) alive = guard.ok();
+        const int d2 = dep2[lane + 32 * u];
+        if (d2 != 0xffff && d2 >= item0)
+          while (alive && flags[d2] != i + 1) alive = guard.ok();
       }
     } else if (lane == 0) {
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(buf);
       const int s0 = max(sg - C, j0 * C);
-      for (int s2 = s0; s2 < sg; ++s2) {
+      for (int s2 = s0; s2 < sg && alive; ++s2) {
         const int need = (int)(hdr[4 + s2 + 1] - hdr[4 + s2]);
-        while (*(volatile int*)(cnt + s2) != need) __nanosleep(20);
+        while (alive && *(volatile int*)(cnt + s2) != need) alive = guard.ok();
       }
     }
-    __syncwarp();
+    if (!__all_sync(FULL, alive)) return;
     fence_cta();
     const long long c2 = STATS ? clock64() : 0;
     double* sc = reinterpret_cast<double*>(buf + L.coord_off);
@@ -1421,6 +1583,64 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
     LMS_CHECK_LAUNCH();
     k_gzd_mark<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, 32 * upl, tab.p, sfirst.p, tneed.p, rec.p);
     LMS_CHECK_LAUNCH();
+    // skewed claim order inside each tile (LMS_GZ_SKEW=f >= 1; default off:
+    // measured no faster on C4 -- the other warps already hide the dependency
+    // waits -- so the stage-major order is kept)
+    const char* ske = getenv("LMS_GZ_SKEW");
+    if (ske && atoi(ske) >= 1) {
+      DBuf<int> tspan(K > 0 ? K : 1, s);
+      LMS_TRY_CUDA(cudaMemsetAsync(tspan.p, 0, (K > 0 ? K : 1) * sizeof(int), s));
+      k_gzd_span<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, it_lo.p, it_hi.p, tspan.p);
+      LMS_CHECK_LAUNCH();
+      // L = factor x the widest interval: each dependency then lies at least
+      // (factor - 1) interval widths earlier in claim order (LMS_GZ_SKEW)
+      const int factor = std::max(1, std::min(8, atoi(ske)));
+      if (factor > 1) {
+        k_gzd_scale<<<gsz(K), 256, 0, s>>>(tspan.p, K, factor);
+        LMS_CHECK_LAUNCH();
+      }
+      DBuf<uint64_t> key(NI, s), key2(NI, s);
+      DBuf<int32_t> val(NI, s), val2(NI, s), newpos(NI, s);
+      k_gzd_order_key<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, it_lo.p, tspan.p, tneed.p, sfirst.p, key.p,
+                                              val.p);
+      LMS_CHECK_LAUNCH();
+      size_t tb = 0;
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, val.p, val2.p, NI, 0, 28 + kbits, s));
+      DBuf<char> tmp(tb, s);
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key2.p, val.p, val2.p, NI, 0, 28 + kbits, s));
+      k_gzd_inverse<<<gsz(NI), 256, 0, s>>>(val2.p, NI, newpos.p);
+      LMS_CHECK_LAUNCH();
+      DBuf<uint4> rec2(rec16_all > 0 ? rec16_all : 1, s);
+      k_gzd_permute<<<gsz(NI * 32), 256, 0, s>>>(it_ks.p, val2.p, NI, C, P, 32 * upl, tab.p, sfirst.p, newpos.p,
+                                                 rec.p, rec2.p);
+      LMS_CHECK_LAUNCH();
+      DBuf<unsigned long long> bad(1, s);
+      LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
+      k_gzd_check_order<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, 32 * upl, tab.p, sfirst.p, rec2.p, bad.p);
+      LMS_CHECK_LAUNCH();
+      const int64_t nbad = read_i64(bad.p, true, s);
+      if (getenv("LMS_GZ_VERBOSE")) {
+        DBuf<int> nt(1, s);
+        size_t tb3 = 0;
+        LMS_TRY_CUDA(cub::DeviceReduce::Sum(nullptr, tb3, tneed.p, nt.p, K, s));
+        DBuf<char> tmp3(tb3, s);
+        LMS_TRY_CUDA(cub::DeviceReduce::Sum(tmp3.p, tb3, tneed.p, nt.p, K, s));
+        fprintf(stderr, "[gz] tiles with whole-stage waits (kept stage-major): %lld of %lld\n",
+                (long long)read_i64(nt.p, false, s), (long long)K);
+        DBuf<unsigned long long> hist(8, s);
+        LMS_TRY_CUDA(cudaMemsetAsync(hist.p, 0, 8 * sizeof(unsigned long long), s));
+        k_gzd_dep_hist<<<gsz(NI), 256, 0, s>>>(it_ks.p, NI, C, P, 32 * upl, tab.p, sfirst.p, rec.p, hist.p);
+        LMS_CHECK_LAUNCH();
+        unsigned long long hh[8];
+        LMS_TRY_CUDA(cudaMemcpyAsync(hh, hist.p, sizeof(hh), cudaMemcpyDeviceToHost, s));
+        LMS_TRY_CUDA(cudaStreamSynchronize(s));
+        fprintf(stderr, "[gz] deps per item: 0:%llu 1-8:%llu 9-16:%llu 17-32:%llu 33-64:%llu 65-128:%llu >128:%llu "
+                "mean %.1f\n", hh[0], hh[1], hh[2], hh[3], hh[4], hh[5], hh[6], (double)hh[7] / (double)NI);
+      }
+      if (nbad == 0) rec = std::move(rec2);
+      else if (getenv("LMS_GZ_VERBOSE"))
+        fprintf(stderr, "[gz] skewed order rejected: %lld dependencies point forward\n", (long long)nbad);
+    }
   }
   mark("records+deps");
   // the non-empty tiles, in tile order
@@ -1597,7 +1817,7 @@ static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
       S.gz_tiles.p, (int)S.gz_ntiles, S.gz_tab.p, S.gz_item_sweep.p, S.gz_meta.p, S.gz_rec.p, a0, a1, m->x[0].p,
       m->x[1].p, DIM == 3 ? m->x[2].p : nullptr, DIM == 3 ? m->xalt[0].p : nullptr,
       DIM == 3 ? m->xalt[1].p : nullptr, DIM == 3 ? m->xalt[2].p : nullptr, m->C, S.gz_P, j0, S.gz_L,
-      want_stats ? stats : nullptr);
+      want_stats ? stats : nullptr, m->err.p);
   LMS_CHECK_LAUNCH();
   if (want_stats) {
     unsigned long long h[8];
@@ -1681,6 +1901,8 @@ void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s) {
     }
     left -= r;
   }
+  // the kernel's watchdog reports a stuck wait through the handle's error flag
+  check_err_flag(m, s, "lms_smooth (GZ watchdog: a wait exceeded its budget)");
 }
 
 }  // namespace lms
