@@ -246,8 +246,10 @@ __global__ void k_gzd_item_map(const int64_t* __restrict__ sfirst, int64_t nks, 
     }
 }
 
+static int env_int(const char* name, int dflt, int lo, int hi);
+
 // per tile: table entry, record / meta sizes (16-byte units)
-__global__ void k_gzd_tile_sizes(int64_t K, int C, int P, int dim, int U, const int* __restrict__ tR,
+__global__ void k_gzd_tile_sizes(int64_t K, int C, int P, int dim, int U, int run_min, const int* __restrict__ tR,
                                  const int64_t* __restrict__ sfirst, const int64_t* __restrict__ reg_off,
                                  const int64_t* __restrict__ rs, int64_t* rec_sz, int64_t* meta_sz, int64_t* nitems,
                                  int64_t* nslots, int64_t* nruns) {
@@ -261,7 +263,7 @@ __global__ void k_gzd_tile_sizes(int64_t K, int C, int P, int dim, int U, const 
     nslots[k] = nr;
     rec_sz[k] = ni * gz_rec16(R, U);
     const int64_t runs = rs[reg_off[k + 1]] - rs[reg_off[k]];
-    const bool use_runs = dim == 2 && runs > 0 && nr >= 4 * runs;  // 2D (interleaved) and runs long enough
+    const bool use_runs = dim == 2 && runs > 0 && nr >= run_min * runs;  // 2D (interleaved) and runs long enough
     nruns[k] = use_runs ? runs : 0;
     meta_sz[k] = nr > 0 ? (4 * (int64_t)HW + (use_runs ? 8 * runs : 4 * r4(nr)) + 15) / 16 : 0;
   }
@@ -690,6 +692,21 @@ struct GzGuard {
     __nanosleep(n < 64 ? 20 : 128);
     return true;
   }
+  // for mbarrier waits: try_wait already suspends the thread in hardware
+  // until the phase completes (or a time limit), so no sleep on top of it
+  __device__ bool ok_spin() {
+    ++n;
+    if ((n & 255) == 0 && (*sabort || *(volatile int*)gabort)) {
+      *sabort = 1;
+      return false;
+    }
+    if (n > (1ll << 25)) {
+      atomicCAS(gabort, 0, (int)LMS_E_CUDA);
+      *sabort = 1;
+      return false;
+    }
+    return true;
+  }
 };
 __device__ __forceinline__ bool mbar_wait_g(uint64_t* b, uint32_t parity, GzGuard& g) {
   const uint32_t a = smem_u32(b);
@@ -701,7 +718,7 @@ __device__ __forceinline__ bool mbar_wait_g(uint64_t* b, uint32_t parity, GzGuar
         : "r"(a), "r"(parity)
         : "memory");
     if (done) return true;
-    if (!g.ok()) return false;
+    if (!g.ok_spin()) return false;
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
@@ -751,31 +768,69 @@ struct GzRec {
   int t;      // item index inside the tile
 };
 
+// Predicated shared-memory loads: a lane whose neighbour position is padding
+// issues no access and keeps -0.0, the identity of IEEE addition (x + -0.0 ==
+// x bit for bit, for every x), so the ordered sums need no per-neighbour
+// branch and every gather of an update is in flight at once.
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a, bool p) {
+  double2 v = make_double2(-0.0, -0.0);
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %3, 0; @q ld.shared.v2.f64 {%0, %1}, [%2];}"
+               : "+d"(v.x), "+d"(v.y)
+               : "r"(a), "r"((uint32_t)p));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a, bool p) {
+  double v = -0.0;
+  asm volatile("{.reg .pred q; setp.ne.u32 q, %2, 0; @q ld.shared.f64 %0, [%1];}" : "+d"(v) : "r"(a), "r"((uint32_t)p));
+  return v;
+}
+
+// Eq. 1's division x / d, correctly rounded, from r = RN(1/d) (the table
+// rcp[d], d <= GZ_RCP_MAX): q = RN(x r) is within one ulp of x/d, the
+// remainder x - q d is exact under FMA, and RN(q + (x - q d) r) = RN(x/d)
+// (Markstein's correction theorem).  Needs x normal and away
+// from the exponent range's ends: zero, subnormal, huge, inf and NaN sums take
+// __ddiv_rn instead (gz_div_ok).
+constexpr int GZ_RCP_MAX = 32;
+__device__ __forceinline__ bool gz_div_ok(double x) {
+  const uint32_t e = ((uint32_t)__double2hiint(x) >> 20) & 0x7ffu;
+  return e - 64u < 0x7ffu - 64u;  // 2^-959 <= |x| < 2^1024, finite
+}
+__device__ __forceinline__ double gz_div(double x, double d, double r) {
+  const double q = __dmul_rn(x, r);
+  const double e = __fma_rn(-q, d, x);
+  return __fma_rn(e, r, q);
+}
+
 // Eq. 1 for this lane's update: neighbours (CSR order) from shared memory,
-// ordered IEEE adds, IEEE division, result back to shared memory; returns the
-// new value through (ox, oy, oz).
+// ordered IEEE adds, correctly rounded division, result back to shared
+// memory; returns the new value through (ox, oy, oz).
 template <int DIM, int RMAX>
 __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uint4* __restrict__ rowg, double* sc,
-                                          int nr4, double& ox, double& oy, double& oz) {
+                                          const double* rcp, int nr4, double& ox, double& oy, double& oz) {
   const int v = (int)(r.pb & 0x7fffu);
   uint16_t u[RMAX];
 #pragma unroll
   for (int p = 0; p < RMAX / 8; ++p) unpack8(r.row[p], u + 8 * p);
-  double sx = 0.0, sy = 0.0, sz = 0.0;
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sc);
+  double sx, sy, sz = 0.0;
   int d = 0;
   if (DIM == 2) {
-    const double2* s2 = reinterpret_cast<const double2*>(sc);
     double2 g[RMAX];
 #pragma unroll
-    for (int w = 0; w < RMAX; ++w)
-      if (u[w] != GZ_PAD) g[w] = s2[u[w]];
+    for (int w = 0; w < RMAX; ++w) {
+      const bool ok = u[w] != GZ_PAD;
+      g[w] = lds_f64x2(sb + 16u * u[w], ok);
+      d += ok;
+    }
+    sx = g[0].x;
+    sy = g[0].y;
 #pragma unroll
-    for (int w = 0; w < RMAX; ++w)
-      if (u[w] != GZ_PAD) {
-        if (w == 0) { sx = g[w].x; sy = g[w].y; }
-        else { sx = __dadd_rn(sx, g[w].x); sy = __dadd_rn(sy, g[w].y); }
-        ++d;
-      }
+    for (int w = 1; w < RMAX; ++w) {
+      sx = __dadd_rn(sx, g[w].x);
+      sy = __dadd_rn(sy, g[w].y);
+    }
+    const double2* s2 = reinterpret_cast<const double2*>(sc);
     for (int p = RMAX / 8; p * 8 < R; ++p) {  // rows longer than RMAX: ordered tail from global
       uint16_t t[8];
       unpack8(rowg[p], t);
@@ -787,25 +842,34 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
       }
     }
     const double dd = (double)d;
-    ox = __ddiv_rn(sx, dd);
-    oy = __ddiv_rn(sy, dd);
+    const double rr = rcp[d <= GZ_RCP_MAX ? d : 0];
+    if (d >= 1 && d <= GZ_RCP_MAX && gz_div_ok(sx) && gz_div_ok(sy)) {
+      ox = gz_div(sx, dd, rr);
+      oy = gz_div(sy, dd, rr);
+    } else {
+      ox = __ddiv_rn(d ? sx : 0.0, dd);
+      oy = __ddiv_rn(d ? sy : 0.0, dd);
+    }
     reinterpret_cast<double2*>(sc)[v] = make_double2(ox, oy);
   } else {
     double gx[RMAX], gy[RMAX], gz[RMAX];
 #pragma unroll
     for (int w = 0; w < RMAX; ++w) {
       const bool ok = u[w] != GZ_PAD;
-      gx[w] = ok ? sc[u[w]] : 0.0;
-      gy[w] = ok ? sc[nr4 + u[w]] : 0.0;
-      gz[w] = ok ? sc[2 * nr4 + u[w]] : 0.0;
+      gx[w] = lds_f64(sb + 8u * u[w], ok);
+      gy[w] = lds_f64(sb + 8u * (nr4 + u[w]), ok);
+      gz[w] = lds_f64(sb + 8u * (2 * nr4 + u[w]), ok);
+      d += ok;
     }
+    sx = gx[0];
+    sy = gy[0];
+    sz = gz[0];
 #pragma unroll
-    for (int w = 0; w < RMAX; ++w)
-      if (u[w] != GZ_PAD) {
-        if (w == 0) { sx = gx[w]; sy = gy[w]; sz = gz[w]; }
-        else { sx = __dadd_rn(sx, gx[w]); sy = __dadd_rn(sy, gy[w]); sz = __dadd_rn(sz, gz[w]); }
-        ++d;
-      }
+    for (int w = 1; w < RMAX; ++w) {
+      sx = __dadd_rn(sx, gx[w]);
+      sy = __dadd_rn(sy, gy[w]);
+      sz = __dadd_rn(sz, gz[w]);
+    }
     for (int p = RMAX / 8; p * 8 < R; ++p) {
       uint16_t t[8];
       unpack8(rowg[p], t);
@@ -817,9 +881,16 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
       }
     }
     const double dd = (double)d;
-    ox = __ddiv_rn(sx, dd);
-    oy = __ddiv_rn(sy, dd);
-    oz = __ddiv_rn(sz, dd);
+    const double rr = rcp[d <= GZ_RCP_MAX ? d : 0];
+    if (d >= 1 && d <= GZ_RCP_MAX && gz_div_ok(sx) && gz_div_ok(sy) && gz_div_ok(sz)) {
+      ox = gz_div(sx, dd, rr);
+      oy = gz_div(sy, dd, rr);
+      oz = gz_div(sz, dd, rr);
+    } else {
+      ox = __ddiv_rn(d ? sx : 0.0, dd);
+      oy = __ddiv_rn(d ? sy : 0.0, dd);
+      oz = __ddiv_rn(d ? sz : 0.0, dd);
+    }
     sc[v] = ox;
     sc[nr4 + v] = oy;
     sc[2 * nr4 + v] = oz;
@@ -827,44 +898,37 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
 }
 
 // Two updates per lane (2D): the lane's update of item A and of item B, with
-// all sixteen gathers issued before the two ordered sums (more loads in flight
+// all gathers of both issued before the two ordered sums (more loads in flight
 // per warp, two independent FP64 add chains per axis).
 template <int RMAX>
 __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const GzRec<RMAX>& rb, bool vb, int R,
                                            const uint4* __restrict__ rowgA, const uint4* __restrict__ rowgB,
-                                           double* sc, double2& oa, double2& ob) {
+                                           double* sc, const double* rcp, double2& oa, double2& ob) {
   double2* s2 = reinterpret_cast<double2*>(sc);
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sc);
   uint16_t ua[RMAX], ub[RMAX];
 #pragma unroll
   for (int p = 0; p < RMAX / 8; ++p) {
     unpack8(ra.row[p], ua + 8 * p);
     unpack8(rb.row[p], ub + 8 * p);
   }
-#pragma unroll
-  for (int w = 0; w < RMAX; ++w) {
-    if (!va) ua[w] = GZ_PAD;
-    if (!vb) ub[w] = GZ_PAD;
-  }
   double2 ga[RMAX], gb[RMAX];
-#pragma unroll
-  for (int w = 0; w < RMAX; ++w) {
-    if (ua[w] != GZ_PAD) ga[w] = s2[ua[w]];
-    if (ub[w] != GZ_PAD) gb[w] = s2[ub[w]];
-  }
-  double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
   int da = 0, db = 0;
 #pragma unroll
   for (int w = 0; w < RMAX; ++w) {
-    if (ua[w] != GZ_PAD) {
-      if (w == 0) { ax = ga[w].x; ay = ga[w].y; }
-      else { ax = __dadd_rn(ax, ga[w].x); ay = __dadd_rn(ay, ga[w].y); }
-      ++da;
-    }
-    if (ub[w] != GZ_PAD) {
-      if (w == 0) { bx = gb[w].x; by = gb[w].y; }
-      else { bx = __dadd_rn(bx, gb[w].x); by = __dadd_rn(by, gb[w].y); }
-      ++db;
-    }
+    const bool oka = va && ua[w] != GZ_PAD, okb = vb && ub[w] != GZ_PAD;
+    ga[w] = lds_f64x2(sb + 16u * ua[w], oka);
+    gb[w] = lds_f64x2(sb + 16u * ub[w], okb);
+    da += oka;
+    db += okb;
+  }
+  double ax = ga[0].x, ay = ga[0].y, bx = gb[0].x, by = gb[0].y;
+#pragma unroll
+  for (int w = 1; w < RMAX; ++w) {
+    ax = __dadd_rn(ax, ga[w].x);
+    ay = __dadd_rn(ay, ga[w].y);
+    bx = __dadd_rn(bx, gb[w].x);
+    by = __dadd_rn(by, gb[w].y);
   }
   for (int p = RMAX / 8; p * 8 < R; ++p) {  // rows longer than RMAX: ordered tails
     uint16_t t[8];
@@ -889,12 +953,20 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
   }
   if (va) {
     const double dd = (double)da;
-    oa = make_double2(__ddiv_rn(ax, dd), __ddiv_rn(ay, dd));
+    const double rr = rcp[da <= GZ_RCP_MAX ? da : 0];
+    if (da >= 1 && da <= GZ_RCP_MAX && gz_div_ok(ax) && gz_div_ok(ay))
+      oa = make_double2(gz_div(ax, dd, rr), gz_div(ay, dd, rr));
+    else
+      oa = make_double2(__ddiv_rn(da ? ax : 0.0, dd), __ddiv_rn(da ? ay : 0.0, dd));
     s2[ra.pb & 0x7fffu] = oa;
   }
   if (vb) {
     const double dd = (double)db;
-    ob = make_double2(__ddiv_rn(bx, dd), __ddiv_rn(by, dd));
+    const double rr = rcp[db <= GZ_RCP_MAX ? db : 0];
+    if (db >= 1 && db <= GZ_RCP_MAX && gz_div_ok(bx) && gz_div_ok(by))
+      ob = make_double2(gz_div(bx, dd, rr), gz_div(by, dd, rr));
+    else
+      ob = make_double2(__ddiv_rn(db ? bx : 0.0, dd), __ddiv_rn(db ? by : 0.0, dd));
     s2[rb.pb & 0x7fffu] = ob;
   }
 }
@@ -906,7 +978,7 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
 // records into the record ring (one TMA bulk copy per record, in claim
 // order), warps 2.. are workers (one claimed item at a time).
 template <int DIM, int RMAX, int UPL, bool STATS>
-__global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
+__global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
                                                                       const GzTile* __restrict__ tab,
                                                                       const int32_t* __restrict__ item_sweep,
                                                                       const uint4* __restrict__ meta,
@@ -940,6 +1012,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
   int* t_buf = t_pre + L.tiles_cap + 1;  // buffer | (phase parity << 16) of the CTA's i-th tile
   unsigned char* stg = sm + L.off_stage;
   unsigned char* rring = sm + L.off_rec;
+  double* rcp = reinterpret_cast<double*>(sm + L.off_rcp);  // [GZ_RCP_MAX + 1] RN(1/d)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_my = ntiles > (int)blockIdx.x ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   const int PC = P * C;
@@ -961,6 +1034,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
     ctl[0] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (threadIdx.x <= GZ_RCP_MAX) rcp[threadIdx.x] = threadIdx.x ? __ddiv_rn(1.0, (double)threadIdx.x) : 0.0;
   // dependency flags are tagged with the tile index + 1, so they must start
   // below every tag (shared memory is not cleared between launches)
   for (int b = 0; b < NB; ++b) {
@@ -988,10 +1062,14 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
   GzGuard guard{gabort, &s_abort};
 
   if (warp == 0) {  // -------------------------------------------- region producer
+    const long long p0 = STATS ? clock64() : 0;
+    long long pw = 0;
     for (int i = 0; i < n_my; ++i) {
       const int b = i % NB;
       const uint32_t ph = (uint32_t)(i / NB) & 1u;
+      const long long q0 = STATS ? clock64() : 0;
       if (i >= NB && !mbar_wait_g(empty + b, ph ^ 1u, guard)) return;
+      if (STATS) pw += clock64() - q0;
       const int k = tiles[blockIdx.x + (long long)i * gridDim.x];
       const GzTile t = tab[k];
       const uint32_t bytes = t.meta16 * 16u;
@@ -1047,6 +1125,10 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
       }
       __syncwarp();
     }
+    if (STATS && lane == 0) {
+      atomicAdd(stats + 4, (unsigned long long)pw);
+      atomicAdd(stats + 5, (unsigned long long)(clock64() - p0));
+    }
     return;
   }
   if (warp == 1) {  // ---------------------------------------------- record loader
@@ -1055,37 +1137,60 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
     // in HBM, so a batch is one bulk copy per tile it touches (when the
     // tile's record size equals the slot stride, else one per record)
     if (lane == 0) {
-      int ti = 0;
+      // the current tile's parameters live in registers: the tables are in
+      // shared memory, whose pipe the workers keep busy, and a chain of
+      // dependent lookups per batch made this thread the kernel's bottleneck
       const int BS = L.BS;
       const int nbat = (total + BS - 1) / BS;
+      int ti = 0, lo = 0, hi = 0, r16 = 0;
+      const uint4* tsrc = rec;  // record of claim lo
+      auto load_tile = [&](int j) {
+        ti = j;
+        lo = t_pre[j];
+        hi = t_pre[j + 1];
+        r16 = t_rec16[j];
+        tsrc = rec + t_rec[j] + (long long)t_item0[j] * r16;
+      };
+      if (nbat > 0) load_tile(0);
+      const long long l0 = STATS ? clock64() : 0;
+      long long lw = 0;
       for (int g = 0; g < nbat; ++g) {
         const int slot = g & (RR - 1);  // RR is a power of two
+        const long long q0 = STATS ? clock64() : 0;
         if (g >= RR && !mbar_wait_g(rempty + slot, ((uint32_t)(g >> L.RR_log2) & 1u) ^ 1u, guard)) return;
+        if (STATS) lw += clock64() - q0;
         const int k0 = g * BS, k1 = min(total, k0 + BS);
-        uint32_t bytes = 0;
-        for (int kc = k0, tj = ti; kc < k1;) {  // pass 1: bytes of the batch
-          while (kc >= t_pre[tj + 1]) ++tj;
-          const int kend = min(k1, t_pre[tj + 1]);
-          bytes += (uint32_t)(kend - kc) * (uint32_t)t_rec16[tj] * 16u;
-          kc = kend;
+        while (k0 >= hi) load_tile(ti + 1);
+        uint32_t bytes;
+        if (k1 <= hi) {
+          bytes = (uint32_t)(k1 - k0) * (uint32_t)r16 * 16u;
+        } else {  // the batch crosses into later tiles
+          bytes = (uint32_t)(hi - k0) * (uint32_t)r16 * 16u;
+          for (int tj = ti + 1, kc = hi; kc < k1; ++tj) {
+            const int kend = min(k1, t_pre[tj + 1]);
+            bytes += (uint32_t)(kend - kc) * (uint32_t)t_rec16[tj] * 16u;
+            kc = kend;
+          }
         }
         mbar_expect_tx(rfull + slot, bytes);
         unsigned char* dst = rring + (size_t)slot * BS * L.rec_bytes;
         for (int kc = k0; kc < k1;) {
-          while (kc >= t_pre[ti + 1]) ++ti;
-          const int kend = min(k1, t_pre[ti + 1]);
-          const int t = t_item0[ti] + (kc - t_pre[ti]);
-          const uint32_t rb = (uint32_t)t_rec16[ti] * 16u;
-          const uint4* src = rec + t_rec[ti] + (long long)t * t_rec16[ti];
+          while (kc >= hi) load_tile(ti + 1);
+          const int kend = min(k1, hi);
+          const uint32_t rb = (uint32_t)r16 * 16u;
+          const uint4* src = tsrc + (long long)(kc - lo) * r16;
           if ((int)rb == L.rec_bytes) {
             bulk_g2s(dst + (size_t)(kc - k0) * L.rec_bytes, src, (uint32_t)(kend - kc) * rb, rfull + slot);
           } else {
             for (int q = kc; q < kend; ++q)
-              bulk_g2s(dst + (size_t)(q - k0) * L.rec_bytes, src + (long long)(q - kc) * t_rec16[ti], rb,
-                       rfull + slot);
+              bulk_g2s(dst + (size_t)(q - k0) * L.rec_bytes, src + (long long)(q - kc) * r16, rb, rfull + slot);
           }
           kc = kend;
         }
+      }
+      if (STATS) {
+        atomicAdd(stats + 6, (unsigned long long)lw);
+        atomicAdd(stats + 7, (unsigned long long)(clock64() - l0));
       }
     }
     return;
@@ -1159,14 +1264,26 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
     const int sg = (int)(desc.x >> 16);
     // this item's dependencies
     alive = 1;
+    int d2v[UPL];
     if (desc.y == 0) {
       const uint16_t* dep2 = reinterpret_cast<const uint16_t*>(rbase + gz_dep2_off(R, U));
+#pragma unroll
+      for (int u = 0; u < UPL; ++u) d2v[u] = dep2[lane + 32 * u];
+    }
+    // the record is in registers now: hand its ring slot back before the
+    // dependency waits and the compute, so the ring holds prefetched records
+    // rather than items in progress (rows longer than RMAX read their tail
+    // from the record during the update: those release at completion)
+    const bool early = R <= RMAX;
+    __syncwarp();
+    if (early && lane == 0) mbar_arrive(rempty + slot);
+    if (desc.y == 0) {
 #pragma unroll
       for (int u = 0; u < UPL; ++u) {
         const int dep = (int)(r[u].pb >> 16);
         if (dep != 0xffff && dep >= item0)
           while (alive && flags[dep] != i + 1) alive = guard.ok();
-        const int d2 = dep2[lane + 32 * u];
+        const int d2 = d2v[u];
         if (d2 != 0xffff && d2 >= item0)
           while (alive && flags[d2] != i + 1) alive = guard.ok();
       }
@@ -1187,7 +1304,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
       const bool va = (r[0].pb & 0x7fffu) != 0x7fffu, vb = (r[UPL - 1].pb & 0x7fffu) != 0x7fffu;
       double2 oa, ob;
       gz_update2<RMAX>(r[0], va, r[UPL - 1], vb, R, reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3),
-                       reinterpret_cast<const uint4*>(rbase) + (lane + 32) * (R >> 3), sc, oa, ob);
+                       reinterpret_cast<const uint4*>(rbase) + (lane + 32) * (R >> 3), sc, rcp, oa, ob);
       if (last) {  // owned vertices, final values of the pass
         if (va && (r[0].pb & 0x8000u)) a1[r[0].gid] = oa;
         if (vb && (r[UPL - 1].pb & 0x8000u)) a1[r[UPL - 1].gid] = ob;
@@ -1199,7 +1316,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
           const int nr4 = DIM == 3 ? (int)r4(reinterpret_cast<const uint32_t*>(buf)[1]) : 0;
           double ox, oy, oz;
           gz_update<DIM, RMAX>(r[u], R, reinterpret_cast<const uint4*>(rbase) + (lane + 32 * u) * (R >> 3), sc,
-                               nr4, ox, oy, oz);
+                               rcp, nr4, ox, oy, oz);
           if (last && (r[u].pb & 0x8000u)) {
             if (DIM == 2) {
               a1[r[u].gid] = make_double2(ox, oy);
@@ -1213,7 +1330,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 768 : 384, 1) k_sweep_gz(const int3
     }
     __syncwarp();
     if (lane == 0) {
-      mbar_arrive(rempty + slot);  // one of the batch's records consumed
+      if (!early) mbar_arrive(rempty + slot);  // one of the batch's records consumed
       fence_cta();
       flags[t] = i + 1;
       if (desc.z) atomicAdd(cnt + sg, 1);  // stage counters: only tiles with whole-stage waits read them
@@ -1525,7 +1642,10 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   }
   DBuf<int64_t> rec_sz(K, s), meta_sz(K, s), nitems(K, s), nslots(K, s), nruns(K, s), rec_off(K + 1, s),
       meta_off(K + 1, s);
-  k_gzd_tile_sizes<<<gsz(K), 256, 0, s>>>(K, C, P, m->dim, 32 * upl, tR.p, sfirst.p, reg_off.p, rs.p, rec_sz.p, meta_sz.p, nitems.p,
+  // region copies: TMA bulk copies of id runs when the runs average at least
+  // LMS_GZ_RUN_MIN slots, else 16-byte cp.async gathers
+  const int run_min = env_int("LMS_GZ_RUN_MIN", 4, 1, 1 << 30);
+  k_gzd_tile_sizes<<<gsz(K), 256, 0, s>>>(K, C, P, m->dim, 32 * upl, run_min, tR.p, sfirst.p, reg_off.p, rs.p, rec_sz.p, meta_sz.p, nitems.p,
                                           nslots.p, nruns.p);
   LMS_CHECK_LAUNCH();
   const int64_t rec16_all = scan_i64(rec_sz.p, K, rec_off.p, s);
@@ -1698,9 +1818,10 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   // wait unambiguous.  The ring is also the record prefetch depth: about 45
   // records are consumed per TMA latency on C4, so at least 8 batches (64
   // records; 4 batches measured 1.7x slower).  RR is a power of two.
-  L->BS = upl == 2 ? 4 : 8;  // records per batch (about 3-6 KB per batch)
-  L->BS_log2 = upl == 2 ? 2 : 3;
-  L->RR = 8;
+  L->BS_log2 = env_int("LMS_GZ_BS_LOG2", upl == 2 ? 2 : 3, 0, 4);  // records per batch (about 3-6 KB per batch)
+  L->BS = 1 << L->BS_log2;
+  L->RR = env_int("LMS_GZ_RR", 8, 8, 64);
+  while (L->RR & (L->RR - 1)) ++L->RR;
   while (L->RR * L->BS < nw + L->BS) L->RR *= 2;
   L->RR_log2 = 0;
   while ((1 << L->RR_log2) < L->RR) ++L->RR_log2;
@@ -1718,7 +1839,8 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   for (int nb = want_nb > 0 ? want_nb : 8; nb >= 1; --nb) {
     L->NB = nb;
     const int ctl = (2 * nb + 2 * L->RR + 1) * 8 + (1 + 2 * nb) * 4;
-    L->off_tab = r16i(ctl);
+    L->off_rcp = r16i(ctl);
+    L->off_tab = L->off_rcp + r16i(8 * (GZ_RCP_MAX + 1));
     const int tab_bytes = r16i((int64_t)tiles_cap * (8 + 4 + 4 + 4 + 4) + 4 * ((int64_t)tiles_cap + 1));
     L->off_stage = L->off_tab + tab_bytes;
     L->off_rec = L->off_stage + L->stage_bytes;
@@ -1738,11 +1860,12 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   }
   int cap = 0, nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
+  cap -= 16;  // the kernel's static shared memory (abort flag)
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
   // updates per lane (LMS_GZ_UPL=2 in 2D: 64-update items; measured slower on
   // C4 -- coarser items wait on more dependencies -- so 1 is the default)
   const int upl = env_int("LMS_GZ_UPL", 1, 1, m->dim == 2 ? 2 : 1);
-  const int maxw = (m->dim == 2 ? 768 : 384) / 32;  // the kernel's launch bounds
+  const int maxw = (m->dim == 2 ? 1024 : 384) / 32;  // the kernel's launch bounds
   // 22 workers measured best on C4 (more warps only lengthen every item: the
   // shared-memory pipe is the shared resource); + region producer + record loader
   const int nw = env_int("LMS_GZ_WORKERS", std::min(maxw - 2, m->dim == 2 ? 22 : 10), 1, maxw - 2);
@@ -1826,6 +1949,8 @@ static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
     const double it = h[3] ? (double)h[3] : 1.0;
     fprintf(stderr, "[gz stats] per item cycles: wait_tile=%.0f wait_deps=%.0f compute=%.0f (items=%.0f)\n",
             h[0] / it, h[1] / it, h[2] / it, it);
+    fprintf(stderr, "[gz stats] per CTA kcycles: producer wait_empty=%.1f of %.1f, record loader wait_empty=%.1f of %.1f\n",
+            h[4] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid, h[7] / 1e3 / grid);
   }
 }
 

@@ -92,6 +92,7 @@ struct GzLayout {
   int flag_off = 0, cnt_off = 0, coord_off = 0, buf_bytes = 0;  // inside a buffer
   int stage_bytes = 0;          // producer staging (largest meta block)
   int tiles_cap = 0;            // tiles per CTA (table size)
+  int off_rcp = 0;              // RN(1/d) table for the division (d <= 32)
   int off_tab = 0, off_stage = 0, off_ring = 0;  // region offsets
 };
 
