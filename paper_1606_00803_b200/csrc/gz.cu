@@ -329,145 +329,187 @@ __global__ void k_gzd_region(const uint64_t* __restrict__ reg, int64_t n, int C,
   }
 }
 
-// one warp per item: the record (rows, slots + owned flags, ids, descriptor)
-// and the item's touched slot interval [lo, hi].  Lane l builds positions l,
-// l + 32, ... (U = 32 * UPL positions).  2D rows of 8 get a greedy bank-aware
-// placement: the 16-byte shared-memory gathers and the result stores are
-// processed 8 lanes at a time, and lanes of one quarter-warp hitting the same
-// bank group serialise, so each update goes to the group of 8 positions where
-// it collides least (groups of the same instruction are positions 32u..32u+31).
-__global__ void __launch_bounds__(256) k_gzd_records(const int32_t* __restrict__ it_ks,
-                                                     const int32_t* __restrict__ it_q, int64_t NI,
+// slot of vertex g in a tile's region (ids sorted ascending, in shared memory)
+__device__ __forceinline__ int region_slot(const uint32_t* __restrict__ rid, int nr, uint32_t g) {
+  int lo = 0, n = nr;
+  while (n > 0) {
+    const int h = n >> 1;
+    if (rid[lo + h] < g) {
+      lo += h + 1;
+      n -= h + 1;
+    } else {
+      n = h;
+    }
+  }
+  return lo;
+}
+
+// One CTA per tile (grid-stride), one warp per item of the tile: the record
+// (rows, slots + owned flags, ids, descriptor) and the item's touched slot
+// interval [lo, hi].  The tile's region ids are staged in shared memory for
+// the neighbour -> slot searches.  Lane l builds positions l, l + 32, ...
+// (U = 32 * UPL positions).  2D rows of 8 get a greedy bank-aware placement:
+// the 16-byte shared-memory gathers and the result stores are processed 8
+// lanes at a time, and lanes of one quarter-warp hitting the same bank group
+// serialise, so each update (most neighbours first, then by position) goes to
+// the group of 8 positions where it collides least, lowest group on ties
+// (groups of the same instruction are positions 32u..32u+31); lane a keeps
+// group a's bank masks and the warp takes the arg-min.
+__global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* __restrict__ it_ks,
+                                                     const int32_t* __restrict__ it_q,
                               int C, int P, int UPL, const int64_t* __restrict__ kc_off, const int32_t* __restrict__ cntj,
                               const uint64_t* __restrict__ ck, const int32_t* __restrict__ cv,
                               const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
                               const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                               const int32_t* __restrict__ tile_of, const uint64_t* __restrict__ reg,
                               const int64_t* __restrict__ reg_off, uint4* rec, int32_t* it_lo, int32_t* it_hi) {
+  extern __shared__ uint32_t gz_rid[];  // [max region slots]
   __shared__ uint8_t gz_banks[8 * 64 * 9];
   __shared__ uint8_t gz_pos[8 * 64];
+  __shared__ uint8_t gz_cnt[8 * 64];
+  __shared__ uint8_t gz_ord[8 * 64];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
+  const int nwib = blockDim.x >> 5;
   const int PC = P * C;
   const int U = 32 * UPL;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t it = w0; it < NI; it += nw) {
-    const int64_t ks = it_ks[it];
-    const int64_t k = ks / PC;
-    const int sg = (int)(ks - k * PC);
-    const int j = sg / C, c = sg - j * C;
-    const int q = it_q[it];
-    const int64_t kc = k * C + c;
-    const int nupd = cntj[kc * P + j];
-    const int n = min(U, nupd - U * q);
+  uint8_t* bk = gz_banks + wib * 64 * 9;
+  uint8_t* ps = gz_pos + wib * 64;
+  uint8_t* cn = gz_cnt + wib * 64;
+  uint8_t* od = gz_ord + wib * 64;
+  for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
+    const int64_t ra = reg_off[k], rb = reg_off[k + 1];
+    const int nr = (int)(rb - ra);
+    __syncthreads();  // the previous tile's searches are done
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) gz_rid[i] = (uint32_t)(reg[ra + i] & 0xffffffffull);
+    __syncthreads();
     const GzTile t = tab[k];
     const int R = (int)t.R;
-    const int64_t tloc = it - sfirst[k * PC];  // item index inside the tile
-    unsigned char* base = reinterpret_cast<unsigned char*>(rec + t.rec_base + tloc * t.rec16);
-    uint16_t* rows = reinterpret_cast<uint16_t*>(base);
-    uint32_t* pb = reinterpret_cast<uint32_t*>(base + 2 * U * R);
-    int32_t* gid = reinterpret_cast<int32_t*>(base + 2 * U * R + 4 * U);
-    uint32_t* desc = reinterpret_cast<uint32_t*>(base + 2 * U * R + 8 * U);
-    const uint64_t kh = (uint64_t)k << 32;
-    const int64_t ra = reg_off[k], rb = reg_off[k + 1];
-    uint8_t* bk = gz_banks + wib * 64 * 9;
-    uint8_t* ps = gz_pos + wib * 64;
-    // bank groups of each update (position-independent), then the placement
-    if (R == 8) {
+    const int64_t i0 = sfirst[k * PC], i1 = sfirst[(k + 1) * PC];
+    for (int64_t it = i0 + wib; it < i1; it += nwib) {
+      const int64_t ks = it_ks[it];
+      const int sg = (int)(ks - k * PC);
+      const int j = sg / C, c = sg - j * C;
+      const int q = it_q[it];
+      const int64_t kc = k * C + c;
+      const int nupd = cntj[kc * P + j];
+      const int n = min(U, nupd - U * q);
+      const int64_t tloc = it - i0;  // item index inside the tile
+      unsigned char* base = reinterpret_cast<unsigned char*>(rec + t.rec_base + tloc * t.rec16);
+      uint16_t* rows = reinterpret_cast<uint16_t*>(base);
+      uint32_t* pb = reinterpret_cast<uint32_t*>(base + 2 * U * R);
+      int32_t* gid = reinterpret_cast<int32_t*>(base + 2 * U * R + 4 * U);
+      uint32_t* desc = reinterpret_cast<uint32_t*>(base + 2 * U * R + 8 * U);
+      // bank groups of each update (position-independent), then the placement
+      if (R == 8) {
+        for (int u0 = 0; u0 < U; u0 += 32) {
+          const int e = u0 + lane;
+          int cnt = 0;
+          for (int w = 0; w < 9; ++w) bk[e * 9 + w] = 0xff;
+          if (e < n) {
+            const int64_t uu = kc_off[kc] + (int64_t)U * q + e;
+            const int32_t v = cv[uu];
+            bk[e * 9] = (uint8_t)((ck[uu] & 0xffffull) & 7u);
+            cnt = 1;
+            const int32_t b = rp[v], d = rp[v + 1] - b;
+            for (int w = 0; w < d && w < 8; ++w) {
+              bk[e * 9 + 1 + w] = (uint8_t)(region_slot(gz_rid, nr, (uint32_t)col[b + w]) & 7);
+              ++cnt;
+            }
+          }
+          cn[e] = (uint8_t)cnt;
+        }
+        __syncwarp();
+        // placement order: most banks first, then by position
+        for (int e = lane; e < U; e += 32) {
+          const int ce = cn[e];
+          int r = 0;
+          for (int e2 = 0; e2 < U; ++e2) {
+            const int c2 = cn[e2];
+            r += (c2 > ce) || (c2 == ce && e2 < e);
+          }
+          od[r] = (uint8_t)e;
+        }
+        __syncwarp();
+        const int ng = U / 8;
+        uint64_t qlo = 0;  // this lane's group (lane < ng): banks used per neighbour slot w < 8
+        uint32_t qhi = 0;  // ... and for w = 8
+        int qn = 0;
+        for (int r = 0; r < U; ++r) {
+          const int e = od[r];
+          int pen = 1 << 20;
+          if (lane < ng && qn < 8) {
+            pen = 0;
+            for (int w = 0; w < 9; ++w) {
+              const int bb = bk[e * 9 + w];
+              if (bb != 0xff) pen += (int)((w < 8 ? (qlo >> (8 * w + bb)) : (uint64_t)(qhi >> bb)) & 1u);
+            }
+          }
+          int key = (pen << 5) | lane;
+          for (int o = 16; o; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+          const int best = key & 31;
+          if (lane == best) {
+            ps[e] = (uint8_t)(8 * best + qn);
+            ++qn;
+            for (int w = 0; w < 9; ++w) {
+              const int bb = bk[e * 9 + w];
+              if (bb != 0xff) {
+                if (w < 8) qlo |= 1ull << (8 * w + bb);
+                else qhi |= 1u << bb;
+              }
+            }
+          }
+        }
+        __syncwarp();
+      } else {
+        for (int e = lane; e < U; e += 32) ps[e] = (uint8_t)e;
+        __syncwarp();
+      }
+      int lo = 0x7fffffff, hi = -1;
       for (int u0 = 0; u0 < U; u0 += 32) {
         const int e = u0 + lane;
-        for (int w = 0; w < 9; ++w) bk[e * 9 + w] = 0xff;
+        const int pos = ps[e];
+        uint32_t p = 0xffff0000u | 0x7fffu;  // slot 0x7fff = empty position
+        int32_t g = -1;
         if (e < n) {
           const int64_t uu = kc_off[kc] + (int64_t)U * q + e;
           const int32_t v = cv[uu];
-          bk[e * 9] = (uint8_t)((ck[uu] & 0xffffull) & 7u);
+          const int lv = (int)(ck[uu] & 0xffffull);
+          g = v;
+          p = 0xffff0000u | (uint32_t)lv | (tile_of[v] == (int32_t)k ? 0x8000u : 0u);
+          lo = min(lo, lv);
+          hi = max(hi, lv);
           const int32_t b = rp[v], d = rp[v + 1] - b;
-          for (int w = 0; w < d && w < 8; ++w) {
-            const int sl = (int)(lower_bound_u64(reg, ra, rb, kh | (uint32_t)col[b + w]) - ra);
-            bk[e * 9 + 1 + w] = (uint8_t)(sl & 7);
+          for (int w = 0; w < R; ++w) {
+            uint16_t li = GZ_PAD;
+            if (w < d) {
+              const int sl = region_slot(gz_rid, nr, (uint32_t)col[b + w]);
+              li = (uint16_t)sl;
+              lo = min(lo, sl);
+              hi = max(hi, sl);
+            }
+            rows[pos * R + w] = li;
           }
+        } else {
+          for (int w = 0; w < R; ++w) rows[pos * R + w] = GZ_PAD;
         }
+        pb[pos] = p;
+        gid[pos] = g;
       }
       __syncwarp();
+      for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
       if (lane == 0) {
-        uint8_t qm[8][9];
-        int qn[8];
-        const int ng = U / 8;
-        for (int a = 0; a < ng; ++a) {
-          qn[a] = 0;
-          for (int w = 0; w < 9; ++w) qm[a][w] = 0;
-        }
-        for (int dd = 9; dd >= 0; --dd)  // most neighbours first; empty positions (no banks) last
-          for (int e = 0; e < U; ++e) {
-            int cntl = 0;
-            for (int w = 0; w < 9; ++w) cntl += bk[e * 9 + w] != 0xff;
-            if (cntl != dd) continue;
-            int best = -1, bp = 1 << 30;
-            for (int a = 0; a < ng; ++a) {
-              if (qn[a] >= 8) continue;
-              int pen = 0;
-              for (int w = 0; w < 9; ++w) {
-                const int bb = bk[e * 9 + w];
-                if (bb != 0xff) pen += (qm[a][w] >> bb) & 1;
-              }
-              if (pen < bp) { bp = pen; best = a; }
-            }
-            ps[e] = (uint8_t)(8 * best + qn[best]++);
-            for (int w = 0; w < 9; ++w) {
-              const int bb = bk[e * 9 + w];
-              if (bb != 0xff) qm[best][w] |= (uint8_t)(1u << bb);
-            }
-          }
+        desc[0] = (uint32_t)n | ((uint32_t)j << 8) | ((uint32_t)sg << 16);
+        desc[1] = 0;
+        desc[2] = 0;
+        desc[3] = 0;
+        it_lo[it] = lo;
+        it_hi[it] = hi;
       }
-      __syncwarp();
-    } else {
-      for (int e = lane; e < U; e += 32) ps[e] = (uint8_t)e;
-      __syncwarp();
-    }
-    int lo = 0x7fffffff, hi = -1;
-    for (int u0 = 0; u0 < U; u0 += 32) {
-      const int e = u0 + lane;
-      const int pos = ps[e];
-      uint32_t p = 0xffff0000u | 0x7fffu;  // slot 0x7fff = empty position
-      int32_t g = -1;
-      if (e < n) {
-        const int64_t uu = kc_off[kc] + (int64_t)U * q + e;
-        const int32_t v = cv[uu];
-        const int lv = (int)(ck[uu] & 0xffffull);
-        g = v;
-        p = 0xffff0000u | (uint32_t)lv | (tile_of[v] == (int32_t)k ? 0x8000u : 0u);
-        lo = min(lo, lv);
-        hi = max(hi, lv);
-        const int32_t b = rp[v], d = rp[v + 1] - b;
-        for (int w = 0; w < R; ++w) {
-          uint16_t li = GZ_PAD;
-          if (w < d) {
-            const int sl = (int)(lower_bound_u64(reg, ra, rb, kh | (uint32_t)col[b + w]) - ra);
-            li = (uint16_t)sl;
-            lo = min(lo, sl);
-            hi = max(hi, sl);
-          }
-          rows[pos * R + w] = li;
-        }
-      } else {
-        for (int w = 0; w < R; ++w) rows[pos * R + w] = GZ_PAD;
-      }
-      pb[pos] = p;
-      gid[pos] = g;
-    }
-    __syncwarp();
-    for (int o = 16; o; o >>= 1) {
-      lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-      hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    if (lane == 0) {
-      desc[0] = (uint32_t)n | ((uint32_t)j << 8) | ((uint32_t)sg << 16);
-      desc[1] = 0;
-      desc[2] = 0;
-      desc[3] = 0;
-      it_lo[it] = lo;
-      it_hi[it] = hi;
+      __syncwarp();  // ps / bk reuse by the warp's next item
     }
   }
 }
@@ -1440,19 +1482,22 @@ __device__ __forceinline__ uint64_t orderable(double d) {
   const uint64_t u = (uint64_t)__double_as_longlong(d);
   return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
-__global__ void k_kd_xkey(const double* __restrict__ x, int64_t V, uint64_t* key, int32_t* ids) {
+// 32-bit keys: the tiling only needs spatially compact tiles, not an exact
+// order (ties keep the stable sort's input order), and a 32-bit key is half the
+// passes and half the bytes of a 64-bit one
+__global__ void k_kd_xkey(const double* __restrict__ x, int64_t V, uint32_t* key, int32_t* ids) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
-    key[v] = orderable(x[v]);
+    key[v] = (uint32_t)(orderable(x[v]) >> 32);
     ids[v] = (int32_t)v;
   }
 }
-// sorted position p -> strip; key (strip, y)
+// sorted position p -> strip; key (strip, top 32 - sb bits of y)
 __global__ void k_kd_ykey(const int32_t* __restrict__ sorted_ids, const double* __restrict__ y, int64_t V,
-                          int64_t per_strip, uint64_t* key, int32_t* ids) {
+                          int64_t per_strip, int sb, uint32_t* key, int32_t* ids) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < V; p += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = sorted_ids[p];
-    const uint64_t strip = (uint64_t)(p / per_strip);
-    key[p] = (strip << 44) | (orderable(y[v]) >> 20);
+    const uint32_t strip = (uint32_t)(p / per_strip);
+    key[p] = (sb > 0 ? strip << (32 - sb) : 0u) | (uint32_t)(orderable(y[v]) >> (32 + sb));
     ids[p] = v;
   }
 }
@@ -1472,17 +1517,18 @@ static int64_t kd_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) 
   if (nbx > (1 << 19)) nbx = 1 << 19;
   const int64_t per_strip = (V + nbx - 1) / nbx;
   const int64_t tps = (per_strip + T - 1) / T;
-  DBuf<uint64_t> k1(V, s), k2(V, s);
+  DBuf<uint32_t> k1(V, s), k2(V, s);
   DBuf<int32_t> i1(V, s), i2(V, s);
   k_kd_xkey<<<gsz(V), 256, 0, s>>>(m->x[0].p, V, k1.p, i1.p);
   LMS_CHECK_LAUNCH();
   size_t tb = 0;
-  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 64, s));
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 32, s));
   DBuf<char> tmp(tb, s);
-  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 64, s));
-  k_kd_ykey<<<gsz(V), 256, 0, s>>>(i2.p, m->x[1].p, V, per_strip, k1.p, i1.p);
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 32, s));
+  const int sb = nbx > 1 ? bits_for(nbx) : 0;
+  k_kd_ykey<<<gsz(V), 256, 0, s>>>(i2.p, m->x[1].p, V, per_strip, sb, k1.p, i1.p);
   LMS_CHECK_LAUNCH();
-  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 64, s));
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 32, s));
   k_kd_tile<<<gsz(V), 256, 0, s>>>(i2.p, V, per_strip, T, tps, tile_of);
   LMS_CHECK_LAUNCH();
   return nbx * tps;
@@ -1529,9 +1575,12 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
     if (V > 1) {
       DBuf<uint64_t> out(V, s);
       size_t tb = 0;
-      LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, l0.p, out.p, V, 0, 64, s));
+      // keys are generated in vertex order and the radix sort is stable, so
+      // sorting on the tile bits alone gives (tile, id) order; fixed vertices
+      // (all ones) sort last
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, l0.p, out.p, V, 32, end_bit, s));
       DBuf<char> tmp(tb, s);
-      LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, l0.p, out.p, V, 0, 64, s));
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, l0.p, out.p, V, 32, end_bit, s));
       l0 = std::move(out);
     }
   }
@@ -1692,9 +1741,11 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   }
   if (NI > 0) {
     DBuf<int32_t> it_lo(NI, s), it_hi(NI, s);
-    k_gzd_records<<<gsz(NI * 32), 256, 0, s>>>(it_ks.p, it_q.p, NI, C, P, upl, kc_off.p, cntj.p, ck2.p, cv2.p, tab.p,
-                                               sfirst.p, m->row_ptr.p, m->col.p, tile_of.p, reg.p, reg_off.p, rec.p,
-                                               it_lo.p, it_hi.p);
+    const int rid_bytes = (int)(4 * std::max<int64_t>(out->max_slots, 1));
+    LMS_TRY_CUDA(cudaFuncSetAttribute(k_gzd_records, cudaFuncAttributeMaxDynamicSharedMemorySize, rid_bytes));
+    k_gzd_records<<<(unsigned)std::min<int64_t>(K, 1 << 20), 256, rid_bytes, s>>>(
+        K, it_ks.p, it_q.p, C, P, upl, kc_off.p, cntj.p, ck2.p, cv2.p, tab.p, sfirst.p, m->row_ptr.p, m->col.p,
+        tile_of.p, reg.p, reg_off.p, rec.p, it_lo.p, it_hi.p);
     LMS_CHECK_LAUNCH();
     DBuf<int> tneed(K > 0 ? K : 1, s);
     LMS_TRY_CUDA(cudaMemsetAsync(tneed.p, 0, (K > 0 ? K : 1) * sizeof(int), s));
@@ -1873,14 +1924,15 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   const int dim = m->dim, C = m->C;
   GzNeeds nd;
   Schedule& S = m->sched;
-  // uniform spatial bins first; equal-count (kd) tiles for 2D meshes whose
-  // density varies too much for bins (or LMS_GZ_TILING=kd)
+  // 2D: equal-count (kd) tiles at T, 4T/5, ... (as fast as uniform bins on
+  // uniform meshes, and their regions are bounded on graded ones, so the
+  // first attempt fits: a failed attempt costs a whole build);
+  // LMS_GZ_TILING=bins puts uniform spatial bins at T first.  3D: bins at
+  // shrinking T.
   const char* te = getenv("LMS_GZ_TILING");
-  const bool kd_only = te && !strcmp(te, "kd");
-  // attempts: bins at T, then (2D) equal-count tiles at T, 4T/5, ...; 3D: bins
-  // at shrinking T
+  const bool bins_first = dim != 2 || (te && !strcmp(te, "bins"));
   std::vector<std::pair<int, int>> tries;
-  if (!kd_only) tries.push_back({0, T});
+  if (bins_first) tries.push_back({0, T});
   for (int t = T; t >= 32; t = t * 4 / 5)
     if (dim == 2) tries.push_back({1, t});
     else if (t != T) tries.push_back({0, t});

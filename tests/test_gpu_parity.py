@@ -131,13 +131,13 @@ def test_gz_coordinate_updates_between_calls(pair):
         assert bits_equal(gpu_coords(gm), want)
 
 
-def test_gz_equal_count_tiling(pair, monkeypatch):
-    """LMS_GZ_TILING=kd: equal-count strip tiles (the fallback for graded
-    meshes) give the same bit-exact sweeps."""
+def test_gz_spatial_bins_tiling(pair, monkeypatch):
+    """LMS_GZ_TILING=bins: uniform spatial bins (the 3D tiling; 2D defaults
+    to equal-count strip tiles) give the same bit-exact sweeps in 2D."""
     m, om, gm0 = pair
     if m["dim"] != 2:
-        pytest.skip("equal-count tiling is 2D")
-    monkeypatch.setenv("LMS_GZ_TILING", "kd")
+        pytest.skip("3D always uses bins")
+    monkeypatch.setenv("LMS_GZ_TILING", "bins")
     want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 4)
     with gpu_mesh(m) as gm:
         gm.set_schedule("gz", tile=100, lag=2)
