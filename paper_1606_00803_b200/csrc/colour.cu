@@ -12,14 +12,26 @@
 // all at once with first-fit.  A vertex is coloured exactly when the sequential
 // greedy would have all the information it uses, hence the result is identical
 // to the sequential definition.
-// Execution: no rounds and no grid barriers (k_jp_warp): persistent warps
-// take ready vertices from a queue (or continue with one they just released)
-// and colour each one when its counter reaches zero.  The critical path is
-// the dependency chain (about nx + 2 ny vertices on a row-major grid) times a
-// few memory round trips, instead of one grid barrier per JP round.
+// Execution (default, k_gc_seq): the definition's own order, in parallel.
+// Positions i = orig_id are cut into chunks of S consecutive positions; a
+// thread colours its chunk in order, so the chain along consecutive ids costs
+// no communication, and a CTA owns a unit of blockDim * S positions whose
+// colours it keeps in shared memory, so most cross-chunk waits are
+// shared-memory spins; only edges into earlier units go through global
+// memory.  Units are claimed in increasing order by co-resident CTAs, so the
+// lowest uncoloured position always has every input and a running thread:
+// no deadlock.  A vertex is coloured from exactly the colours the sequential
+// greedy uses, hence the same result.  Fallback (orig_id not a permutation of
+// 0..V-1, or more than 31 lower neighbours; LMS_COLOUR=jp): k_jp_warp,
+// persistent warps taking ready vertices from a queue (or continuing with one
+// they just released) -- the critical path there is the dependency chain
+// (about nx + 2 ny vertices on a row-major grid) times a few global memory
+// round trips, about 4 us per step.
 #include <algorithm>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -29,6 +41,13 @@
 namespace cg = cooperative_groups;
 
 namespace lms {
+
+static int env_int_c(const char* name, int dflt, int lo, int hi) {
+  const char* e = getenv(name);
+  if (!e || !*e) return dflt;
+  const int v = atoi(e);
+  return v < lo ? lo : (v > hi ? hi : v);
+}
 
 __global__ void k_validate_csr(const int32_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t V,
                                int64_t nnz, int* err) {
@@ -215,6 +234,344 @@ __global__ void __launch_bounds__(256) k_jp_warp(const int32_t* __restrict__ rec
   }
 }
 
+// ---------------------------------------------------------------- in-order path
+// vid[orig_id[v]] = v; error flag if orig_id is not a permutation of 0..V-1
+__global__ void k_gc_vid(const int32_t* __restrict__ oid, int64_t V, int32_t* vid, int* bad) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = oid[v];
+    if (i < 0 || i >= V || atomicExch(&vid[i], (int32_t)v) != -1) atomicExch(bad, 1);
+  }
+}
+// largest number of lower-orig_id free neighbours of a free vertex
+__global__ void k_gc_max_lower(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                               const uint8_t* __restrict__ fixed, const int32_t* __restrict__ oid, int64_t V,
+                               int* out) {
+  int mx = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    if (fixed[v]) continue;
+    const int32_t me = oid[v];
+    int n = 0;
+    for (int32_t j = rp[v]; j < rp[v + 1]; ++j) {
+      const int32_t u = col[j];
+      n += !fixed[u] && oid[u] < me;
+    }
+    mx = max(mx, n);
+  }
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+// record of position i (stride RL ints): [0] = number of lower free neighbours
+// (-1: fixed vertex), then their positions (orig_ids), in CSR order
+// Also: colpos[i] = -1 (free, not yet coloured) or 127 (fixed: never read as
+// an input, but complete for the mirror), and ulo[unit] = lowest position
+// before the unit that the unit's vertices read (the mirror window).
+__global__ void k_gc_records(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const uint8_t* __restrict__ fixed, const int32_t* __restrict__ oid, int64_t V, int RL,
+                             int64_t UNIT, int32_t* rec, int8_t* colpos, int* ulo) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t me = oid[v];
+    int32_t* r = rec + (int64_t)me * RL;
+    colpos[me] = fixed[v] ? 127 : -1;
+    if (fixed[v]) { r[0] = -1; continue; }
+    const int64_t ub = me / UNIT * UNIT;
+    int n = 0, lo = INT32_MAX;
+    for (int32_t j = rp[v]; j < rp[v + 1]; ++j) {
+      const int32_t u = col[j];
+      const int32_t pu = oid[u];
+      if (!fixed[u] && pu < me) {
+        r[1 + n++] = pu;
+        if (pu < ub) lo = min(lo, pu);
+      }
+    }
+    r[0] = n;
+    if (lo != INT32_MAX) atomicMin(&ulo[me / UNIT], lo);
+  }
+}
+
+__device__ __forceinline__ int ld_vol_s8(const int8_t* p) { return *(const volatile int8_t*)p; }
+
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// One thread per chunk of S positions, colouring it in order; a unit of
+// NWK * 32 * S positions per CTA (NWK worker warps), units claimed in
+// increasing order (ctr).  Chunk of worker (warp w, lane l) = l * NWK + w, so
+// the lanes of a warp hold chunks NWK apart (mostly independent).  A worker
+// warp loops in lock step: each lane colours its next position if all its
+// inputs are ready, else tries again next round (no divergent spin loops).
+// cs: the unit's colours (shared); colpos: colours by position (global);
+// colour: by vertex.  A lane's next G records stream into its own
+// shared-memory ring by cp.async (one commit group per record).  Inputs from
+// earlier units: the last warp mirrors the unit's window [ulo, ub) of colpos
+// into shared memory in 16-byte blocks (re-reading only blocks not yet
+// complete), so a worker polls shared memory there too; one round trip to
+// global memory per step on unit-boundary rows would otherwise set the pace of
+// the whole wavefront.
+template <int RL, int G>
+__global__ void __launch_bounds__(288) k_gc_seq(const int32_t* __restrict__ rec, const int32_t* __restrict__ vid,
+                                                const int* __restrict__ ulo, int64_t V, int S, int MW, int* ctr,
+                                                int8_t* colpos, int8_t* colour, int* maxc, int* err,
+                                                unsigned long long* st) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  __shared__ int64_t s_base, s_mlo;
+  __shared__ int s_done;
+  constexpr int NV = RL / 4;  // int4 per record
+  constexpr int NWK = 8;      // worker warps
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t UNIT = (int64_t)NWK * 32 * S;
+  int4* ring = reinterpret_cast<int4*>(gsm) + (size_t)threadIdx.x * G * NV;  // worker lane's G records
+  int8_t* cs = reinterpret_cast<int8_t*>(gsm + (size_t)NWK * 32 * G * NV * 16);
+  int8_t* mir = cs + UNIT;  // [MW] mirror of colpos[s_mlo, ub)
+  int mymax = -1;
+  bool dead = false;
+  unsigned long long n_rounds = 0, n_prog = 0, n_sweeps = 0, t_unit = 0, n_units = 0;
+  long long tu0 = 0;
+  for (;;) {
+    __syncthreads();  // the previous unit is done with cs / mir / s_*
+    if (st && threadIdx.x == 0) {
+      const long long t = clock64();
+      if (tu0) { t_unit += t - tu0; ++n_units; }
+      tu0 = t;
+    }
+    if (threadIdx.x == 0) {
+      const int64_t ub = (int64_t)atomicAdd(ctr, 1) * UNIT;
+      s_base = ub;
+      int64_t lo = ub < V ? (int64_t)ulo[ub / UNIT] : ub;
+      lo = lo >= ub ? ub : (lo & ~(int64_t)15);
+      s_mlo = ub - lo <= MW ? lo : ub;  // window too wide: workers read global memory
+      s_done = 0;
+    }
+    for (int64_t q = threadIdx.x; q < UNIT + MW; q += blockDim.x) cs[q] = -1;
+    __syncthreads();
+    const int64_t ub = s_base;
+    if (ub >= V) break;
+    const int64_t mlo = s_mlo;
+    if (warp == NWK) {  // ------------------------------------------ mirror
+      const int nblk = (int)((ub - mlo) >> 4);
+      int4* m16 = reinterpret_cast<int4*>(mir);
+      const int4* g16 = reinterpret_cast<const int4*>(colpos + mlo);
+      long long idle = 0;
+      while (nblk > 0) {
+        bool all = true;
+        for (int k = lane; k < nblk; k += 32) {
+          const int4 h = m16[k];
+          if (((h.x | h.y | h.z | h.w) & 0x80808080) == 0) continue;  // complete
+          int4 g;
+          asm volatile("ld.volatile.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
+                       : "l"(g16 + k));
+          asm volatile("st.volatile.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(m16 + k)),
+                       "r"(g.x), "r"(g.y), "r"(g.z), "r"(g.w)
+                       : "memory");
+          if ((g.x | g.y | g.z | g.w) & 0x80808080) all = false;
+        }
+        ++n_sweeps;
+        if (__all_sync(FULL, all)) break;
+        if (*(volatile int*)&s_done == NWK * 32) break;  // the workers are done with the unit
+        if (++idle > (1ll << 30)) break;
+      }
+      continue;
+    }
+    const int64_t a = ub + (int64_t)(lane * NWK + warp) * S;
+    const int64_t b = min(a + S, V);
+    auto issue = [&](int64_t p) {  // record p into its ring slot (an empty group past the chunk)
+      if (p < b) {
+        int4* d = ring + (int)((p - a) % G) * NV;  // slots within the lane's padded ring
+        const int4* src = reinterpret_cast<const int4*>(rec + p * RL);
+#pragma unroll
+        for (int w = 0; w < NV; ++w) cpa16(d + w, src + w);
+      }
+      cpa_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < G; ++k) issue(a + k);
+    int64_t i = a;
+    long long stall = 0;
+    while (__any_sync(FULL, i < b && !dead)) {
+      bool prog = false;
+      if (i < b && !dead) {
+        cpa_wait<G - 1>();  // record i landed (records i .. i+G-1 are the outstanding groups)
+        const int4* r4 = ring + (int)((i - a) % G) * NV;
+        int4 qr[NV];
+#pragma unroll
+        for (int w = 0; w < NV; ++w) qr[w] = r4[w];
+        const int n = qr[0].x;
+        bool ready = true;
+        uint64_t used0 = 0, used1 = 0;
+#pragma unroll
+        for (int w = 1; w < RL; ++w) {
+          if (w > n) break;
+          const int4 v4 = qr[w >> 2];
+          const int64_t pp = (w & 3) == 0 ? v4.x : (w & 3) == 1 ? v4.y : (w & 3) == 2 ? v4.z : v4.w;
+          const int c = pp >= ub ? ld_vol_s8(cs + (pp - ub))
+                                 : (pp >= mlo ? ld_vol_s8(mir + (pp - mlo)) : ld_vol_s8(colpos + pp));
+          if (c < 0) ready = false;
+          else if (c < 64) used0 |= 1ull << c;
+          else used1 |= 1ull << (c - 64);
+        }
+        if (ready) {
+          if (n >= 0) {  // a free vertex (fixed ones keep colour -1)
+            int c = ~used0 ? __ffsll((long long)~used0) - 1 : (~used1 ? 64 + __ffsll((long long)~used1) - 1 : 128);
+            if (c > 126) { raise_err(err, LMS_E_ARG); c = 126; }
+            *(volatile int8_t*)(cs + (i - ub)) = (int8_t)c;
+            *(volatile int8_t*)(colpos + i) = (int8_t)c;  // by position; k_gc_scatter maps to vertices
+            mymax = c > mymax ? c : mymax;
+          }
+          issue(i + G);  // into the slot record i just vacated
+          ++i;
+          prog = true;
+        }
+      }
+      ++n_rounds;
+      n_prog += prog;
+      if (!__any_sync(FULL, prog)) {
+        if (++stall > (1ll << 28)) {  // cannot happen (every wait is on a lower position)
+          raise_err(err, LMS_E_CUDA);
+          dead = true;
+        }
+      } else {
+        stall = 0;
+      }
+    }
+    cpa_wait<0>();
+    if (lane == 0) atomicAdd(&s_done, 32);
+  }
+  for (int o = 16; o; o >>= 1) mymax = max(mymax, __shfl_down_sync(0xffffffffu, mymax, o));
+  if ((threadIdx.x & 31) == 0 && mymax >= 0) atomicMax(maxc, mymax);
+  if (st && lane == 0) {
+    atomicAdd(st + 0, n_rounds);
+    atomicAdd(st + 2, n_sweeps);
+    if (threadIdx.x == 0) { atomicAdd(st + 3, t_unit); atomicAdd(st + 4, n_units); }
+  }
+  if (st) {
+    for (int o = 16; o; o >>= 1) n_prog += __shfl_down_sync(0xffffffffu, n_prog, o);
+    if (lane == 0) atomicAdd(st + 1, n_prog);
+  }
+}
+
+// colour[v] = colour of position orig_id[v] (fixed vertices: -1)
+__global__ void k_gc_scatter(const int32_t* __restrict__ oid, const uint8_t* __restrict__ fixed,
+                             const int8_t* __restrict__ colpos, int64_t V, int8_t* colour) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+    colour[v] = fixed[v] ? (int8_t)-1 : colpos[oid[v]];
+}
+
+// in-order colouring; false if it does not apply (caller falls back to JP)
+static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
+  const int64_t V = m->V;
+  if (V <= 0 || V > (int64_t)INT32_MAX) return false;
+  const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
+  DBuf<int32_t> vid(V, s);
+  DBuf<int> flags(2, s);  // [0] not a permutation, [1] max lower neighbours
+  LMS_TRY_CUDA(cudaMemsetAsync(vid.p, 0xff, V * sizeof(int32_t), s));
+  LMS_TRY_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), s));
+  k_gc_vid<<<Gv, 256, 0, s>>>(m->orig_id.p, V, vid.p, flags.p);
+  LMS_CHECK_LAUNCH();
+  k_gc_max_lower<<<Gv, 256, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, m->orig_id.p, V, flags.p + 1);
+  LMS_CHECK_LAUNCH();
+  int h[2] = {0, 0};
+  LMS_TRY_CUDA(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  if (h[0] || h[1] > 31) return false;
+  const int RL = h[1] <= 3 ? 4 : h[1] <= 7 ? 8 : h[1] <= 15 ? 16 : 32;
+  const int threads = 288;  // 8 worker warps + the mirror warp
+  // chunk: longer chunks mean fewer cross-thread hops but fewer units in flight
+  const int S = env_int_c("LMS_GC_CHUNK", V >= (int64_t)8 << 20 ? 256 : 128, 8, 4096);
+  const int64_t UNIT = (int64_t)256 * S;
+  const int64_t units = (V + UNIT - 1) / UNIT;
+  DBuf<int32_t> rec((size_t)V * RL, s);
+  DBuf<int8_t> colpos(V + 16, s);
+  DBuf<int> ulo(units, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(ulo.p, 0x7f, units * sizeof(int), s));
+  k_gc_records<<<Gv, 256, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, m->orig_id.p, V, RL, UNIT, rec.p, colpos.p,
+                                  ulo.p);
+  LMS_CHECK_LAUNCH();
+  DBuf<int> ctr(1, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(int), s));
+  // mirror window: the widest unit's reach back (16-byte blocks), capped
+  // (units reaching further read global memory)
+  int MW = 0;
+  {
+    std::vector<int> hl(units);
+    LMS_TRY_CUDA(cudaMemcpyAsync(hl.data(), ulo.p, units * sizeof(int), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    for (int64_t u = 0; u < units; ++u)
+      if (hl[u] < u * UNIT) MW = (int)std::max<int64_t>(MW, u * UNIT - (hl[u] & ~15));
+    const int cap = env_int_c("LMS_GC_MIRROR", 16384, 0, 65536) & ~15;
+    if (MW > cap) MW = cap;
+    MW = (MW + 15) & ~15;
+  }
+  constexpr int G = 8;  // records in flight per worker lane
+  const size_t smem = (size_t)256 * G * (RL / 4) * 16 + (size_t)UNIT + (size_t)MW;
+  void (*kern)(const int32_t*, const int32_t*, const int*, int64_t, int, int, int*, int8_t*, int8_t*, int*, int*,
+               unsigned long long*) =
+      RL == 4 ? k_gc_seq<4, G> : RL == 8 ? k_gc_seq<8, G> : RL == 16 ? k_gc_seq<16, G> : k_gc_seq<32, G>;
+  if (smem > 227 * 1024) return false;
+  if (smem > 48 * 1024) LMS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int nsm = 0, occ = 0;
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  LMS_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  if (occ < 1) return false;
+  // co-resident CTAs (a thread may wait on any earlier unit's thread)
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * occ, units));
+  const int32_t* a_rec = rec.p;
+  const int32_t* a_vid = vid.p;
+  const int* a_ulo = ulo.p;
+  int64_t a_V = V;
+  int a_S = S;
+  int a_mw = MW;
+  int* a_ctr = ctr.p;
+  int8_t* a_cp = colpos.p;
+  int8_t* a_col = m->colour.p;
+  int* a_max = maxc;
+  int* a_err = m->err.p;
+  static unsigned long long* gst = nullptr;
+  unsigned long long* a_st = nullptr;
+  if (getenv("LMS_COLOUR_STATS")) {
+    if (!gst) LMS_TRY_CUDA(cudaMalloc(&gst, 8 * sizeof(unsigned long long)));
+    LMS_TRY_CUDA(cudaMemsetAsync(gst, 0, 8 * sizeof(unsigned long long), s));
+    a_st = gst;
+  }
+  void* args[] = {&a_rec, &a_vid, &a_ulo, &a_V, &a_S, &a_mw, &a_ctr, &a_cp, &a_col, &a_max, &a_err, &a_st};
+  const bool verbose = getenv("LMS_COLOUR_VERBOSE") != nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (verbose) {
+    LMS_TRY_CUDA(cudaEventCreate(&e0));
+    LMS_TRY_CUDA(cudaEventCreate(&e1));
+    LMS_TRY_CUDA(cudaEventRecord(e0, s));
+  }
+  LMS_TRY_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(threads), args, smem, s));
+  LMS_CHECK_LAUNCH();
+  if (verbose) {
+    LMS_TRY_CUDA(cudaEventRecord(e1, s));
+    LMS_TRY_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    LMS_TRY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    fprintf(stderr, "[colour] in-order: RL=%d S=%d mirror=%d blocks=%d units=%lld kernel %.3f ms\n", RL, S, MW,
+            blocks, (long long)units, ms);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  k_gc_scatter<<<Gv, 256, 0, s>>>(m->orig_id.p, m->fixed.p, colpos.p, V, m->colour.p);
+  LMS_CHECK_LAUNCH();
+  if (a_st) {
+    unsigned long long h2[8];
+    LMS_TRY_CUDA(cudaMemcpyAsync(h2, a_st, sizeof(h2), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "[colour stats] warp rounds=%llu lane progress=%llu (%.2f per round) mirror sweeps=%llu "
+            "units=%llu mean unit %.1f kcycles\n", h2[0], h2[1], h2[0] ? (double)h2[1] / h2[0] : 0.0, h2[2], h2[4],
+            h2[4] ? h2[3] / 1e3 / h2[4] : 0.0);
+  }
+  return true;
+}
+
 __global__ void k_max_deg(const int32_t* __restrict__ rp, int64_t V, int* out) {
   int mx = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
@@ -252,6 +609,18 @@ void compute_colouring(lms_mesh_s* m, cudaStream_t s) {
     check_err_flag(m, s, "colour (fixed vertices must have colour -1, free ones >= 0)");
   } else {
     m->colour.alloc(V, s);
+    const char* ce = getenv("LMS_COLOUR");
+    const bool want_jp = ce && !strcmp(ce, "jp");
+    if (!want_jp && colour_in_order(m, maxc.p, s)) {
+      k_check_all_coloured<<<Gv, 256, 0, s>>>(m->colour.p, m->fixed.p, V, m->err.p);
+      LMS_CHECK_LAUNCH();
+      check_err_flag(m, s, "colouring (more than 127 colours)");
+      int h = -1;
+      LMS_TRY_CUDA(cudaMemcpyAsync(&h, maxc.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      LMS_TRY_CUDA(cudaStreamSynchronize(s));
+      m->C = h + 1;
+      return;
+    }
     DBuf<int32_t> cnt(V, s), Q(V, s);
     DBuf<int> sizes(128, s);
     LMS_TRY_CUDA(cudaMemsetAsync(sizes.p, 0, 128 * sizeof(int), s));

@@ -318,3 +318,36 @@ def test_C4_full_bench_config():
     want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 3)
     assert bits_equal(gpu_coords(gm), want), gm.schedule_info()
     gm.close()
+
+
+@pytest.mark.parametrize("chunk", [8, 32])
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_colouring_in_order_many_units(chunk, shuffle, monkeypatch):
+    """The in-order colouring kernel with tiny chunks (units of 256 * chunk
+    positions: many units, so waits cross units through global memory), on
+    meshes whose lower neighbours reach back a whole row or plane, with the
+    identity orig_id and with a shuffled one: colours bit-exact against the
+    oracle's sequential greedy (reading Z2)."""
+    monkeypatch.setenv("LMS_GC_CHUNK", str(chunk))
+    for m in (meshgen.grid2d(301, 97, 0.3, seed=11), meshgen.kuhn3d(21, 0.25, seed=12)):
+        om = oracle.prepare(m)
+        fixed = oracle.boundary(m.V, m["elems"])
+        oid = np.random.default_rng(13).permutation(m.V).astype(np.int32) if shuffle else np.arange(m.V, dtype=np.int32)
+        want, C = oracle.colour(om["row_ptr"], om["col"], fixed, oid)
+        gm = lms.Mesh.from_csr([cuda(c) for c in m["coords"]], cuda(fixed), cuda(om["row_ptr"], torch.int32),
+                               cuda(om["col"], torch.int32), orig_id=cuda(oid))
+        try:
+            assert np.array_equal(np_(gm.colour()), want)
+            assert gm.info()["C"] == C
+        finally:
+            gm.close()
+
+
+def test_colouring_queue_fallback(monkeypatch):
+    """LMS_COLOUR=jp: the dependency-queue colouring (the fallback for an
+    orig_id that is not a permutation) is bit-exact too."""
+    monkeypatch.setenv("LMS_COLOUR", "jp")
+    m = meshgen.grid2d(301, 97, 0.3, seed=11)
+    om = oracle.prepare(m)
+    with gpu_mesh(m) as gm:
+        assert np.array_equal(np_(gm.colour()), om["colour"])

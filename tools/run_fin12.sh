@@ -1,0 +1,7 @@
+#!/bin/bash
+export LMS_COLOUR_VERBOSE=1
+for cfg in C4 C3 C5; do
+  for S in 64 128 256; do for sl in 0 32; do LMS_GC_SLEEP=$sl LMS_GC_CHUNK=$S REPS=2 timeout 300 python tools/time_colour.py $cfg 2>&1 | grep "\[colour\]" | tail -1 | sed "s/^/$cfg /"; done; done
+done > gpurun_out/fin12_colour.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q -k "build or colour or smoke" > gpurun_out/fin12_tests.log 2>&1; tail -1 gpurun_out/fin12_tests.log
+echo done
