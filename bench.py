@@ -302,6 +302,11 @@ def run_ours(args):
             "traffic_source": tr.get("source") if tr else None}
 
     # ---------------- e2e: whole path from pinned host buffers, every step
+    # (the device-timed mesh is released first: a user's job starts from host
+    # buffers, without another resident mesh fragmenting the allocator pool)
+    gm.close()
+    del coords_d, elems_d
+    torch.cuda.synchronize()
     e2e = None
     if not args.no_e2e:
         hc = [torch.from_numpy(c).pin_memory() for c in m["coords"]]
@@ -387,7 +392,6 @@ def run_ours(args):
             "setup_ms": setup,
         }
         print(json.dumps(line), flush=True)
-    gm.close()
     if world > 1:
         dist.destroy_process_group()
 

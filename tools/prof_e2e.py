@@ -16,6 +16,8 @@ ap.add_argument("--sweeps", type=int, default=50)
 ap.add_argument("--schedule", default="auto")
 ap.add_argument("--ordering", default="original")
 ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--prof", action="store_true", help="bracket the last step with cudaProfilerStart/Stop")
+ap.add_argument("--loop", action="store_true", help="also time bench.py-style back-to-back steps")
 a = ap.parse_args()
 m = meshgen.make_config(a.config)
 hc = [torch.from_numpy(c).pin_memory() for c in m["coords"]]
@@ -41,9 +43,26 @@ def step(prof):
     if prof:
         torch.cuda.profiler.stop()
     g.close()
-    names = ["h2d", "build_csr", "order+permute", "schedule", "sweeps", "d2h"]
+    mark()
+    names = ["h2d", "build_csr", "order+permute", "schedule", "sweeps", "d2h", "close"]
     return {n: round((t[i + 1] - t[i]) * 1e3, 2) for i, n in enumerate(names)} | {"total": round((t[-1] - t[0]) * 1e3, 2)}
 
 
 for i in range(a.steps):
-    print(json.dumps(step(i == a.steps - 1)))
+    print(json.dumps(step(i == a.steps - 1 and a.prof)))
+# back-to-back steps without intermediate syncs (bench.py's e2e loop)
+if a.loop:
+    def plain():
+        dc = [x.to(dev, non_blocking=True) for x in hc]; de = he.to(dev, non_blocking=True)
+        g = lms.Mesh.build_csr(dc, de)
+        p = g.order(a.ordering, 0); g.permute(p)
+        g.set_schedule(a.schedule, 0, 0); g.smooth(a.sweeps)
+        for o, h in zip(g.coords(), hout):
+            h.copy_(o, non_blocking=True)
+        torch.cuda.synchronize()
+        g.close()
+    for n in (1, 3):
+        t0 = time.perf_counter()
+        for _ in range(n):
+            plain()
+        print(json.dumps({"loop_steps": n, "ms_per_step": round((time.perf_counter() - t0) * 1e3 / n, 2)}))
