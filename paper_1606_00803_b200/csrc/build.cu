@@ -13,8 +13,11 @@
 //      lexicographic order, l^2 = dx*dx + dy*dy [+ dz*dz], every op separately
 //      rounded), q_v = (sum of q_e over attached elements, ascending element id)
 //      / count.
+#include <cstring>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
 #include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 
 #include "lms_internal.cuh"
@@ -83,6 +86,111 @@ __global__ void k_keys_to_csr(const unsigned long long* __restrict__ uk, const i
       fixed_or_null[c] = 1;
     }
   }
+}
+
+// ---- bucketed CSR: pairs scattered into per-source buckets, rows sorted and
+// de-duplicated locally (same CSR as the global sort: rows ascending, unique)
+__global__ void k_pair_count(const int32_t* __restrict__ el, int64_t n_el, int k, int32_t* cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x)
+    for (int s = 0; s < k; ++s) atomicAdd(&cnt[el[e * k + s]], k - 1);
+}
+__global__ void k_pair_scatter(const int32_t* __restrict__ el, int64_t n_el, int k, int32_t* cur, int32_t* buf) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_el; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t w[4];
+    for (int s = 0; s < k; ++s) w[s] = el[e * k + s];
+    for (int s = 0; s < k; ++s) {
+      const int32_t p = atomicAdd(&cur[w[s]], k - 1);
+      int o = 0;
+      for (int t = 0; t < k; ++t)
+        if (t != s) buf[p + o++] = w[t];
+    }
+  }
+}
+constexpr int CSR_ROW_CAP = 128;  // longer bucketed rows: the global-sort path
+// row v: sort its bucket, drop duplicates (in place), ndeg[v] = unique count;
+// triangles: a neighbour seen once is an edge of one triangle -> v is boundary
+__global__ void k_row_unique(const int32_t* __restrict__ off, int32_t* buf, int64_t V, int32_t* ndeg,
+                             uint8_t* fixed_or_null) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t b = off[v], L = off[v + 1] - b;
+    int32_t a[CSR_ROW_CAP];
+    for (int i = 0; i < L; ++i) {  // insertion sort
+      const int32_t x = buf[b + i];
+      int j = i;
+      while (j > 0 && a[j - 1] > x) {
+        a[j] = a[j - 1];
+        --j;
+      }
+      a[j] = x;
+    }
+    int u = 0;
+    bool single = false;
+    for (int i = 0; i < L;) {
+      int j = i + 1;
+      while (j < L && a[j] == a[i]) ++j;
+      single |= (j - i) == 1;
+      buf[b + u++] = a[i];
+      i = j;
+    }
+    ndeg[v] = u;
+    if (fixed_or_null && single) fixed_or_null[v] = 1;
+  }
+}
+// eight lanes per row: unique bucket prefix -> col
+__global__ void k_row_compact(const int32_t* __restrict__ off, const int32_t* __restrict__ buf,
+                              const int32_t* __restrict__ row_ptr, int64_t V, int32_t* __restrict__ col) {
+  const int sub = threadIdx.x & 7;
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3;
+  const int64_t ng = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  for (int64_t v = g; v < V; v += ng) {
+    const int32_t b = off[v], o = row_ptr[v], d = row_ptr[v + 1] - o;
+    for (int32_t j = sub; j < d; j += 8) col[o + j] = buf[b + j];
+  }
+}
+
+static bool build_csr_bucketed(lms_mesh_s* m, bool want_boundary, cudaStream_t s) {
+  const int k = m->k;
+  const int64_t n_el = m->n_el, V = m->V;
+  const unsigned Ge = grid_for(n_el, 256) > 8192 ? 8192 : grid_for(n_el, 256);
+  const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
+  DBuf<int32_t> cnt(V + 1, s), off(V + 1, s), mx(1, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(cnt.p, 0, (V + 1) * sizeof(int32_t), s));
+  k_pair_count<<<Ge, 256, 0, s>>>(m->elems.p, n_el, k, cnt.p);
+  LMS_CHECK_LAUNCH();
+  size_t tb = 0, tb2 = 0;
+  LMS_TRY_CUDA(cub::DeviceReduce::Max(nullptr, tb, cnt.p, mx.p, V, s));
+  LMS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt.p, off.p, V + 1, s));
+  DBuf<char> tmp(std::max(tb, tb2), s);
+  LMS_TRY_CUDA(cub::DeviceReduce::Max(tmp.p, tb, cnt.p, mx.p, V, s));
+  int h_mx = 0;
+  LMS_TRY_CUDA(cudaMemcpyAsync(&h_mx, mx.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  if (h_mx > CSR_ROW_CAP) return false;
+  LMS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, cnt.p, off.p, V + 1, s));
+  const int64_t nk = n_el * k * (k - 1);
+  DBuf<int32_t> buf(nk, s);
+  LMS_TRY_CUDA(cudaMemcpyAsync(cnt.p, off.p, (V + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));  // cursors
+  k_pair_scatter<<<Ge, 256, 0, s>>>(m->elems.p, n_el, k, cnt.p, buf.p);
+  LMS_CHECK_LAUNCH();
+  uint8_t* fx = nullptr;
+  if (want_boundary) {
+    LMS_TRY_CUDA(cudaMemsetAsync(m->fixed.p, 0, V, s));
+    if (k == 3) fx = m->fixed.p;
+  }
+  LMS_TRY_CUDA(cudaMemsetAsync(cnt.p + V, 0, sizeof(int32_t), s));
+  k_row_unique<<<Gv, 256, 0, s>>>(off.p, buf.p, V, cnt.p, fx);
+  LMS_CHECK_LAUNCH();
+  m->row_ptr.alloc(V + 1, s);
+  LMS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, cnt.p, m->row_ptr.p, V + 1, s));
+  int h_nnz = 0;
+  LMS_TRY_CUDA(cudaMemcpyAsync(&h_nnz, m->row_ptr.p + V, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  m->nnz = h_nnz;
+  m->col.alloc(m->nnz, s);
+  const unsigned Gw = grid_for(V * 8, 256) > 8192 ? 8192 : grid_for(V * 8, 256);
+  k_row_compact<<<Gw, 256, 0, s>>>(off.p, buf.p, m->row_ptr.p, V, m->col.p);
+  LMS_CHECK_LAUNCH();
+  return true;
 }
 
 __global__ void k_check_isolated(const int32_t* __restrict__ row_ptr, int64_t V, int* err) {
@@ -182,6 +290,15 @@ void build_csr_from_elems(lms_mesh_s* m, const int32_t* d_elems, bool want_bound
   const int b = bits_for(V);
   const int64_t nk = n_el * k * (k - 1);
   if (nk >= ((int64_t)1 << 31)) fail(LMS_E_ARG, "too many element pairs for the CSR build");
+  const char* ce = getenv("LMS_CSR");
+  if (!(ce && !strcmp(ce, "sort")) && build_csr_bucketed(m, want_boundary, s)) {
+    if (want_boundary && k == 4) boundary_faces(m, s);
+    const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
+    k_check_isolated<<<Gv, 256, 0, s>>>(m->row_ptr.p, V, m->err.p);
+    LMS_CHECK_LAUNCH();
+    check_err_flag(m, s, "lms_build_csr");
+    return;
+  }
   DBuf<unsigned long long> keys(nk, s), sorted(nk, s);
   k_expand_pairs<<<Ge, 256, 0, s>>>(m->elems.p, n_el, k, b, keys.p);
   LMS_CHECK_LAUNCH();
