@@ -27,7 +27,7 @@ LMS_STATUS = {0: "LMS_OK", -1: "LMS_E_ARG", -2: "LMS_E_INDEX", -3: "LMS_E_ISOLAT
 EXPORTS = ["lms_build_csr", "lms_mesh_from_csr", "lms_mesh_destroy", "lms_order", "lms_permute", "lms_smooth",
            "lms_set_schedule", "lms_mesh_info", "lms_schedule_info", "lms_export_coords", "lms_import_coords",
            "lms_export_csr", "lms_export_colour", "lms_export_fixed", "lms_export_orig_id", "lms_export_elems",
-           "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_set_tiling", "lms_schedule_info2",
+           "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_cache_release", "lms_set_tiling", "lms_schedule_info2",
            "lms_smooth_colour", "lms_gather_coords", "lms_scatter_coords"]
 
 
@@ -77,6 +77,7 @@ def load_library(build: bool = True):
         "lms_scatter_coords": [P, P, i64, P, P],
         "lms_last_error": [],
         "lms_kernel_launches": [],
+        "lms_cache_release": [],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -85,6 +86,7 @@ def load_library(build: bool = True):
     L.lms_mesh_destroy.restype = None
     L.lms_last_error.restype = ct.c_char_p
     L.lms_kernel_launches.restype = i64
+    L.lms_cache_release.restype = None
     _lib = L
     return L
 
@@ -95,6 +97,11 @@ def lib():
 
 def kernel_launches() -> int:
     return int(lib().lms_kernel_launches())
+
+
+def cache_release() -> None:
+    """lms_cache_release: hand the library's cached scratch blocks back to the CUDA pool."""
+    lib().lms_cache_release()
 
 
 def _check(st: int, what: str):

@@ -3,6 +3,9 @@
 #include <atomic>
 #include <cstring>
 
+#include <chrono>
+#include <cstdio>
+
 #include "lms_internal.cuh"
 
 namespace lms {
@@ -89,6 +92,19 @@ static void keep_pool_memory(int dev) {
 }
 
 static lms_mesh_s* new_mesh(int dim, int64_t V, cudaStream_t s) {
+  if (getenv("LMS_BUILD_VERBOSE")) {
+    int dev = 0;
+    cudaMemPool_t pool, cur;
+    cudaGetDevice(&dev);
+    cudaDeviceGetDefaultMemPool(&pool, dev);
+    cudaDeviceGetMemPool(&cur, dev);
+    uint64_t rc = 0, uc = 0, th = 0;
+    cudaMemPoolGetAttribute(cur, cudaMemPoolAttrReservedMemCurrent, &rc);
+    cudaMemPoolGetAttribute(cur, cudaMemPoolAttrUsedMemCurrent, &uc);
+    cudaMemPoolGetAttribute(cur, cudaMemPoolAttrReleaseThreshold, &th);
+    fprintf(stderr, "[pool] current==default %d reserved %.2f GB used %.2f GB threshold %.1f GB\n", (int)(pool == cur),
+            rc / 1e9, uc / 1e9, th / 1e9);
+  }
   auto* m = new lms_mesh_s();
   m->dim = dim;
   m->V = V;
@@ -122,6 +138,16 @@ lms_status lms_build_csr(int32_t dim, int64_t n_vertices, const double* const* d
   if (n_elems * verts_per_elem >= ((int64_t)1 << 31)) fail(LMS_E_ARG, "too many elements for int32 indexing");
   check_coords(dim, d_coords);
   cudaStream_t s = (cudaStream_t)stream;
+  // LMS_BUILD_VERBOSE: synchronising phase timings on stderr
+  const bool tv = getenv("LMS_BUILD_VERBOSE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!tv) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[build_csr] %-12s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   m = new_mesh(dim, n_vertices, s);
   try {
     m->k = verts_per_elem;
@@ -133,11 +159,15 @@ lms_status lms_build_csr(int32_t dim, int64_t n_vertices, const double* const* d
     m->fixed.alloc(n_vertices, s);
     if (d_fixed)
       LMS_TRY_CUDA(cudaMemcpyAsync(m->fixed.p, d_fixed, n_vertices, cudaMemcpyDeviceToDevice, s));
+    mark("coords");
     build_csr_from_elems(m, d_elems, d_fixed == nullptr, s);
+    mark("csr");
     m->orig_id.alloc(n_vertices, s);
     fill_iota(m->orig_id.p, n_vertices, s);
     compute_colouring(m, s);   // colour from orig_id = input label (reading Z2)
+    mark("colouring");
     m->n_free = count_free(m, s);
+    mark("count");
   } catch (...) {
     delete m;
     throw;

@@ -1,0 +1,113 @@
+// alloc.cu -- scratch allocator behind DBuf (lms_internal.cuh).
+//
+// Every library call allocates and frees its temporaries stream-ordered; an
+// e2e step of C4 makes a few hundred such calls.  cudaMallocAsync from a pool
+// whose memory is retained is cheap on average, but each call is a driver API
+// call, and measured e2e steps showed occasional stalls of tens to hundreds of
+// ms inside them.  This keeps freed blocks in a host-side cache keyed by
+// (stream, size) and hands them back to the next allocation on the same
+// stream: the blocks' previous uses precede any new use in that stream's
+// order, exactly the guarantee cudaFreeAsync + cudaMallocAsync gave.  A block
+// is reused for a request of at least 3/4 of its size.  Cached bytes are
+// capped (LMS_CACHE_GB, default 16 GB; 0 disables the cache); beyond the cap,
+// and on lms_cache_release(), blocks go back to the pool with cudaFreeAsync on
+// their stream.
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <unordered_map>
+
+#include "lms_internal.cuh"
+
+namespace lms {
+
+namespace {
+struct Cache {
+  std::mutex mu;
+  std::unordered_map<void*, size_t> live;                         // block -> bytes
+  std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free_;  // (stream, bytes) -> blocks
+  size_t cached = 0;
+  size_t cap = 0;
+  bool init = false;
+};
+Cache& cache() {
+  static Cache* c = new Cache();  // never destroyed: frees may run at exit
+  return *c;
+}
+size_t round_bytes(size_t b) {
+  if (b <= 4096) return 4096;
+  const size_t g = b < ((size_t)1 << 20) ? 4096 : ((size_t)2 << 20);  // 4 KB, then 2 MB granules
+  return (b + g - 1) / g * g;
+}
+}  // namespace
+
+void* ws_alloc(size_t bytes, cudaStream_t s) {
+  Cache& c = cache();
+  const size_t rb = round_bytes(bytes);
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    if (!c.init) {
+      double gb = 16.0;
+      if (const char* e = getenv("LMS_CACHE_GB")) gb = atof(e);
+      c.cap = gb > 0 ? (size_t)(gb * 1073741824.0) : 0;
+      c.init = true;
+    }
+    if (c.cap) {
+      // smallest cached block of this stream with rb <= size <= 4/3 rb
+      auto it = c.free_.lower_bound({s, rb});
+      if (it != c.free_.end() && it->first.first == s && it->first.second <= rb + rb / 3 && !it->second.empty()) {
+        void* p = it->second.back();
+        it->second.pop_back();
+        c.cached -= it->first.second;
+        c.live[p] = it->first.second;
+        if (it->second.empty()) c.free_.erase(it);
+        return p;
+      }
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, rb, s);
+  if (e == cudaErrorMemoryAllocation) {  // give the cache back to the pool and retry once
+    cudaGetLastError();
+    lms_cache_release();
+    e = cudaMallocAsync(&p, rb, s);
+  }
+  LMS_TRY_CUDA(e);
+  std::lock_guard<std::mutex> g(c.mu);
+  c.live[p] = rb;
+  return p;
+}
+
+void ws_free(void* p, cudaStream_t s) {
+  if (!p) return;
+  Cache& c = cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  auto it = c.live.find(p);
+  const size_t b = it == c.live.end() ? 0 : it->second;
+  if (it != c.live.end()) c.live.erase(it);
+  if (!c.cap || b == 0 || b > c.cap) {
+    cudaFreeAsync(p, s);
+    return;
+  }
+  c.free_[{s, b}].push_back(p);
+  c.cached += b;
+  while (c.cached > c.cap && !c.free_.empty()) {  // over the cap: largest blocks back to the pool
+    auto last = std::prev(c.free_.end());
+    void* q = last->second.back();
+    last->second.pop_back();
+    c.cached -= last->first.second;
+    cudaFreeAsync(q, last->first.first);
+    if (last->second.empty()) c.free_.erase(last);
+  }
+}
+
+}  // namespace lms
+
+extern "C" void lms_cache_release(void) {
+  lms::Cache& c = lms::cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  for (auto& kv : c.free_)
+    for (void* q : kv.second) cudaFreeAsync(q, kv.first.first);
+  c.free_.clear();
+  c.cached = 0;
+}

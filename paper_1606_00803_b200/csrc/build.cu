@@ -13,6 +13,8 @@
 //      lexicographic order, l^2 = dx*dx + dy*dy [+ dz*dz], every op separately
 //      rounded), q_v = (sum of q_e over attached elements, ascending element id)
 //      / count.
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -107,15 +109,18 @@ __global__ void k_pair_scatter(const int32_t* __restrict__ el, int64_t n_el, int
   }
 }
 constexpr int CSR_ROW_CAP = 128;  // longer bucketed rows: the global-sort path
-// row v: sort its bucket, drop duplicates (in place), ndeg[v] = unique count;
-// triangles: a neighbour seen once is an edge of one triangle -> v is boundary
+// row v: sort its bucket in place (no per-thread stack array: a kernel that
+// needs a large local-memory reservation can make the driver resize it at
+// launch, an occasional stall of hundreds of ms), drop duplicates, ndeg[v] =
+// unique count; triangles: a neighbour seen once is an edge of one triangle ->
+// v is boundary
 __global__ void k_row_unique(const int32_t* __restrict__ off, int32_t* buf, int64_t V, int32_t* ndeg,
                              uint8_t* fixed_or_null) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t b = off[v], L = off[v + 1] - b;
-    int32_t a[CSR_ROW_CAP];
-    for (int i = 0; i < L; ++i) {  // insertion sort
-      const int32_t x = buf[b + i];
+    int32_t* a = buf + off[v];
+    const int32_t L = off[v + 1] - off[v];
+    for (int i = 1; i < L; ++i) {  // insertion sort (rows are short)
+      const int32_t x = a[i];
       int j = i;
       while (j > 0 && a[j - 1] > x) {
         a[j] = a[j - 1];
@@ -126,10 +131,11 @@ __global__ void k_row_unique(const int32_t* __restrict__ off, int32_t* buf, int6
     int u = 0;
     bool single = false;
     for (int i = 0; i < L;) {
+      const int32_t x = a[i];
       int j = i + 1;
-      while (j < L && a[j] == a[i]) ++j;
+      while (j < L && a[j] == x) ++j;
       single |= (j - i) == 1;
-      buf[b + u++] = a[i];
+      a[u++] = x;
       i = j;
     }
     ndeg[v] = u;
@@ -149,14 +155,25 @@ __global__ void k_row_compact(const int32_t* __restrict__ off, const int32_t* __
 }
 
 static bool build_csr_bucketed(lms_mesh_s* m, bool want_boundary, cudaStream_t s) {
+  const bool tv = getenv("LMS_BUILD_VERBOSE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!tv) return;
+    cudaStreamSynchronize(s);
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[csr] %-10s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
   const int k = m->k;
   const int64_t n_el = m->n_el, V = m->V;
   const unsigned Ge = grid_for(n_el, 256) > 8192 ? 8192 : grid_for(n_el, 256);
   const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
   DBuf<int32_t> cnt(V + 1, s), off(V + 1, s), mx(1, s);
   LMS_TRY_CUDA(cudaMemsetAsync(cnt.p, 0, (V + 1) * sizeof(int32_t), s));
+  mark("alloc0");
   k_pair_count<<<Ge, 256, 0, s>>>(m->elems.p, n_el, k, cnt.p);
   LMS_CHECK_LAUNCH();
+  mark("count");
   size_t tb = 0, tb2 = 0;
   LMS_TRY_CUDA(cub::DeviceReduce::Max(nullptr, tb, cnt.p, mx.p, V, s));
   LMS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb2, cnt.p, off.p, V + 1, s));
@@ -168,10 +185,13 @@ static bool build_csr_bucketed(lms_mesh_s* m, bool want_boundary, cudaStream_t s
   if (h_mx > CSR_ROW_CAP) return false;
   LMS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, cnt.p, off.p, V + 1, s));
   const int64_t nk = n_el * k * (k - 1);
+  mark("scan");
   DBuf<int32_t> buf(nk, s);
+  mark("alloc_buf");
   LMS_TRY_CUDA(cudaMemcpyAsync(cnt.p, off.p, (V + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));  // cursors
   k_pair_scatter<<<Ge, 256, 0, s>>>(m->elems.p, n_el, k, cnt.p, buf.p);
   LMS_CHECK_LAUNCH();
+  mark("scatter");
   uint8_t* fx = nullptr;
   if (want_boundary) {
     LMS_TRY_CUDA(cudaMemsetAsync(m->fixed.p, 0, V, s));
@@ -180,6 +200,7 @@ static bool build_csr_bucketed(lms_mesh_s* m, bool want_boundary, cudaStream_t s
   LMS_TRY_CUDA(cudaMemsetAsync(cnt.p + V, 0, sizeof(int32_t), s));
   k_row_unique<<<Gv, 256, 0, s>>>(off.p, buf.p, V, cnt.p, fx);
   LMS_CHECK_LAUNCH();
+  mark("unique");
   m->row_ptr.alloc(V + 1, s);
   LMS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb2, cnt.p, m->row_ptr.p, V + 1, s));
   int h_nnz = 0;
@@ -188,8 +209,10 @@ static bool build_csr_bucketed(lms_mesh_s* m, bool want_boundary, cudaStream_t s
   m->nnz = h_nnz;
   m->col.alloc(m->nnz, s);
   const unsigned Gw = grid_for(V * 8, 256) > 8192 ? 8192 : grid_for(V * 8, 256);
+  mark("scan2");
   k_row_compact<<<Gw, 256, 0, s>>>(off.p, buf.p, m->row_ptr.p, V, m->col.p);
   LMS_CHECK_LAUNCH();
+  mark("compact");
   return true;
 }
 

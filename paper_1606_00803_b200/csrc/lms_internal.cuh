@@ -39,7 +39,16 @@ struct Err {
 inline void fail(lms_status st, const std::string& msg) { throw Err{st, msg}; }
 
 // ----------------------------------------------------------------- device buffers
-// RAII device buffer allocated stream-ordered (cudaMallocAsync) on the handle's stream.
+// Scratch allocator (alloc.cu): stream-ordered cudaMallocAsync behind a small
+// cache of freed blocks keyed by (stream, size).  A block freed on stream s is
+// reused only by a later allocation on the same stream, so the stream order
+// that made cudaFreeAsync safe makes the reuse safe too.  Capped by
+// LMS_CACHE_GB (default 16; 0 = off); cached blocks go back to the pool
+// (cudaFreeAsync) beyond the cap and on lms_cache_release.
+void* ws_alloc(size_t bytes, cudaStream_t s);
+void ws_free(void* p, cudaStream_t s);
+
+// RAII device buffer allocated stream-ordered on the handle's stream.
 template <typename T>
 struct DBuf {
   T* p = nullptr;
@@ -54,7 +63,7 @@ struct DBuf {
     // the old buffer is freed in the order of the NEW buffer's stream (the
     // stream of the call that produced the replacement)
     if (this != &o) {
-      if (p) cudaFreeAsync(p, o.s);
+      if (p) ws_free(p, o.s);
       p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0;
     }
     return *this;
@@ -64,10 +73,10 @@ struct DBuf {
     release();
     s = st;
     n = count;
-    if (count) LMS_TRY_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T), st));
+    if (count) p = static_cast<T*>(ws_alloc(count * sizeof(T), st));
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) ws_free(p, s);
     p = nullptr;
     n = 0;
   }
