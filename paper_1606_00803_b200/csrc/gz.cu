@@ -109,26 +109,46 @@ __global__ void k_gz_lvl0(const uint8_t* __restrict__ fixed, const int32_t* __re
     keys[v] = fixed[v] ? ~0ull : (((uint64_t)(uint32_t)tile_of[v] << 32) | (uint32_t)v);
 }
 
-// expansion counts: neighbours of free entries (+1 for the entry itself if self)
+// expansion counts: neighbours of free entries (+1 for the entry itself if
+// self).  tile_of != nullptr (ring 1 from the owned free vertices): only
+// neighbours in another tile or fixed -- the tile's own free vertices are
+// ring 0, so the rest would be dropped by the set difference anyway, and
+// skipping them shrinks the candidate list from ~deg x V to the tiles' rims.
+__device__ __forceinline__ bool gz_keep(const int32_t* __restrict__ tile_of, const uint8_t* __restrict__ fixed,
+                                        int32_t u, uint32_t tile) {
+  return !tile_of || fixed[u] || (uint32_t)tile_of[u] != tile;
+}
 __global__ void k_gz_cnt(const uint64_t* __restrict__ keys, int64_t n, const int32_t* __restrict__ rp,
-                         const uint8_t* __restrict__ fixed, int self, int64_t* cnt) {
+                         const int32_t* __restrict__ col, const uint8_t* __restrict__ fixed,
+                         const int32_t* __restrict__ tile_of, int self, int64_t* cnt) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t v = (int32_t)(keys[i] & 0xffffffffull);
-    cnt[i] = (fixed[v] ? 0 : (int64_t)(rp[v + 1] - rp[v])) + self;
+    const uint64_t key = keys[i];
+    const int32_t v = (int32_t)(key & 0xffffffffull);
+    const uint32_t tile = (uint32_t)(key >> 32);
+    int64_t c = self;
+    if (!fixed[v]) {
+      if (!tile_of) c += rp[v + 1] - rp[v];
+      else
+        for (int32_t e = rp[v]; e < rp[v + 1]; ++e) c += gz_keep(tile_of, fixed, col[e], tile);
+    }
+    cnt[i] = c;
   }
 }
 
 __global__ void k_gz_emit(const uint64_t* __restrict__ keys, int64_t n, const int64_t* __restrict__ off,
                           const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                          const uint8_t* __restrict__ fixed, int self, uint64_t* out) {
+                          const uint8_t* __restrict__ fixed, const int32_t* __restrict__ tile_of, int self,
+                          uint64_t* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t key = keys[i];
     const uint64_t hi = key & 0xffffffff00000000ull;
     const int32_t v = (int32_t)(key & 0xffffffffull);
+    const uint32_t tile = (uint32_t)(key >> 32);
     int64_t o = off[i];
     if (self) out[o++] = key;
     if (!fixed[v])
-      for (int32_t e = rp[v]; e < rp[v + 1]; ++e) out[o++] = hi | (uint32_t)col[e];
+      for (int32_t e = rp[v]; e < rp[v + 1]; ++e)
+        if (gz_keep(tile_of, fixed, col[e], tile)) out[o++] = hi | (uint32_t)col[e];
   }
 }
 
@@ -1451,16 +1471,16 @@ static int64_t scan_i64(const int64_t* in, int64_t n, int64_t* out, cudaStream_t
 
 // expand entries: neighbours of free entries (+ the entries themselves if self)
 static int64_t expand(const DBuf<uint64_t>& keys, int64_t n, lms_mesh_s* m, int self, DBuf<uint64_t>& out,
-                      cudaStream_t s) {
+                      cudaStream_t s, const int32_t* tile_of = nullptr) {
   DBuf<int64_t> cnt(n > 0 ? n : 1, s), off(n + 1, s);
   if (n > 0) {
-    k_gz_cnt<<<gsz(n), 256, 0, s>>>(keys.p, n, m->row_ptr.p, m->fixed.p, self, cnt.p);
+    k_gz_cnt<<<gsz(n), 256, 0, s>>>(keys.p, n, m->row_ptr.p, m->col.p, m->fixed.p, tile_of, self, cnt.p);
     LMS_CHECK_LAUNCH();
   }
   const int64_t tot = scan_i64(cnt.p, n, off.p, s);
   out.alloc(tot > 0 ? tot : 1, s);
   if (n > 0 && tot > 0) {
-    k_gz_emit<<<gsz(n), 256, 0, s>>>(keys.p, n, off.p, m->row_ptr.p, m->col.p, m->fixed.p, self, out.p);
+    k_gz_emit<<<gsz(n), 256, 0, s>>>(keys.p, n, off.p, m->row_ptr.p, m->col.p, m->fixed.p, tile_of, self, out.p);
     LMS_CHECK_LAUNCH();
   }
   return tot;
@@ -1589,7 +1609,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   // levels 1..D-1: breadth-first rings through free vertices, per tile
   for (int L = 1; L < D; ++L) {
     DBuf<uint64_t> cand;
-    int64_t nc = expand(lev[L - 1], nlev[L - 1], m, 0, cand, s);
+    int64_t nc = expand(lev[L - 1], nlev[L - 1], m, 0, cand, s, L == 1 ? tile_of.p : nullptr);
     sort_keys(cand, nc, end_bit, s);
     nc = unique_keys(cand, nc, s);
     DBuf<uint8_t> keep(nc > 0 ? nc : 1, s);
@@ -1626,9 +1646,11 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   const int64_t nU = read_i64(nu.p, true, s);
   for (int L = 1; L < D; ++L) lev[L].release();
   mark("update set");
-  // region = U and its neighbours, sorted by (tile, id)
+  // region = U and its neighbours, sorted by (tile, id).  Every owned free
+  // vertex is in U (level 0, colour <= D - 1) and enters through `self`, so
+  // the expansion skips in-tile free neighbours (the tile_of filter)
   DBuf<uint64_t> reg;
-  int64_t nreg_all = expand(ukey, nU, m, 1, reg, s);
+  int64_t nreg_all = expand(ukey, nU, m, 1, reg, s, tile_of.p);
   sort_keys(reg, nreg_all, end_bit, s);
   nreg_all = unique_keys(reg, nreg_all, s);
   DBuf<int64_t> reg_off(K + 1, s);
