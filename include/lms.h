@@ -210,6 +210,17 @@ int64_t lms_kernel_launches(void);
  * destroying a stream the library was used on; the blocks are freed in each
  * owning stream's order.  Never fails. */
 void lms_cache_release(void);
+/* Route the library's device allocations (mesh buffers and every call's
+ * temporaries) through a caller's allocator, e.g. the torch caching
+ * allocator; (NULL, NULL) restores the default (cudaMallocAsync behind the
+ * scratch cache above).  alloc(bytes, stream, ctx) returns device memory
+ * usable in `stream` order (NULL = out of memory -> LMS_E_NOMEM); free(p,
+ * stream, ctx) is called in the order of the stream that last used p.
+ * Blocks keep the allocator that made them: switch only when no handle is
+ * alive.  LMS_E_ARG if exactly one of alloc / free is NULL.  Not
+ * thread-safe against concurrent library calls. */
+lms_status lms_set_allocator(void* (*alloc)(size_t bytes, lms_stream_t stream, void* ctx),
+                             void (*free_fn)(void* p, lms_stream_t stream, void* ctx), void* ctx);
 
 #ifdef __cplusplus
 }

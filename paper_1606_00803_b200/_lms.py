@@ -27,7 +27,7 @@ LMS_STATUS = {0: "LMS_OK", -1: "LMS_E_ARG", -2: "LMS_E_INDEX", -3: "LMS_E_ISOLAT
 EXPORTS = ["lms_build_csr", "lms_mesh_from_csr", "lms_mesh_destroy", "lms_order", "lms_permute", "lms_smooth",
            "lms_set_schedule", "lms_mesh_info", "lms_schedule_info", "lms_export_coords", "lms_import_coords",
            "lms_export_csr", "lms_export_colour", "lms_export_fixed", "lms_export_orig_id", "lms_export_elems",
-           "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_cache_release", "lms_set_tiling", "lms_schedule_info2",
+           "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_cache_release", "lms_set_allocator", "lms_set_tiling", "lms_schedule_info2",
            "lms_smooth_colour", "lms_gather_coords", "lms_scatter_coords"]
 
 
@@ -78,6 +78,7 @@ def load_library(build: bool = True):
         "lms_last_error": [],
         "lms_kernel_launches": [],
         "lms_cache_release": [],
+        "lms_set_allocator": [P, P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -97,6 +98,36 @@ def lib():
 
 def kernel_launches() -> int:
     return int(lib().lms_kernel_launches())
+
+
+# lms_set_allocator callbacks: void* alloc(size_t, stream, ctx), void free(void*, stream, ctx)
+_ALLOC_FN = ct.CFUNCTYPE(ct.c_void_p, ct.c_size_t, ct.c_void_p, ct.c_void_p)
+_FREE_FN = ct.CFUNCTYPE(None, ct.c_void_p, ct.c_void_p, ct.c_void_p)
+_alloc_keep = None  # the active callbacks (kept alive while installed)
+
+
+def use_torch_allocator(enable: bool = True) -> None:
+    """lms_set_allocator with torch's caching allocator (enable=True), or back to
+    the library's default (cudaMallocAsync behind its scratch cache).  Switch
+    only while no Mesh is alive: a block is freed by the allocator that made it."""
+    global _alloc_keep
+    if enable:
+        def _alloc(n, stream, ctx):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(n), torch.cuda.current_device(), stream or 0)
+            except Exception:  # out of memory -> NULL -> LMS_E_NOMEM
+                return None
+
+        def _free(p, stream, ctx):
+            torch.cuda.caching_allocator_delete(p)
+
+        cbs = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+        _check(lib().lms_set_allocator(ct.cast(cbs[0], ct.c_void_p), ct.cast(cbs[1], ct.c_void_p), None),
+               "lms_set_allocator")
+        _alloc_keep = cbs
+    else:
+        _check(lib().lms_set_allocator(None, None, None), "lms_set_allocator")
+        _alloc_keep = None
 
 
 def cache_release() -> None:

@@ -22,6 +22,16 @@
 namespace lms {
 
 namespace {
+// caller-supplied allocator (lms_set_allocator); null = cudaMallocAsync + cache
+struct UserAlloc {
+  void* (*alloc)(size_t, lms_stream_t, void*) = nullptr;
+  void (*free)(void*, lms_stream_t, void*) = nullptr;
+  void* ctx = nullptr;
+};
+UserAlloc& user() {
+  static UserAlloc u;
+  return u;
+}
 struct Cache {
   std::mutex mu;
   std::unordered_map<void*, size_t> live;                         // block -> bytes
@@ -44,6 +54,13 @@ size_t round_bytes(size_t b) {
 void* ws_alloc(size_t bytes, cudaStream_t s) {
   Cache& c = cache();
   const size_t rb = round_bytes(bytes);
+  if (user().alloc) {
+    void* p = user().alloc(rb, (lms_stream_t)s, user().ctx);
+    if (!p) fail(LMS_E_NOMEM, "lms_set_allocator: the caller's allocator returned NULL");
+    std::lock_guard<std::mutex> g(c.mu);
+    c.live[p] = 0;  // 0 = the caller's block
+    return p;
+  }
   {
     std::lock_guard<std::mutex> g(c.mu);
     if (!c.init) {
@@ -84,8 +101,14 @@ void ws_free(void* p, cudaStream_t s) {
   std::lock_guard<std::mutex> g(c.mu);
   auto it = c.live.find(p);
   const size_t b = it == c.live.end() ? 0 : it->second;
+  const bool mine = it != c.live.end() && it->second != 0;
+  if (it != c.live.end() && it->second == 0) {  // the caller's allocator
+    c.live.erase(it);
+    if (user().free) user().free(p, (lms_stream_t)s, user().ctx);
+    return;
+  }
   if (it != c.live.end()) c.live.erase(it);
-  if (!c.cap || b == 0 || b > c.cap) {
+  if (!mine || !c.cap || b > c.cap) {
     cudaFreeAsync(p, s);
     return;
   }
@@ -102,6 +125,18 @@ void ws_free(void* p, cudaStream_t s) {
 }
 
 }  // namespace lms
+
+extern "C" lms_status lms_set_allocator(void* (*alloc)(size_t, lms_stream_t, void*),
+                                        void (*free_fn)(void*, lms_stream_t, void*), void* ctx) {
+  if ((alloc == nullptr) != (free_fn == nullptr)) return LMS_E_ARG;
+  lms_cache_release();  // cached blocks came from the previous allocator
+  lms::Cache& c = lms::cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  lms::user().alloc = alloc;
+  lms::user().free = free_fn;
+  lms::user().ctx = ctx;
+  return LMS_OK;
+}
 
 extern "C" void lms_cache_release(void) {
   lms::Cache& c = lms::cache();

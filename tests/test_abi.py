@@ -60,3 +60,14 @@ def test_no_cpu_fallback_without_gpu():
     import paper_1606_00803_b200 as lms
     with pytest.raises(Exception):
         lms.Mesh.build_csr([torch.zeros(3, dtype=torch.float64)] * 2, torch.zeros((1, 3), dtype=torch.int32))
+
+
+def test_set_allocator_arguments():
+    """lms_set_allocator: exactly one hook NULL is LMS_E_ARG; (NULL, NULL)
+    restores the default allocator (no device work, so it runs on CPU)."""
+    import ctypes as ct
+    import paper_1606_00803_b200 as lms
+    L = lms.lib()
+    cb = ct.CFUNCTYPE(ct.c_void_p, ct.c_size_t, ct.c_void_p, ct.c_void_p)(lambda n, s, c: None)
+    assert L.lms_set_allocator(ct.cast(cb, ct.c_void_p), None, None) == -1  # LMS_E_ARG
+    assert L.lms_set_allocator(None, None, None) == 0

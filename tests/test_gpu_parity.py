@@ -351,3 +351,23 @@ def test_colouring_queue_fallback(monkeypatch):
     om = oracle.prepare(m)
     with gpu_mesh(m) as gm:
         assert np.array_equal(np_(gm.colour()), om["colour"])
+
+
+def test_torch_allocator_backs_the_library():
+    """lms_set_allocator with torch's caching allocator: every buffer of the
+    build, colouring, schedule and sweeps comes from torch, results bit-exact."""
+    m = meshgen.grid2d(200, 150, 0.3, seed=21)
+    om = oracle.prepare(m)
+    want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 3)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    lms.use_torch_allocator(True)
+    try:
+        with gpu_mesh(m) as gm:
+            assert torch.cuda.memory_allocated() > before  # the handle's buffers are torch's
+            gm.set_schedule("gz", tile=500, lag=1)
+            gm.smooth(3)
+            assert bits_equal(gpu_coords(gm), want)
+        torch.cuda.synchronize()
+    finally:
+        lms.use_torch_allocator(False)
