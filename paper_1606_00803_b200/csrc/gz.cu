@@ -349,6 +349,10 @@ __global__ void k_gzd_region(const uint64_t* __restrict__ reg, int64_t n, int C,
   }
 }
 
+// 8-bit masks grouped by popcount, ascending within a group (gap placement)
+__constant__ uint8_t kGapMasks[256] = {0, 1, 2, 4, 8, 16, 32, 64, 128, 3, 5, 6, 9, 10, 12, 17, 18, 20, 24, 33, 34, 36, 40, 48, 65, 66, 68, 72, 80, 96, 129, 130, 132, 136, 144, 160, 192, 7, 11, 13, 14, 19, 21, 22, 25, 26, 28, 35, 37, 38, 41, 42, 44, 49, 50, 52, 56, 67, 69, 70, 73, 74, 76, 81, 82, 84, 88, 97, 98, 100, 104, 112, 131, 133, 134, 137, 138, 140, 145, 146, 148, 152, 161, 162, 164, 168, 176, 193, 194, 196, 200, 208, 224, 15, 23, 27, 29, 30, 39, 43, 45, 46, 51, 53, 54, 57, 58, 60, 71, 75, 77, 78, 83, 85, 86, 89, 90, 92, 99, 101, 102, 105, 106, 108, 113, 114, 116, 120, 135, 139, 141, 142, 147, 149, 150, 153, 154, 156, 163, 165, 166, 169, 170, 172, 177, 178, 180, 184, 195, 197, 198, 201, 202, 204, 209, 210, 212, 216, 225, 226, 228, 232, 240, 31, 47, 55, 59, 61, 62, 79, 87, 91, 93, 94, 103, 107, 109, 110, 115, 117, 118, 121, 122, 124, 143, 151, 155, 157, 158, 167, 171, 173, 174, 179, 181, 182, 185, 186, 188, 199, 203, 205, 206, 211, 213, 214, 217, 218, 220, 227, 229, 230, 233, 234, 236, 241, 242, 244, 248, 63, 95, 111, 119, 123, 125, 126, 159, 175, 183, 187, 189, 190, 207, 215, 219, 221, 222, 231, 235, 237, 238, 243, 245, 246, 249, 250, 252, 127, 191, 223, 239, 247, 251, 253, 254, 255};
+__constant__ uint16_t kGapOff[10] = {0, 1, 9, 37, 93, 163, 219, 247, 255, 256};
+
 // slot of vertex g in a tile's region (ids sorted ascending, in shared memory)
 __device__ __forceinline__ int region_slot(const uint32_t* __restrict__ rid, int nr, uint32_t g) {
   int lo = 0, n = nr;
@@ -388,6 +392,8 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
   __shared__ uint8_t gz_pos[8 * 64];
   __shared__ uint8_t gz_cnt[8 * 64];
   __shared__ uint8_t gz_ord[8 * 64];
+  __shared__ uint8_t gz_gap[8 * 64];
+  __shared__ uint16_t gz_slot[8 * 64 * 8];  // rows of 8: neighbour slots found in the bank pass
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int nwib = blockDim.x >> 5;
@@ -397,6 +403,8 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
   uint8_t* ps = gz_pos + wib * 64;
   uint8_t* cn = gz_cnt + wib * 64;
   uint8_t* od = gz_ord + wib * 64;
+  uint8_t* gp = gz_gap + wib * 64;  // row positions used by each update's neighbours (rows of 8)
+  uint16_t* sl8 = gz_slot + wib * 64 * 8;
   for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
     const int64_t ra = reg_off[k], rb = reg_off[k + 1];
     const int nr = (int)(rb - ra);
@@ -433,7 +441,9 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
             cnt = 1;
             const int32_t b = rp[v], d = rp[v + 1] - b;
             for (int w = 0; w < d && w < 8; ++w) {
-              bk[e * 9 + 1 + w] = (uint8_t)(region_slot(gz_rid, nr, (uint32_t)col[b + w]) & 7);
+              const int sl = region_slot(gz_rid, nr, (uint32_t)col[b + w]);
+              sl8[e * 8 + w] = (uint16_t)sl;
+              bk[e * 9 + 1 + w] = (uint8_t)(sl & 7);
               ++cnt;
             }
           }
@@ -481,6 +491,52 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
           }
         }
         __syncwarp();
+        // Row positions: the kernel gathers neighbour position w of all 8
+        // lanes of a quarter-warp at once and skips padding anywhere, summing
+        // over increasing w -- so an update's d neighbours may occupy any d of
+        // the 8 positions in CSR order (the sum order is unchanged).  Lane a
+        // places group a's updates (most neighbours first) at the positions
+        // whose banks are least used by the group so far, lowest mask on ties.
+        // eight lanes per group, all groups at once: group a's members are the
+        // updates at positions 8a .. 8a+7, placed in that order (most banks
+        // first); sub-lane j evaluates masks j, j + 8, ... of the popcount
+        // class and the group takes the arg-min (lowest mask on ties)
+        for (int e = lane; e < U; e += 32) od[ps[e]] = (uint8_t)e;  // od := position -> update
+        __syncwarp();
+        for (int a0 = 0; a0 < ng; a0 += 4) {
+          const int a = a0 + (lane >> 3), sub = lane & 7;
+          uint64_t occ = 0;  // bit 8w + bank: bank already read at position w
+          for (int j = 0; j < 8; ++j) {
+            const int e = a < ng ? od[8 * a + j] : 0;
+            const int dn = a < ng && cn[e] > 0 ? cn[e] - 1 : 0;
+            uint32_t nb = 0;  // neighbour k's bank at bits 3k
+            for (int kk = 0; kk < dn && kk < 8; ++kk) nb |= (uint32_t)bk[e * 9 + 1 + kk] << (3 * kk);
+            int key = 0x7fffffff;
+            if (dn > 0 && dn < 8)
+              for (int t = kGapOff[dn] + sub; t < kGapOff[dn + 1]; t += 8) {
+                const int msk = kGapMasks[t];
+                int c = 0;
+                uint32_t q = nb;
+#pragma unroll
+                for (int w = 0; w < 8; ++w)
+                  if ((msk >> w) & 1) {
+                    c += (int)((occ >> (8 * w + (q & 7u))) & 1u);
+                    q >>= 3;
+                  }
+                key = min(key, (c << 8) | msk);
+              }
+            for (int o = 1; o < 8; o <<= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+            const int best = dn >= 8 ? 0xff : (dn > 0 ? (key & 0xff) : 0);
+            if (a < ng && sub == 0) gp[e] = (uint8_t)best;
+            uint32_t q = nb;
+            for (int w = 0; w < 8; ++w)
+              if ((best >> w) & 1) {
+                occ |= 1ull << (8 * w + (q & 7u));
+                q >>= 3;
+              }
+          }
+        }
+        __syncwarp();
       } else {
         for (int e = lane; e < U; e += 32) ps[e] = (uint8_t)e;
         __syncwarp();
@@ -500,10 +556,13 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
           lo = min(lo, lv);
           hi = max(hi, lv);
           const int32_t b = rp[v], d = rp[v + 1] - b;
-          for (int w = 0; w < R; ++w) {
+          const int gm = R == 8 ? gp[e] : 0;
+          for (int w = 0, kk = 0; w < R; ++w) {
             uint16_t li = GZ_PAD;
-            if (w < d) {
-              const int sl = region_slot(gz_rid, nr, (uint32_t)col[b + w]);
+            const bool use = R == 8 ? (((gm >> w) & 1) && kk < d) : w < d;
+            if (use) {
+              const int sl = R == 8 ? sl8[e * 8 + kk] : region_slot(gz_rid, nr, (uint32_t)col[b + kk]);
+              ++kk;
               li = (uint16_t)sl;
               lo = min(lo, sl);
               hi = max(hi, sl);
