@@ -371,3 +371,39 @@ def test_torch_allocator_backs_the_library():
         torch.cuda.synchronize()
     finally:
         lms.use_torch_allocator(False)
+
+
+def _fan_with_grid(n_spokes=90):
+    """A 30x20 grid plus a hub vertex joined to a ring of n_spokes rim vertices:
+    the hub's row has 2 * n_spokes pair entries (> the bucketed build's 128)."""
+    g = meshgen.grid2d(30, 20, 0.3, seed=31)
+    V0 = g.V
+    ang = np.arange(n_spokes) * (2.0 * np.pi / n_spokes)
+    rim = np.stack([3.0 + np.cos(ang), np.sin(ang)])
+    hub = V0 + n_spokes
+    x = np.concatenate([g["coords"][0], rim[0], [3.0]])
+    y = np.concatenate([g["coords"][1], rim[1], [0.0]])
+    tri = [[V0 + i, V0 + (i + 1) % n_spokes, hub] for i in range(n_spokes)]
+    elems = np.concatenate([np.asarray(g["elems"], dtype=np.int32), np.asarray(tri, dtype=np.int32)])
+    return meshgen.Mesh(dim=2, coords=[x, y], elems=elems)
+
+
+@pytest.mark.parametrize("path", ["bucketed", "sort"])
+def test_csr_paths_and_long_rows(path, monkeypatch):
+    """The CSR build's two paths agree with the oracle: the bucketed build
+    (per-source buckets, per-row sort), whose long-row fallback the hub vertex
+    triggers, and LMS_CSR=sort (global radix sort).  CSR, boundary mask and
+    colours bit-exact; a few sweeps bit-exact."""
+    if path == "sort":
+        monkeypatch.setenv("LMS_CSR", "sort")
+    m = _fan_with_grid()
+    om = oracle.prepare(m)
+    om["fixed"] = oracle.boundary(m.V, m["elems"])
+    with gpu_mesh(m) as gm:
+        rp, col = gpu_csr(gm)
+        assert np.array_equal(rp, om["row_ptr"]) and np.array_equal(col, om["col"])
+        assert np.array_equal(np_(gm.fixed()), om["fixed"])
+        assert np.array_equal(np_(gm.colour()), om["colour"])
+        gm.smooth(3)
+        want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 3)
+        assert bits_equal(gpu_coords(gm), want)
