@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-sweeps", type=int, default=2)
+    p.add_argument("--force-dist", action="store_true",
+                   help="take the multi-GPU path even at one rank (tests its plumbing under torchrun)")
     p.add_argument("--dist", default="auto", choices=["auto", "deep", "colour"],
                    help="N>1: deep halo + GZ (2D default) or per-colour exchange + S1")
     return p.parse_args()
@@ -201,7 +203,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.force_dist:
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -212,7 +214,7 @@ def run_ours(args):
     m = meshgen.make_config(args.config)
     dim = m["dim"]
     V = m.V
-    if world > 1:
+    if world > 1 or args.force_dist:
         return run_ours_dist(args, m, cfg, sweeps, world, rank, dev)
 
     # ---------------- setup phases (A2-A8), each timed with CUDA events
