@@ -242,23 +242,49 @@ __global__ void k_gc_vid(const int32_t* __restrict__ oid, int64_t V, int32_t* vi
     if (i < 0 || i >= V || atomicExch(&vid[i], (int32_t)v) != -1) atomicExch(bad, 1);
   }
 }
-// largest number of lower-orig_id free neighbours of a free vertex
+// largest number of lower-orig_id free neighbours of a free vertex; and the
+// mean reach back (position - lowest lower neighbour's position) over free
+// vertices with a lower neighbour: reach[0] = sum, reach[1] = count
 __global__ void k_gc_max_lower(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                const uint8_t* __restrict__ fixed, const int32_t* __restrict__ oid, int64_t V,
-                               int* out) {
+                               int* out, unsigned long long* reach, uint8_t* pstate) {
   int mx = 0;
+  unsigned long long rs = 0, rc = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
-    if (fixed[v]) continue;
     const int32_t me = oid[v];
+    if (fixed[v]) {
+      pstate[me] = 0;
+      continue;
+    }
     int n = 0;
+    int32_t lo = me;
+    bool cont = false;
     for (int32_t j = rp[v]; j < rp[v + 1]; ++j) {
       const int32_t u = col[j];
-      n += !fixed[u] && oid[u] < me;
+      const int32_t pu = oid[u];
+      if (!fixed[u] && pu < me) {
+        ++n;
+        lo = min(lo, pu);
+        cont |= pu == me - 1;
+      }
     }
+    pstate[me] = cont ? 2 : 1;  // free: 1 = starts a chain of consecutive ids, 2 = continues one
     mx = max(mx, n);
+    if (n) {
+      rs += (unsigned long long)(me - lo);
+      ++rc;
+    }
   }
-  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+  for (int o = 16; o; o >>= 1) {
+    mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    rs += __shfl_down_sync(0xffffffffu, rs, o);
+    rc += __shfl_down_sync(0xffffffffu, rc, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out, mx);
+    atomicAdd(reach, rs);
+    atomicAdd(reach + 1, rc);
+  }
 }
 // record of position i (stride RL ints): [0] = number of lower free neighbours
 // (-1: fixed vertex), then their positions (orig_ids), in CSR order
@@ -456,6 +482,216 @@ __global__ void __launch_bounds__(288) k_gc_seq(const int32_t* __restrict__ rec,
   }
 }
 
+// ---- batched in-order colouring (default).  One greedy step is a function of
+// the previous colour alone: with the colours of v's other lower neighbours
+// fixed (mask), c_v = mex(mask + {c_{v-1}}) = (c_{v-1} == m1) ? m2 : m1, where
+// m1 = mex(mask) and m2 = mex(mask + {m1}).  Maps of the form
+// c -> (c == k) ? x : y are closed under composition, so a warp colours 32
+// consecutive positions at once: each lane builds its map, a 5-step shuffle
+// scan composes them, and lane j reads its colour off the composed map (the
+// first lane's map is constant, so every composed map is).  A batch in which
+// some position depends on an in-batch position other than its predecessor
+// takes a 32-step shuffle chain instead.  Warp chunks of SW consecutive
+// positions, CTA units of 8 * SW, the mirror warp and the claim order are as
+// in k_gc_seq.
+__device__ __forceinline__ int gc_mex(uint64_t u0, uint64_t u1) {
+  return ~u0 ? __ffsll((long long)~u0) - 1 : (~u1 ? 64 + __ffsll((long long)~u1) - 1 : 128);
+}
+// packed map (k << 16 | x << 8 | y): c -> (c == k) ? x : y;  k = 255: constant y
+__device__ __forceinline__ int gc_apply(int f, int c) { return c == ((f >> 16) & 255) ? ((f >> 8) & 255) : (f & 255); }
+__device__ __forceinline__ int gc_compose(int a, int b) {  // a o b (b first)
+  return (b & 0xff0000) | (gc_apply(a, (b >> 8) & 255) << 8) | gc_apply(a, b & 255);
+}
+
+template <int RL>
+__global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ rec, const int* __restrict__ ulo,
+                                                  int64_t V, int SW, int MW, int* ctr, int8_t* colpos, int* maxc,
+                                                  int* err, unsigned long long* st) {
+  extern __shared__ __align__(16) unsigned char gsm[];
+  __shared__ int64_t s_base, s_mlo;
+  __shared__ int s_done;
+  constexpr int NV = RL / 4;  // int4 per record
+  constexpr int NWK = 8;      // worker warps
+  constexpr int G = 4;        // record batches in flight per warp
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t UNIT = (int64_t)NWK * SW;
+  int4* ring = reinterpret_cast<int4*>(gsm) + (size_t)warp * G * 32 * NV;  // [G][32][NV] per warp
+  int8_t* cs = reinterpret_cast<int8_t*>(gsm + (size_t)NWK * G * 32 * NV * 16);
+  int8_t* mir = cs + UNIT;
+  int mymax = -1;
+  bool dead = false;
+  unsigned long long n_rounds = 0, n_batches = 0, n_chain = 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t ub = (int64_t)atomicAdd(ctr, 1) * UNIT;
+      s_base = ub;
+      int64_t lo = ub < V ? (int64_t)ulo[ub / UNIT] : ub;
+      lo = lo >= ub ? ub : (lo & ~(int64_t)15);
+      s_mlo = ub - lo <= MW ? lo : ub;
+      s_done = 0;
+    }
+    for (int64_t q = threadIdx.x; q < UNIT + MW; q += blockDim.x) cs[q] = -1;
+    __syncthreads();
+    const int64_t ub = s_base;
+    if (ub >= V) break;
+    const int64_t mlo = s_mlo;
+    if (warp == NWK) {  // ------------------------------------------ mirror
+      const int nblk = (int)((ub - mlo) >> 4);
+      int4* m16 = reinterpret_cast<int4*>(mir);
+      const int4* g16 = reinterpret_cast<const int4*>(colpos + mlo);
+      long long idle = 0;
+      while (nblk > 0) {
+        bool all = true;
+        for (int k = lane; k < nblk; k += 32) {
+          const int4 h = m16[k];
+          if (((h.x | h.y | h.z | h.w) & 0x80808080) == 0) continue;
+          int4 g;
+          asm volatile("ld.volatile.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
+                       : "l"(g16 + k));
+          asm volatile("st.volatile.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(m16 + k)),
+                       "r"(g.x), "r"(g.y), "r"(g.z), "r"(g.w)
+                       : "memory");
+          if ((g.x | g.y | g.z | g.w) & 0x80808080) all = false;
+        }
+        if (__all_sync(FULL, all)) break;
+        if (*(volatile int*)&s_done == NWK) break;
+        if (++idle > (1ll << 30)) break;
+      }
+      continue;
+    }
+    const int64_t a = ub + (int64_t)warp * SW;
+    const int64_t b = min(a + SW, V);
+    const int nb = a < b ? (int)((b - a + 31) / 32) : 0;
+    auto issue = [&](int t) {  // records of batch t into its ring slot (empty group past the chunk)
+      const int64_t p = a + 32 * (int64_t)t + lane;
+      if (t < nb && p < b) {
+        int4* d = ring + ((size_t)(t % G) * 32 + lane) * NV;
+        const int4* src = reinterpret_cast<const int4*>(rec + p * RL);
+#pragma unroll
+        for (int w = 0; w < NV; ++w) cpa16(d + w, src + w);
+      }
+      cpa_commit();
+    };
+#pragma unroll
+    for (int t = 0; t < G; ++t) issue(t);
+    long long stall = 0;
+    for (int t = 0; t < nb && !dead;) {
+      cpa_wait<G - 1>();  // this lane's record of batch t landed
+      const int64_t base = a + 32 * (int64_t)t;
+      const int64_t i = base + lane;
+      const bool valid = i < b;
+      int4 qr[NV];
+      const int4* r4 = ring + ((size_t)(t % G) * 32 + lane) * NV;
+#pragma unroll
+      for (int w = 0; w < NV; ++w) qr[w] = valid ? r4[w] : make_int4(-1, 0, 0, 0);
+      const int n = qr[0].x;
+      bool ready = true, dep_prev = false, cplx = false;
+      uint32_t inb = 0;
+      uint64_t used0 = 0, used1 = 0;
+#pragma unroll
+      for (int w = 1; w < RL; ++w) {
+        if (w > n) break;
+        const int4 v4 = qr[w >> 2];
+        const int64_t pp = (w & 3) == 0 ? v4.x : (w & 3) == 1 ? v4.y : (w & 3) == 2 ? v4.z : v4.w;
+        if (pp >= base) {  // in this batch (pp < i)
+          const int lj = (int)(pp - base);
+          inb |= 1u << lj;
+          if (lj == lane - 1) dep_prev = true;
+          else cplx = true;
+        } else {
+          const int c = pp >= ub ? ld_vol_s8(cs + (pp - ub))
+                                 : (pp >= mlo ? ld_vol_s8(mir + (pp - mlo)) : ld_vol_s8(colpos + pp));
+          if (c < 0) ready = false;
+          else if (c < 64) used0 |= 1ull << c;
+          else used1 |= 1ull << (c - 64);
+        }
+      }
+      ++n_rounds;
+      if (!__all_sync(FULL, ready)) {  // an input from an earlier batch is not coloured yet
+        if (++stall > (1ll << 28)) {  // cannot happen (every wait is on a lower position)
+          raise_err(err, LMS_E_CUDA);
+          dead = true;
+        }
+        continue;
+      }
+      stall = 0;
+      int colr;
+      if (!__any_sync(FULL, cplx)) {
+        int f;
+        if (n < 0) {
+          f = 0xff0000;  // fixed / past the chunk: a constant (never an input)
+        } else {
+          const int m1 = gc_mex(used0, used1);
+          const int m2 = m1 < 64 ? gc_mex(used0 | (1ull << m1), used1) : gc_mex(used0, used1 | (1ull << (m1 - 64)));
+          f = dep_prev ? ((min(m1, 254) << 16) | (min(m2, 255) << 8) | min(m1, 255))
+                       : (0xff0000 | (min(m1, 255) << 8) | min(m1, 255));
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int pf = __shfl_up_sync(FULL, f, o);
+          if (lane >= o) f = gc_compose(f, pf);
+        }
+        colr = f & 255;
+      } else {  // general in-batch dependencies: a 32-step chain
+        ++n_chain;
+        colr = -1;
+        for (int tt = 0; tt < 32; ++tt) {
+          if (lane == tt && n >= 0) colr = gc_mex(used0, used1);
+          const int ct = __shfl_sync(FULL, colr, tt);
+          if (((inb >> tt) & 1u) && ct >= 0) {
+            if (ct < 64) used0 |= 1ull << ct;
+            else used1 |= 1ull << (ct - 64);
+          }
+        }
+      }
+      if (valid && n >= 0) {
+        int c = colr;
+        if (c > 126) { raise_err(err, LMS_E_ARG); c = 126; }
+        *(volatile int8_t*)(cs + (i - ub)) = (int8_t)c;
+        *(volatile int8_t*)(colpos + i) = (int8_t)c;
+        mymax = c > mymax ? c : mymax;
+      }
+      ++n_batches;
+      issue(t + G);
+      ++t;
+    }
+    cpa_wait<0>();
+    __syncwarp();
+    if (lane == 0) atomicAdd(&s_done, 1);
+  }
+  for (int o = 16; o; o >>= 1) mymax = max(mymax, __shfl_down_sync(0xffffffffu, mymax, o));
+  if ((threadIdx.x & 31) == 0 && mymax >= 0) atomicMax(maxc, mymax);
+  if (st && lane == 0) {
+    atomicAdd(st + 0, n_rounds);
+    atomicAdd(st + 1, n_batches);
+    atomicAdd(st + 2, n_chain);
+  }
+}
+
+// Chunks of SW positions that hold free positions of one chain of consecutive
+// ids and then the start of another: in such a chunk the second chain waits
+// for the end of the first (chunks run in order), which serialises whole
+// chains across chunks.  Splitting one chain across chunks is harmless.
+__global__ void k_gc_bad_chunks(const uint8_t* __restrict__ pstate, int64_t V, int64_t SW,
+                                unsigned long long* bad) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k * SW < V; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = k * SW, b = min(a + SW, V);
+    bool seen = false;
+    for (int64_t p = a; p < b; ++p) {
+      const uint8_t st = pstate[p];
+      if (st == 1 && seen) {
+        atomicAdd(bad, 1ull);
+        break;
+      }
+      seen |= st != 0;
+    }
+  }
+}
+
 // colour[v] = colour of position orig_id[v] (fixed vertices: -1)
 __global__ void k_gc_scatter(const int32_t* __restrict__ oid, const uint8_t* __restrict__ fixed,
                              const int8_t* __restrict__ colpos, int64_t V, int8_t* colour) {
@@ -474,17 +710,62 @@ static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
   LMS_TRY_CUDA(cudaMemsetAsync(flags.p, 0, 2 * sizeof(int), s));
   k_gc_vid<<<Gv, 256, 0, s>>>(m->orig_id.p, V, vid.p, flags.p);
   LMS_CHECK_LAUNCH();
-  k_gc_max_lower<<<Gv, 256, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, m->orig_id.p, V, flags.p + 1);
+  DBuf<unsigned long long> reach(2, s);
+  DBuf<uint8_t> pstate(V, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(reach.p, 0, 2 * sizeof(unsigned long long), s));
+  k_gc_max_lower<<<Gv, 256, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, m->orig_id.p, V, flags.p + 1, reach.p,
+                                    pstate.p);
   LMS_CHECK_LAUNCH();
   int h[2] = {0, 0};
+  unsigned long long hr[2] = {0, 0};
   LMS_TRY_CUDA(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaMemcpyAsync(hr, reach.p, sizeof(hr), cudaMemcpyDeviceToHost, s));
   LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  const int64_t mean_reach = hr[1] ? (int64_t)(hr[0] / hr[1]) : 1024;
   if (h[0] || h[1] > 31) return false;
   const int RL = h[1] <= 3 ? 4 : h[1] <= 7 ? 8 : h[1] <= 15 ? 16 : 32;
   const int threads = 288;  // 8 worker warps + the mirror warp
-  // chunk: longer chunks mean fewer cross-thread hops but fewer units in flight
+  // batched (default; LMS_GC=lanes: thread-per-chunk k_gc_seq).  Batched: warp
+  // chunks of SW consecutive positions, units of 8 * SW.  Lanes: thread
+  // chunks of S, units of 256 * S (longer chunks: fewer cross-thread hops but
+  // fewer units in flight)
+  // Defaults (measured on C2-C5): batched for 2D, lanes for 3D.  A batched
+  // warp's chunk is about the mean reach back (on a row-major grid, a row): a
+  // longer chunk would hold a vertex and its row-below neighbours, serialising
+  // rows inside one warp instead of pipelining them across warps; it is halved
+  // while the mesh would not give half the SMs a unit.
+  // Chunks must not put the tail of one chain of consecutive ids and the head
+  // of the next in one chunk (k_gc_bad_chunks): that serialises the chains.
+  // 2D: the batched kernel with SW = the power of two nearest the mean reach
+  // (a grid row) if its chunks are aligned (<= 1% bad); else the per-thread
+  // kernel if its chunks of S are; else the queue kernel (false here).
+  const char* gce = getenv("LMS_GC");
   const int S = env_int_c("LMS_GC_CHUNK", V >= (int64_t)8 << 20 ? 256 : 128, 8, 4096);
-  const int64_t UNIT = (int64_t)256 * S;
+  int nsm0 = 0;
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, m->device));
+  int64_t sw = 1024;
+  while (sw * 2 <= std::min<int64_t>(mean_reach + mean_reach / 8, 16384)) sw *= 2;
+  while (sw > 1024 && (V + 8 * sw - 1) / (8 * sw) < nsm0 / 2) sw /= 2;
+  const int SW = env_int_c("LMS_GC_WCHUNK", (int)sw, 32, 1 << 20) & ~31;
+  auto aligned = [&](int64_t chunk) {
+    DBuf<unsigned long long> bad(1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
+    const int64_t nk = (V + chunk - 1) / chunk;
+    k_gc_bad_chunks<<<(unsigned)std::min<int64_t>((nk + 255) / 256, 8192), 256, 0, s>>>(pstate.p, V, chunk, bad.p);
+    LMS_CHECK_LAUNCH();
+    unsigned long long hb = 0;
+    LMS_TRY_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    return hb * 100 <= (unsigned long long)nk;
+  };
+  bool batched;
+  if (gce) {
+    batched = strcmp(gce, "lanes") != 0;  // forced (tests, measurements)
+  } else {
+    batched = m->dim == 2 && aligned(SW);
+    if (!batched && !aligned(S)) return false;
+  }
+  const int64_t UNIT = batched ? (int64_t)8 * SW : (int64_t)256 * S;
   const int64_t units = (V + UNIT - 1) / UNIT;
   DBuf<int32_t> rec((size_t)V * RL, s);
   DBuf<int8_t> colpos(V + 16, s);
@@ -508,18 +789,25 @@ static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
     if (MW > cap) MW = cap;
     MW = (MW + 15) & ~15;
   }
-  constexpr int G = 8;  // records in flight per worker lane
-  const size_t smem = (size_t)256 * G * (RL / 4) * 16 + (size_t)UNIT + (size_t)MW;
-  void (*kern)(const int32_t*, const int32_t*, const int*, int64_t, int, int, int*, int8_t*, int8_t*, int*, int*,
-               unsigned long long*) =
+  constexpr int G = 8;  // records in flight per worker lane (lanes kernel); the batched one keeps 4 batches per warp
+  const size_t smem = (batched ? (size_t)8 * 4 * 32 * (RL / 4) * 16 : (size_t)256 * G * (RL / 4) * 16) +
+                      (size_t)UNIT + (size_t)MW;
+  void (*kern_l)(const int32_t*, const int32_t*, const int*, int64_t, int, int, int*, int8_t*, int8_t*, int*, int*,
+                 unsigned long long*) =
       RL == 4 ? k_gc_seq<4, G> : RL == 8 ? k_gc_seq<8, G> : RL == 16 ? k_gc_seq<16, G> : k_gc_seq<32, G>;
+  void (*kern_b)(const int32_t*, const int*, int64_t, int, int, int*, int8_t*, int*, int*, unsigned long long*) =
+      RL == 4 ? k_gc_batch<4> : RL == 8 ? k_gc_batch<8> : RL == 16 ? k_gc_batch<16> : k_gc_batch<32>;
+  const void* kern = batched ? (const void*)kern_b : (const void*)kern_l;
   if (smem > 227 * 1024) return false;
   if (smem > 48 * 1024) LMS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int nsm = 0, occ = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
   LMS_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
   if (occ < 1) return false;
-  // co-resident CTAs (a thread may wait on any earlier unit's thread)
+  // co-resident CTAs (a thread may wait on any earlier unit's thread).  The
+  // batched kernel polls in lock step: more CTAs per SM only slow every warp's
+  // round (LMS_GC_CTAS_PER_SM, default 1 for it)
+  if (batched) occ = std::min(occ, env_int_c("LMS_GC_CTAS_PER_SM", 1, 1, 64));
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * occ, units));
   const int32_t* a_rec = rec.p;
   const int32_t* a_vid = vid.p;
@@ -539,7 +827,10 @@ static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
     LMS_TRY_CUDA(cudaMemsetAsync(gst, 0, 8 * sizeof(unsigned long long), s));
     a_st = gst;
   }
-  void* args[] = {&a_rec, &a_vid, &a_ulo, &a_V, &a_S, &a_mw, &a_ctr, &a_cp, &a_col, &a_max, &a_err, &a_st};
+  int a_sw = SW;
+  void* args_l[] = {&a_rec, &a_vid, &a_ulo, &a_V, &a_S, &a_mw, &a_ctr, &a_cp, &a_col, &a_max, &a_err, &a_st};
+  void* args_b[] = {&a_rec, &a_ulo, &a_V, &a_sw, &a_mw, &a_ctr, &a_cp, &a_max, &a_err, &a_st};
+  void** args = batched ? args_b : args_l;
   const bool verbose = getenv("LMS_COLOUR_VERBOSE") != nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (verbose) {
@@ -554,8 +845,8 @@ static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
     LMS_TRY_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
     LMS_TRY_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    fprintf(stderr, "[colour] in-order: RL=%d S=%d mirror=%d blocks=%d units=%lld kernel %.3f ms\n", RL, S, MW,
-            blocks, (long long)units, ms);
+    fprintf(stderr, "[colour] in-order %s: RL=%d S=%d SW=%d mirror=%d blocks=%d units=%lld kernel %.3f ms\n",
+            batched ? "batched" : "lanes", RL, S, SW, MW, blocks, (long long)units, ms);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
@@ -565,9 +856,13 @@ static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
     unsigned long long h2[8];
     LMS_TRY_CUDA(cudaMemcpyAsync(h2, a_st, sizeof(h2), cudaMemcpyDeviceToHost, s));
     LMS_TRY_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[colour stats] warp rounds=%llu lane progress=%llu (%.2f per round) mirror sweeps=%llu "
-            "units=%llu mean unit %.1f kcycles\n", h2[0], h2[1], h2[0] ? (double)h2[1] / h2[0] : 0.0, h2[2], h2[4],
-            h2[4] ? h2[3] / 1e3 / h2[4] : 0.0);
+    if (batched)
+      fprintf(stderr, "[colour stats] warp rounds=%llu batches=%llu (%.2f per round) chain batches=%llu\n", h2[0],
+              h2[1], h2[0] ? (double)h2[1] / h2[0] : 0.0, h2[2]);
+    else
+      fprintf(stderr, "[colour stats] warp rounds=%llu lane progress=%llu (%.2f per round) mirror sweeps=%llu "
+              "units=%llu mean unit %.1f kcycles\n", h2[0], h2[1], h2[0] ? (double)h2[1] / h2[0] : 0.0, h2[2],
+              h2[4], h2[4] ? h2[3] / 1e3 / h2[4] : 0.0);
   }
   return true;
 }

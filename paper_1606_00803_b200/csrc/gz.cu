@@ -1952,7 +1952,7 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   // records; 4 batches measured 1.7x slower).  RR is a power of two.
   L->BS_log2 = env_int("LMS_GZ_BS_LOG2", upl == 2 ? 2 : 3, 0, 4);  // records per batch (about 3-6 KB per batch)
   L->BS = 1 << L->BS_log2;
-  L->RR = env_int("LMS_GZ_RR", 8, 8, 64);
+  L->RR = env_int("LMS_GZ_RR", 8, 4, 64);
   while (L->RR & (L->RR - 1)) ++L->RR;
   while (L->RR * L->BS < nw + L->BS) L->RR *= 2;
   L->RR_log2 = 0;

@@ -407,3 +407,21 @@ def test_csr_paths_and_long_rows(path, monkeypatch):
         gm.smooth(3)
         want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 3)
         assert bits_equal(gpu_coords(gm), want)
+
+
+@pytest.mark.parametrize("mode,wchunk", [("batch", "512"), ("batch", "1024"), ("lanes", "0"), ("auto", "0")])
+def test_colouring_kernels_on_unaligned_grid(mode, wchunk, monkeypatch):
+    """Every colouring kernel on a grid whose rows (500 ids) do not line up
+    with the chunks: the batched kernel (forced, chunks of 512 / 1024: rows
+    straddle chunks, many units), the per-thread kernel (forced), and the
+    automatic choice (the alignment check falls back to the queue kernel).
+    Colours bit-exact against the oracle's sequential greedy (reading Z2)."""
+    if mode != "auto":
+        monkeypatch.setenv("LMS_GC", mode)
+    if wchunk != "0":
+        monkeypatch.setenv("LMS_GC_WCHUNK", wchunk)
+    m = meshgen.grid2d(500, 90, 0.3, seed=41)
+    om = oracle.prepare(m)
+    with gpu_mesh(m) as gm:
+        assert np.array_equal(np_(gm.colour()), om["colour"])
+        assert gm.info()["C"] == om["C"]
