@@ -119,6 +119,40 @@ __global__ void k_row_unique(const int32_t* __restrict__ off, int32_t* buf, int6
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     int32_t* a = buf + off[v];
     const int32_t L = off[v + 1] - off[v];
+    if (L <= 16) {  // registers: a 16-wide bitonic network, then de-duplicate
+      int32_t r[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) r[i] = i < L ? a[i] : INT32_MAX;
+#pragma unroll
+      for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int l = i ^ j;
+            if (l > i) {
+              const bool up = (i & k) == 0;
+              const int32_t x = r[i], y = r[l];
+              if ((x > y) == up) {
+                r[i] = y;
+                r[l] = x;
+              }
+            }
+          }
+      int u = 0;
+      bool single = false;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i >= L) break;
+        const bool first = i == 0 || r[i] != r[i - 1];
+        const bool last = i == L - 1 || r[i] != r[i + 1];
+        single |= first && last;
+        if (first) a[u++] = r[i];
+      }
+      ndeg[v] = u;
+      if (fixed_or_null && single) fixed_or_null[v] = 1;
+      continue;
+    }
     for (int i = 1; i < L; ++i) {  // insertion sort (rows are short)
       const int32_t x = a[i];
       int j = i;
