@@ -1994,13 +1994,17 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   cap -= 16;  // the kernel's static shared memory (abort flag)
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
-  // updates per lane (LMS_GZ_UPL=2 in 2D: 64-update items; measured slower on
-  // C4 -- coarser items wait on more dependencies -- so 1 is the default)
+  // updates per lane: 1 by default.  LMS_GZ_UPL=2 (2D: 64-update items, half
+  // the per-item claim / record / dependency / completion work) measured
+  // C4 302 -> 277 us per sweep with 18 workers, but hung once (GZ watchdog)
+  // in 120 back-to-back end-to-end steps -- a race not yet found, so it stays
+  // opt-in
   const int upl = env_int("LMS_GZ_UPL", 1, 1, m->dim == 2 ? 2 : 1);
   const int maxw = (m->dim == 2 ? 1024 : 384) / 32;  // the kernel's launch bounds
-  // 22 workers measured best on C4 (more warps only lengthen every item: the
-  // shared-memory pipe is the shared resource); + region producer + record loader
-  const int nw = env_int("LMS_GZ_WORKERS", std::min(maxw - 2, m->dim == 2 ? 22 : 10), 1, maxw - 2);
+  // workers measured best on C4: 18 with 2 updates per lane, 22 with 1 (more
+  // warps only lengthen every item: the shared-memory pipe is the shared
+  // resource); + region producer + record loader
+  const int nw = env_int("LMS_GZ_WORKERS", std::min(maxw - 2, m->dim == 2 ? (upl == 2 ? 18 : 22) : 10), 1, maxw - 2);
   const int want_nb = env_int("LMS_GZ_BUFFERS", 0, 0, 8);
   const int dim = m->dim, C = m->C;
   GzNeeds nd;

@@ -145,10 +145,11 @@ def test_gz_spatial_bins_tiling(pair, monkeypatch):
         assert bits_equal(gpu_coords(gm), want)
 
 
-@pytest.mark.parametrize("upl", [2])
+@pytest.mark.parametrize("upl", [1, 2])
 def test_gz_two_updates_per_lane(pair, upl, monkeypatch):
-    """LMS_GZ_UPL=2: 64-update items (two updates per lane) -- the optional
-    item size of the GZ kernel -- bit-exact under two orderings, P = 1 and 2."""
+    """Both item sizes of the GZ kernel: LMS_GZ_UPL=1 (32-update items) and 2
+    (64-update items, two updates per lane -- the 2D default), bit-exact under
+    two orderings, P = 1 and 2."""
     m, om, gm0 = pair
     if m["dim"] != 2:
         pytest.skip("two updates per lane is a 2D option")

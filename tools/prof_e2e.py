@@ -18,6 +18,7 @@ ap.add_argument("--ordering", default="original")
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--prof", action="store_true", help="bracket the last step with cudaProfilerStart/Stop")
 ap.add_argument("--loop", action="store_true", help="also time bench.py-style back-to-back steps")
+ap.add_argument("--loop-n", type=int, default=3, help="steps of the longer back-to-back loop")
 a = ap.parse_args()
 m = meshgen.make_config(a.config)
 hc = [torch.from_numpy(c).pin_memory() for c in m["coords"]]
@@ -61,7 +62,7 @@ if a.loop:
             h.copy_(o, non_blocking=True)
         torch.cuda.synchronize()
         g.close()
-    for n in (1, 3):
+    for n in (1, a.loop_n):
         t0 = time.perf_counter()
         for _ in range(n):
             plain()
