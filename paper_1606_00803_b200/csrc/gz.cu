@@ -1122,9 +1122,15 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
   uint64_t* rfull = empty + NB;                         // [RR] record batch landed
   uint64_t* rempty = rfull + RR;                        // [RR] record batch consumed (BS arrivals)
   uint64_t* sbar = rempty + RR;                         // [1] producer staging copy landed
-  int* ctl = reinterpret_cast<int*>(sbar + 1);          // [0] cursor, [1..NB] buf_tile, [NB+1..2NB] ndone
+  int* ctl = reinterpret_cast<int*>(sbar + 1);  // [0] cursor, [1..NB] buf_tile, [NB+1..2NB] ndone, then rbat[RR]
   volatile int* buf_tile = ctl + 1;
   int* ndone = ctl + 1 + NB;
+  // rbat[slot]: the record batch the loader last issued into the slot.  A
+  // worker waits for its batch here before the parity wait: TMA copies may
+  // complete out of order, so claims can run a whole ring ahead of a late
+  // batch, and a parity wait on fill m while fill m - 1 of the slot is still
+  // in flight would pass at once (the previous same-parity phase is complete)
+  volatile int* rbat = ctl + 1 + 2 * NB;
   long long* t_rec = reinterpret_cast<long long*>(sm + L.off_tab);
   int* t_rec16 = reinterpret_cast<int*>(t_rec + L.tiles_cap);
   int* t_R = t_rec16 + L.tiles_cap;
@@ -1150,6 +1156,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
     for (int r = 0; r < RR; ++r) {
       mbar_init(rfull + r, 1);
       mbar_init(rempty + r, L.BS);
+      rbat[r] = -1;
     }
     mbar_init(sbar, 1);
     ctl[0] = 0;
@@ -1308,6 +1315,7 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
           }
           kc = kend;
         }
+        rbat[slot] = g;  // batch g issued into the slot (its fill's completion follows on rfull)
       }
       if (STATS) {
         atomicAdd(stats + 6, (unsigned long long)lw);
@@ -1357,7 +1365,8 @@ __global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int
         rring + ((size_t)slot * L.BS + (kc & (L.BS - 1))) * L.rec_bytes;
     int alive = 1;
     if (lane == 0) {
-      alive = mbar_wait_g(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u, guard);
+      while (alive && rbat[slot] != bat) alive = guard.ok_spin();
+      alive = alive && mbar_wait_g(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u, guard);
       if (alive && !tile_ready) {  // the region of the item's tile
         while (alive && buf_tile[tb & 0xffff] != i) alive = guard.ok();
         alive = alive && mbar_wait_g(full + (tb & 0xffff), (uint32_t)(tb >> 16), guard);
@@ -1970,7 +1979,7 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   L->tiles_cap = tiles_cap;
   for (int nb = want_nb > 0 ? want_nb : 8; nb >= 1; --nb) {
     L->NB = nb;
-    const int ctl = (2 * nb + 2 * L->RR + 1) * 8 + (1 + 2 * nb) * 4;
+    const int ctl = (2 * nb + 2 * L->RR + 1) * 8 + (1 + 2 * nb + L->RR) * 4;
     L->off_rcp = r16i(ctl);
     L->off_tab = L->off_rcp + r16i(8 * (GZ_RCP_MAX + 1));
     const int tab_bytes = r16i((int64_t)tiles_cap * (8 + 4 + 4 + 4 + 4) + 4 * ((int64_t)tiles_cap + 1));
@@ -1994,12 +2003,11 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   cap -= 16;  // the kernel's static shared memory (abort flag)
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
-  // updates per lane: 1 by default.  LMS_GZ_UPL=2 (2D: 64-update items, half
-  // the per-item claim / record / dependency / completion work) measured
-  // C4 302 -> 277 us per sweep with 18 workers, but hung once (GZ watchdog)
-  // in 120 back-to-back end-to-end steps -- a race not yet found, so it stays
-  // opt-in
-  const int upl = env_int("LMS_GZ_UPL", 1, 1, m->dim == 2 ? 2 : 1);
+  // updates per lane: 2D default 2 (64-update items halve the per-item claim /
+  // record / dependency / completion work: C4 ~300 -> ~280 us per sweep), 3D 1.
+  // (Its rare failures in back-to-back runs were the record ring's parity
+  // ambiguity under out-of-order TMA completion, fixed by rbat.)
+  const int upl = env_int("LMS_GZ_UPL", m->dim == 2 ? 2 : 1, 1, m->dim == 2 ? 2 : 1);
   const int maxw = (m->dim == 2 ? 1024 : 384) / 32;  // the kernel's launch bounds
   // workers measured best on C4: 18 with 2 updates per lane, 22 with 1 (more
   // warps only lengthen every item: the shared-memory pipe is the shared

@@ -1,0 +1,2 @@
+#!/bin/bash
+for k in 1 2 3 4 5 6; do LMS_GZ_UPL=2 LMS_GZ_WORKERS=18 timeout 300 python tools/prof_e2e.py --steps 0 --loop --loop-n 40 2>&1 | grep -E "loop_steps\": 40|LMSError|Error:" | head -2; done
