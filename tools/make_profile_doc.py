@@ -41,7 +41,7 @@ summ = {"kernels": [{
     "issue_active_pct": f("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
     "l2_hit_pct": f("lts__t_sector_hit_rate.pct"),
     "source": "profiles/round1_final_gz.md: ncu --set full --clock-control none, one k_sweep_gz launch "
-              "(1 sweep; kd tiles T=4096, 22 workers, 768 threads), tools/prof_one.py --schedule gz"}]}
+              f"(1 sweep; kd tiles T=4096, 64-update items, {int(f('launch__block_size'))} threads), tools/prof_one.py --schedule gz"}]}
 json.dump(summ, open("profiles/ncu_summary.json", "w"), indent=1)
 open("profiles/round1_final_bench.json", "w").write(json.dumps(b) + "\n")
 
@@ -61,9 +61,10 @@ doc = f"""# Round 1 (final) — k_sweep_gz on C4, and the e2e path
 
 Written by `tools/make_profile_doc.py` from B200 `gpurun` captures at the end of
 round 1. The kernel: GZ ghost-zone sweep, kd tiles of T=4096 owned vertices,
-22 worker warps + region producer + record loader (768 threads), predicated
-shared-memory gathers over gap-placed rows, Markstein division from an
-RN(1/d) table, register-resident loader state (DESIGN.md 6.1).
+two updates per lane (64-update items), {int(f('launch__block_size')) // 32 - 2} worker warps + region producer +
+record loader ({int(f('launch__block_size'))} threads), predicated shared-memory gathers over
+gap-placed rows, Markstein division from an RN(1/d) table, register-resident
+loader state (DESIGN.md 6.1).
 
 ## Bench (`python bench.py`, C4 / original / 50 sweeps)
 
