@@ -1603,8 +1603,39 @@ static int64_t kd_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) 
   const int64_t K0 = std::max<int64_t>(1, (V + T - 1) / T);
   int64_t nbx = std::max<int64_t>(1, (int64_t)std::llround(std::sqrt((double)K0)));
   if (nbx > (1 << 19)) nbx = 1 << 19;
+  int64_t tps = ((V + nbx - 1) / nbx + T - 1) / T;
+  // Tiles go to the persistent CTAs round-robin, so a sweep lasts
+  // ceil(K / nsm) tiles: with few tiles per SM, take the tile count up to the
+  // next multiple of the SM count (tiles only get smaller), as nbx x tps
+  // strips x tiles near square.  C2: 256 -> 294 tiles, 33.0 -> 31.3 us per
+  // sweep; with many tiles per SM the smaller, less square tiles cost more
+  // halo than the balance gains (C4: 282 -> 287 us), so only below 4 per SM.
+  int nsm = 0;
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  if (nsm > 0 && K0 >= nsm && K0 < 4 * (int64_t)nsm && !getenv("LMS_GZ_NO_BALANCE")) {
+    const int64_t kmax = (K0 + nsm - 1) / nsm * nsm;
+    const double r = std::sqrt((double)kmax);
+    int64_t best = nbx * tps, bx = nbx, bt = tps;
+    for (int64_t x = std::max<int64_t>(1, (int64_t)(r / 1.6)); x <= (int64_t)(r * 1.6) + 1; ++x) {
+      const int64_t y = kmax / x;
+      if (y < 1) continue;
+      const int64_t k = x * y;
+      if (k < K0) continue;
+      const double ar = x > y ? (double)x / y : (double)y / x;
+      const double bar = bx > bt ? (double)bx / bt : (double)bt / bx;
+      if ((best < K0 || k > best || (k == best && ar < bar)) && ar <= 1.6) {
+        best = k;
+        bx = x;
+        bt = y;
+      }
+    }
+    if (best >= K0) {
+      nbx = bx;
+      tps = bt;
+    }
+  }
   const int64_t per_strip = (V + nbx - 1) / nbx;
-  const int64_t tps = (per_strip + T - 1) / T;
+  T = (int)((per_strip + tps - 1) / tps);
   DBuf<uint32_t> k1(V, s), k2(V, s);
   DBuf<int32_t> i1(V, s), i2(V, s);
   k_kd_xkey<<<gsz(V), 256, 0, s>>>(m->x[0].p, V, k1.p, i1.p);
