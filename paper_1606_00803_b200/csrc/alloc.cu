@@ -5,8 +5,8 @@
 // whose memory is retained is cheap on average, but each call is a driver API
 // call, and measured e2e steps showed occasional stalls of tens to hundreds of
 // ms inside them.  This keeps freed blocks in a host-side cache keyed by
-// (stream, size) and hands them back to the next allocation on the same
-// stream: the blocks' previous uses precede any new use in that stream's
+// (device, stream, size) and hands them back to the next allocation on the
+// same stream: the blocks' previous uses precede any new use in that stream's
 // order, exactly the guarantee cudaFreeAsync + cudaMallocAsync gave.  A block
 // is reused for a request of at least 3/4 of its size.  Cached bytes are
 // capped (LMS_CACHE_GB, default 16 GB; 0 disables the cache); beyond the cap,
@@ -14,6 +14,7 @@
 // their stream.
 #include <cstdlib>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <unordered_map>
 
@@ -35,7 +36,9 @@ UserAlloc& user() {
 struct Cache {
   std::mutex mu;
   std::unordered_map<void*, size_t> live;                         // block -> bytes
-  std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free_;  // (stream, bytes) -> blocks
+  // (device, stream, bytes) -> blocks: the legacy default stream has the same
+  // handle on every device, so the device is part of the key
+  std::map<std::tuple<int, cudaStream_t, size_t>, std::vector<void*>> free_;
   size_t cached = 0;
   size_t cap = 0;
   bool init = false;
@@ -43,6 +46,15 @@ struct Cache {
 Cache& cache() {
   static Cache* c = new Cache();  // never destroyed: frees may run at exit
   return *c;
+}
+// cudaFreeAsync with the block's own device current (its stream handle may
+// be the legacy default stream, which names a different stream per device)
+void free_on(int dev, cudaStream_t s, void* p) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  cudaFreeAsync(p, s);
+  if (cur != dev) cudaSetDevice(cur);
 }
 size_t round_bytes(size_t b) {
   if (b <= 4096) return 4096;
@@ -54,6 +66,8 @@ size_t round_bytes(size_t b) {
 void* ws_alloc(size_t bytes, cudaStream_t s) {
   Cache& c = cache();
   const size_t rb = round_bytes(bytes);
+  int dev = 0;
+  LMS_TRY_CUDA(cudaGetDevice(&dev));
   if (user().alloc) {
     void* p = user().alloc(rb, (lms_stream_t)s, user().ctx);
     if (!p) fail(LMS_E_NOMEM, "lms_set_allocator: the caller's allocator returned NULL");
@@ -70,13 +84,14 @@ void* ws_alloc(size_t bytes, cudaStream_t s) {
       c.init = true;
     }
     if (c.cap) {
-      // smallest cached block of this stream with rb <= size <= 4/3 rb
-      auto it = c.free_.lower_bound({s, rb});
-      if (it != c.free_.end() && it->first.first == s && it->first.second <= rb + rb / 3 && !it->second.empty()) {
+      // smallest cached block of this device and stream with rb <= size <= 4/3 rb
+      auto it = c.free_.lower_bound(std::make_tuple(dev, s, rb));
+      if (it != c.free_.end() && std::get<0>(it->first) == dev && std::get<1>(it->first) == s &&
+          std::get<2>(it->first) <= rb + rb / 3 && !it->second.empty()) {
         void* p = it->second.back();
         it->second.pop_back();
-        c.cached -= it->first.second;
-        c.live[p] = it->first.second;
+        c.cached -= std::get<2>(it->first);
+        c.live[p] = std::get<2>(it->first);
         if (it->second.empty()) c.free_.erase(it);
         return p;
       }
@@ -112,14 +127,16 @@ void ws_free(void* p, cudaStream_t s) {
     cudaFreeAsync(p, s);
     return;
   }
-  c.free_[{s, b}].push_back(p);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  c.free_[std::make_tuple(dev, s, b)].push_back(p);
   c.cached += b;
-  while (c.cached > c.cap && !c.free_.empty()) {  // over the cap: largest blocks back to the pool
+  while (c.cached > c.cap && !c.free_.empty()) {  // over the cap: blocks back to the pool
     auto last = std::prev(c.free_.end());
     void* q = last->second.back();
     last->second.pop_back();
-    c.cached -= last->first.second;
-    cudaFreeAsync(q, last->first.first);
+    c.cached -= std::get<2>(last->first);
+    free_on(std::get<0>(last->first), std::get<1>(last->first), q);
     if (last->second.empty()) c.free_.erase(last);
   }
 }
@@ -142,7 +159,7 @@ extern "C" void lms_cache_release(void) {
   lms::Cache& c = lms::cache();
   std::lock_guard<std::mutex> g(c.mu);
   for (auto& kv : c.free_)
-    for (void* q : kv.second) cudaFreeAsync(q, kv.first.first);
+    for (void* q : kv.second) lms::free_on(std::get<0>(kv.first), std::get<1>(kv.first), q);
   c.free_.clear();
   c.cached = 0;
 }
