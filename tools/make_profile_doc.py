@@ -74,6 +74,7 @@ loader state (DESIGN.md 6.1).
 - e2e: **{e2e['value'] / 1e9:.2f} G vertex-updates/s**, {e2e['ms_per_step']:.1f} ms per step. This covers
   host buffers → H2D → build_csr + colouring → order + permute → schedule → 50 sweeps → D2H.
   Phases (ms): {json.dumps({k: round(v, 1) for k, v in e2e['phases_ms'].items()})}
+- cpu_baseline: {(f"{b['cpu_baseline']['value'] / 1e9:.3f} G vertex-updates/s on {b['cpu_baseline']['cores']} host cores ({b['cpu_baseline']['kind']}: {b['cpu_baseline']['sample']})") if b.get('cpu_baseline') else 'not run'}
 - clocks {json.dumps(b['clocks'])}
 
 Full JSON line: `profiles/round1_final_bench.json`.
