@@ -579,19 +579,25 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
 #pragma unroll
     for (int t = 0; t < G; ++t) issue(t);
     long long stall = 0;
-    for (int t = 0; t < nb && !dead;) {
-      cpa_wait<G - 1>();  // this lane's record of batch t landed
-      const int64_t base = a + 32 * (int64_t)t;
-      const int64_t i = base + lane;
-      const bool valid = i < b;
-      int4 qr[NV];
-      const int4* r4 = ring + ((size_t)(t % G) * 32 + lane) * NV;
-#pragma unroll
-      for (int w = 0; w < NV; ++w) qr[w] = valid ? r4[w] : make_int4(-1, 0, 0, 0);
-      const int n = qr[0].x;
-      bool ready = true, dep_prev = false, cplx = false;
-      uint32_t inb = 0;
-      uint64_t used0 = 0, used1 = 0;
+    // lane state for the current batch: its record (registers), the colours
+    // seen so far (an OR: re-reads are harmless) and the first input still
+    // missing (wpp; -1 = none) -- a waiting round polls only that one
+    bool have = false;
+    int64_t base = 0, i = 0, wpp = -1;
+    bool valid = false, dep_prev = false, cplx = false;
+    uint32_t inb = 0;
+    uint64_t used0 = 0, used1 = 0;
+    int n = -1;
+    int4 qr[NV];
+    auto poll = [&](int64_t pp) {
+      return pp >= ub ? ld_vol_s8(cs + (pp - ub))
+                      : (pp >= mlo ? ld_vol_s8(mir + (pp - mlo)) : ld_vol_s8(colpos + pp));
+    };
+    auto scan = [&]() {  // all inputs of position i; wpp = the first not yet coloured
+      wpp = -1;
+      dep_prev = false;
+      cplx = false;
+      inb = 0;
 #pragma unroll
       for (int w = 1; w < RL; ++w) {
         if (w > n) break;
@@ -603,13 +609,34 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
           if (lj == lane - 1) dep_prev = true;
           else cplx = true;
         } else {
-          const int c = pp >= ub ? ld_vol_s8(cs + (pp - ub))
-                                 : (pp >= mlo ? ld_vol_s8(mir + (pp - mlo)) : ld_vol_s8(colpos + pp));
-          if (c < 0) ready = false;
-          else if (c < 64) used0 |= 1ull << c;
-          else used1 |= 1ull << (c - 64);
+          const int c = poll(pp);
+          if (c < 0) {
+            if (wpp < 0) wpp = pp;
+          } else if (c < 64) {
+            used0 |= 1ull << c;
+          } else {
+            used1 |= 1ull << (c - 64);
+          }
         }
       }
+    };
+    for (int t = 0; t < nb && !dead;) {
+      if (!have) {
+        cpa_wait<G - 1>();  // this lane's record of batch t landed
+        base = a + 32 * (int64_t)t;
+        i = base + lane;
+        valid = i < b;
+        const int4* r4 = ring + ((size_t)(t % G) * 32 + lane) * NV;
+#pragma unroll
+        for (int w = 0; w < NV; ++w) qr[w] = valid ? r4[w] : make_int4(-1, 0, 0, 0);
+        n = qr[0].x;
+        used0 = used1 = 0;
+        scan();
+        have = true;
+      } else if (wpp >= 0 && poll(wpp) >= 0) {
+        scan();  // the awaited input arrived: take every input again
+      }
+      const bool ready = wpp < 0;
       ++n_rounds;
       if (!__all_sync(FULL, ready)) {  // an input from an earlier batch is not coloured yet
         if (++stall > (1ll << 28)) {  // cannot happen (every wait is on a lower position)
@@ -618,6 +645,7 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
         }
         continue;
       }
+      have = false;
       stall = 0;
       int colr;
       if (!__any_sync(FULL, cplx)) {
