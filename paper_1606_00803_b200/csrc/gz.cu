@@ -450,15 +450,19 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
           cn[e] = (uint8_t)cnt;
         }
         __syncwarp();
-        // placement order: most banks first, then by position
-        for (int e = lane; e < U; e += 32) {
-          const int ce = cn[e];
-          int r = 0;
-          for (int e2 = 0; e2 < U; ++e2) {
-            const int c2 = cn[e2];
-            r += (c2 > ce) || (c2 == ce && e2 < e);
+        // placement order: most banks first, then by position -- a counting
+        // sort over the bank counts 9 .. 0, one ballot per count and half
+        {
+          const int c0 = cn[lane], c1 = U > 32 ? cn[lane + 32] : -1;
+          const unsigned lt = (1u << lane) - 1u;
+          int above = 0;
+          for (int v = 9; v >= 0; --v) {
+            const unsigned m0 = __ballot_sync(0xffffffffu, c0 == v);
+            const unsigned m1 = __ballot_sync(0xffffffffu, c1 == v);
+            if (c0 == v) od[above + __popc(m0 & lt)] = (uint8_t)lane;
+            if (c1 == v) od[above + __popc(m0) + __popc(m1 & lt)] = (uint8_t)(lane + 32);
+            above += __popc(m0) + __popc(m1);
           }
-          od[r] = (uint8_t)e;
         }
         __syncwarp();
         const int ng = U / 8;
