@@ -174,12 +174,26 @@ __global__ void k_gz_not_in(const uint64_t* __restrict__ cand, int64_t n, const 
 __global__ void k_gz_collect_u(const uint64_t* __restrict__ keys, int64_t n, int L, int D,
                                const uint8_t* __restrict__ fixed, const int8_t* __restrict__ colour,
                                uint64_t* ukey, uint8_t* ud, unsigned long long* nu) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t v = (int32_t)(keys[i] & 0xffffffffull);
-    if (fixed[v] || L + colour[v] > D - 1) continue;
-    const unsigned long long p = atomicAdd(nu, 1ull);
-    ukey[p] = keys[i];
-    ud[p] = (uint8_t)L;
+  // one atomic per warp (a ballot of the kept entries); the order inside the
+  // output does not matter (it is sorted next)
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31; i0 < n;
+       i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + lane;
+    bool keep = false;
+    if (i < n) {
+      const int32_t v = (int32_t)(keys[i] & 0xffffffffull);
+      keep = !fixed[v] && L + colour[v] <= D - 1;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    unsigned long long base = 0;
+    if (lane == 0 && m) base = atomicAdd(nu, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) {
+      const unsigned long long p = base + __popc(m & ((1u << lane) - 1u));
+      ukey[p] = keys[i];
+      ud[p] = (uint8_t)L;
+    }
   }
 }
 
@@ -242,8 +256,15 @@ __global__ void k_gz_kc(const uint64_t* __restrict__ ck, int64_t n, int64_t K, i
 // per tile: longest row among the tile's updates
 __global__ void k_gzd_tile_r(const uint64_t* __restrict__ ck, const int32_t* __restrict__ cv, int64_t n,
                              const int32_t* __restrict__ rp, int* tR) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    atomicMax(&tR[ck[i] >> 23], rp[cv[i] + 1] - rp[cv[i]]);
+  // keys are sorted by tile: lanes of a warp mostly share one, so one
+  // atomic per distinct tile in the warp
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned act = __activemask();
+    const unsigned long long t = ck[i] >> 23;
+    const unsigned grp = __match_any_sync(act, t);
+    const int d = __reduce_max_sync(grp, (unsigned)(rp[cv[i] + 1] - rp[cv[i]]));
+    if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicMax(&tR[t], d);
+  }
 }
 
 // items per (tile, stage): ceil(updates / 32), stage s = j*C + c
