@@ -704,20 +704,16 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
 // ids and then the start of another: in such a chunk the second chain waits
 // for the end of the first (chunks run in order), which serialises whole
 // chains across chunks.  Splitting one chain across chunks is harmless.
-__global__ void k_gc_bad_chunks(const uint8_t* __restrict__ pstate, int64_t V, int64_t SW,
-                                unsigned long long* bad) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k * SW < V; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = k * SW, b = min(a + SW, V);
-    bool seen = false;
-    for (int64_t p = a; p < b; ++p) {
-      const uint8_t st = pstate[p];
-      if (st == 1 && seen) {
-        atomicAdd(bad, 1ull);
-        break;
-      }
-      seen |= st != 0;
-    }
-  }
+// Two parallel passes: the first free position of every chunk, then every
+// chain start after it marks its chunk.
+__global__ void k_gc_first_free(const uint8_t* __restrict__ pstate, int64_t V, int64_t SW, int64_t* first) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < V; p += (int64_t)gridDim.x * blockDim.x)
+    if (pstate[p]) atomicMin(reinterpret_cast<unsigned long long*>(first + p / SW), (unsigned long long)p);
+}
+__global__ void k_gc_bad_chunks(const uint8_t* __restrict__ pstate, const int64_t* __restrict__ first, int64_t V,
+                                int64_t SW, int* bad) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < V; p += (int64_t)gridDim.x * blockDim.x)
+    if (pstate[p] == 1 && p > first[p / SW]) bad[p / SW] = 1;
 }
 
 // colour[v] = colour of position orig_id[v] (fixed vertices: -1)
@@ -776,15 +772,23 @@ static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
   while (sw > 1024 && (V + 8 * sw - 1) / (8 * sw) < nsm0 / 2) sw /= 2;
   const int SW = env_int_c("LMS_GC_WCHUNK", (int)sw, 32, 1 << 20) & ~31;
   auto aligned = [&](int64_t chunk) {
-    DBuf<unsigned long long> bad(1, s);
-    LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(unsigned long long), s));
     const int64_t nk = (V + chunk - 1) / chunk;
-    k_gc_bad_chunks<<<(unsigned)std::min<int64_t>((nk + 255) / 256, 8192), 256, 0, s>>>(pstate.p, V, chunk, bad.p);
+    DBuf<int64_t> first(nk, s);
+    DBuf<int> bad(nk, s), nbad(1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(first.p, 0x7f, nk * sizeof(int64_t), s));
+    LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, nk * sizeof(int), s));
+    k_gc_first_free<<<Gv, 256, 0, s>>>(pstate.p, V, chunk, first.p);
     LMS_CHECK_LAUNCH();
-    unsigned long long hb = 0;
-    LMS_TRY_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
+    k_gc_bad_chunks<<<Gv, 256, 0, s>>>(pstate.p, first.p, V, chunk, bad.p);
+    LMS_CHECK_LAUNCH();
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceReduce::Sum(nullptr, tb, bad.p, nbad.p, (int)nk, s));
+    DBuf<char> tmp(tb, s);
+    LMS_TRY_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, bad.p, nbad.p, (int)nk, s));
+    int hb = 0;
+    LMS_TRY_CUDA(cudaMemcpyAsync(&hb, nbad.p, sizeof(hb), cudaMemcpyDeviceToHost, s));
     LMS_TRY_CUDA(cudaStreamSynchronize(s));
-    return hb * 100 <= (unsigned long long)nk;
+    return (int64_t)hb * 100 <= nk;
   };
   bool batched;
   if (gce) {
