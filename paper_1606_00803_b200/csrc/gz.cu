@@ -1124,7 +1124,7 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
 // records into the record ring (one TMA bulk copy per record, in claim
 // order), warps 2.. are workers (one claimed item at a time).
 template <int DIM, int RMAX, int UPL, bool STATS>
-__global__ void __launch_bounds__(DIM == 2 ? 1024 : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
+__global__ void __launch_bounds__(DIM == 2 ? (UPL == 2 ? 640 : 768) : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
                                                                       const GzTile* __restrict__ tab,
                                                                       const int32_t* __restrict__ item_sweep,
                                                                       const uint4* __restrict__ meta,
@@ -2064,7 +2064,7 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   // (Its rare failures in back-to-back runs were the record ring's parity
   // ambiguity under out-of-order TMA completion, fixed by rbat.)
   const int upl = env_int("LMS_GZ_UPL", m->dim == 2 ? 2 : 1, 1, m->dim == 2 ? 2 : 1);
-  const int maxw = (m->dim == 2 ? 1024 : 384) / 32;  // the kernel's launch bounds
+  const int maxw = (m->dim == 2 ? (upl == 2 ? 640 : 768) : 384) / 32;  // the kernel's launch bounds
   // workers measured best on C4: 18 with 2 updates per lane, 22 with 1 (more
   // warps only lengthen every item: the shared-memory pipe is the shared
   // resource); + region producer + record loader
