@@ -1124,7 +1124,9 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
 // records into the record ring (one TMA bulk copy per record, in claim
 // order), warps 2.. are workers (one claimed item at a time).
 template <int DIM, int RMAX, int UPL, bool STATS>
-__global__ void __launch_bounds__(DIM == 2 ? (UPL == 2 ? 640 : 768) : 384, 1) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
+// register budget per thread for the CTA's threads (2D 64-update items: 21
+// warps x 96; 32-update items: 25 x 80; 3D: 13 x 152)
+__global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
                                                                       const GzTile* __restrict__ tab,
                                                                       const int32_t* __restrict__ item_sweep,
                                                                       const uint4* __restrict__ meta,
@@ -1146,8 +1148,9 @@ __global__ void __launch_bounds__(DIM == 2 ? (UPL == 2 ? 640 : 768) : 384, 1) k_
   uint64_t* empty = full + NB;                          // [NB] buffer's tile finished
   uint64_t* rfull = empty + NB;                         // [RR] record batch landed
   uint64_t* rempty = rfull + RR;                        // [RR] record batch consumed (BS arrivals)
-  uint64_t* sbar = rempty + RR;                         // [1] producer staging copy landed
-  int* ctl = reinterpret_cast<int*>(sbar + 1);  // [0] cursor, [1..NB] buf_tile, [NB+1..2NB] ndone, then rbat[RR]
+  uint64_t* sbar = rempty + RR;                         // [NPW] producer staging copies landed
+  const int NPW = L.NPW;  // region producer warps (warp p stages tiles i = p mod NPW)
+  int* ctl = reinterpret_cast<int*>(sbar + NPW);  // [0] cursor, [1..NB] buf_tile, [NB+1..2NB] ndone, then rbat[RR]
   volatile int* buf_tile = ctl + 1;
   int* ndone = ctl + 1 + NB;
   // rbat[slot]: the record batch the loader last issued into the slot.  A
@@ -1183,7 +1186,7 @@ __global__ void __launch_bounds__(DIM == 2 ? (UPL == 2 ? 640 : 768) : 384, 1) k_
       mbar_init(rempty + r, L.BS);
       rbat[r] = -1;
     }
-    mbar_init(sbar, 1);
+    for (int p = 0; p < L.NPW; ++p) mbar_init(sbar + p, 1);
     ctl[0] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1214,10 +1217,12 @@ __global__ void __launch_bounds__(DIM == 2 ? (UPL == 2 ? 640 : 768) : 384, 1) k_
   const int total = t_pre[n_my];
   GzGuard guard{gabort, &s_abort};
 
-  if (warp == 0) {  // -------------------------------------------- region producer
+  if (warp < NPW) {  // -------------------------------------------- region producers
     const long long p0 = STATS ? clock64() : 0;
     long long pw = 0;
-    for (int i = 0; i < n_my; ++i) {
+    unsigned char* stgp = stg + (size_t)warp * L.stage_bytes;
+    uint64_t* sb = sbar + warp;
+    for (int i = warp; i < n_my; i += NPW) {
       const int b = i % NB;
       const uint32_t ph = (uint32_t)(i / NB) & 1u;
       const long long q0 = STATS ? clock64() : 0;
@@ -1228,15 +1233,15 @@ __global__ void __launch_bounds__(DIM == 2 ? (UPL == 2 ? 640 : 768) : 384, 1) k_
       const uint32_t bytes = t.meta16 * 16u;
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging was read generically
-        mbar_expect_tx(sbar, bytes);
+        mbar_expect_tx(sb, bytes);
         const unsigned char* src = reinterpret_cast<const unsigned char*>(meta + t.meta_base);
         constexpr uint32_t PIECE = 1u << 15;
         for (uint32_t o = 0; o < bytes; o += PIECE)
-          bulk_g2s(stg + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, sbar);
+          bulk_g2s(stgp + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, sb);
       }
-      if (!mbar_wait_g(sbar, (uint32_t)i & 1u, guard)) return;
+      if (!mbar_wait_g(sb, (uint32_t)(i / NPW) & 1u, guard)) return;
       unsigned char* buf = sm + L.off_ring + (size_t)b * L.buf_bytes;
-      const uint32_t* hsrc = reinterpret_cast<const uint32_t*>(stg);
+      const uint32_t* hsrc = reinterpret_cast<const uint32_t*>(stgp);
       uint32_t* hdst = reinterpret_cast<uint32_t*>(buf);
       for (int q = lane; q < HW; q += 32) hdst[q] = hsrc[q];
       int* cnt = reinterpret_cast<int*>(buf + L.cnt_off);
@@ -1284,7 +1289,7 @@ __global__ void __launch_bounds__(DIM == 2 ? (UPL == 2 ? 640 : 768) : 384, 1) k_
     }
     return;
   }
-  if (warp == 1) {  // ---------------------------------------------- record loader
+  if (warp == NPW) {  // -------------------------------------------- record loader
     // batch g = claims [g*BS, (g+1)*BS) -> batch slot g % RR, record q of the
     // batch at q * rec_bytes; consecutive records of one tile are contiguous
     // in HBM, so a batch is one bulk copy per tile it touches (when the
@@ -1349,7 +1354,7 @@ __global__ void __launch_bounds__(DIM == 2 ? (UPL == 2 ? 640 : 768) : 384, 1) k_
     }
     return;
   }
-  if (warp >= 2 + L.NW) return;
+  if (warp >= NPW + 1 + L.NW) return;
   // ------------------------------------------------------------------- workers
   const unsigned FULL = 0xffffffffu;
   // the current tile's parameters, refreshed when a claim crosses into the next tile
@@ -1680,6 +1685,7 @@ static int64_t kd_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) 
 
 struct GzNeeds {
   int64_t max_slots = 0, max_items = 0, max_meta16 = 0, max_row = 0;
+  int64_t mean_meta16 = 0;  // region staging work per tile: meta 16-byte units (run pairs or ids)
 };
 
 // Build the GZ schedule for tiles of ~T owned vertices and P sweeps per pass.
@@ -1869,6 +1875,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   out->max_slots = mx[0];
   out->max_items = mx[1];
   out->max_meta16 = mx[2];
+  out->mean_meta16 = K > 0 ? meta16_all / K : 0;
   out->max_row = mx[3];
   if (mx[0] > GZ_MAX_REGION || mx[1] > 65534) return false;
   if (!fits(*out)) return false;
@@ -2006,7 +2013,7 @@ static int r16i(int64_t n) { return (int)((n + 15) & ~(int64_t)15); }
 
 // Shared-memory plan for given limits; returns total bytes (> cap if none fits).
 static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, int cap, int want_nb, int nw,
-                           int tiles_cap, GzLayout* L) {
+                           int tiles_cap, GzLayout* L, int npw = 1) {
   L->NPW = 1;
   L->NW = nw;
   // A worker waits for the record batch of its claim; that batch's slot could
@@ -2035,12 +2042,15 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   L->tiles_cap = tiles_cap;
   for (int nb = want_nb > 0 ? want_nb : 8; nb >= 1; --nb) {
     L->NB = nb;
-    const int ctl = (2 * nb + 2 * L->RR + 1) * 8 + (1 + 2 * nb + L->RR) * 4;
+    // two producer warps (when asked for) only if the buffers split evenly
+    // between them: each buffer then has one producer
+    L->NPW = (npw == 2 && nb % 2 == 0) ? 2 : 1;
+    const int ctl = (2 * nb + 2 * L->RR + L->NPW) * 8 + (1 + 2 * nb + L->RR) * 4;
     L->off_rcp = r16i(ctl);
     L->off_tab = L->off_rcp + r16i(8 * (GZ_RCP_MAX + 1));
     const int tab_bytes = r16i((int64_t)tiles_cap * (8 + 4 + 4 + 4 + 4) + 4 * ((int64_t)tiles_cap + 1));
     L->off_stage = L->off_tab + tab_bytes;
-    L->off_rec = L->off_stage + L->stage_bytes;
+    L->off_rec = L->off_stage + L->NPW * L->stage_bytes;
     L->off_ring = (L->off_rec + L->RR * L->BS * L->rec_bytes + 127) & ~127;
     const int64_t total = (int64_t)L->off_ring + (int64_t)nb * L->buf_bytes;
     if (total <= cap) return total;
@@ -2064,11 +2074,17 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   // (Its rare failures in back-to-back runs were the record ring's parity
   // ambiguity under out-of-order TMA completion, fixed by rbat.)
   const int upl = env_int("LMS_GZ_UPL", m->dim == 2 ? 2 : 1, 1, m->dim == 2 ? 2 : 1);
-  const int maxw = (m->dim == 2 ? (upl == 2 ? 640 : 768) : 384) / 32;  // the kernel's launch bounds
+  // warps per CTA: the register file is 16 K registers per scheduler and the
+  // CTA's warps are spread over 4 schedulers, so at the kernel's register
+  // budget (__maxnreg__) at most 20 warps (96 regs, 64-update items), 24 (80)
+  // or 12 (3D, 152)
+  const int cap_warps = m->dim == 2 ? (upl == 2 ? 20 : 24) : 12;
+  const int maxw = cap_warps;  // producers + loader + workers
   // workers measured best on C4: 18 with 2 updates per lane, 22 with 1 (more
   // warps only lengthen every item: the shared-memory pipe is the shared
   // resource); + region producer + record loader
-  const int nw = env_int("LMS_GZ_WORKERS", std::min(maxw - 2, m->dim == 2 ? (upl == 2 ? 18 : 22) : 10), 1, maxw - 2);
+  const int nw_env = env_int("LMS_GZ_WORKERS", 0, 0, maxw - 2);
+  const int nw = nw_env ? nw_env : std::min(maxw - 2, m->dim == 2 ? (upl == 2 ? 18 : 22) : 10);
   const int want_nb = env_int("LMS_GZ_BUFFERS", 0, 0, 8);
   const int dim = m->dim, C = m->C;
   GzNeeds nd;
@@ -2100,16 +2116,27 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
     };
     if (build_gz_once(m, t, P, upl, kd != 0, s, &nd, fits)) {
       const int tiles_cap = (int)((S.gz_ntiles + nsm - 1) / nsm) + 1;
-      const int64_t total = plan_layout(nd, dim, C, P, upl, cap, want_nb, nw, tiles_cap, &S.gz_L);
+      // a second region producer when staging is heavy (regions in many short
+      // runs or as id lists: BFS, RDR, random orderings), at the cost of one
+      // worker; measured C4: BFS 385 -> 356 us, original 276 -> 279 us, so
+      // only above 64 meta units per tile (original 52, BFS 83, RDR 132,
+      // random 907).  LMS_GZ_PRODUCERS=1/2 forces.
+      const int npw_env = env_int("LMS_GZ_PRODUCERS", 0, 0, 2);
+      const int npw = npw_env ? npw_env : (nd.mean_meta16 > 64 ? 2 : 1);
+      const int nw2 = npw == 2 ? std::min(nw, maxw - 3) : nw;
+      int64_t total = plan_layout(nd, dim, C, P, upl, cap, want_nb, nw2, tiles_cap, &S.gz_L, npw);
+      if (npw == 2 && (total > cap || (want_nb == 0 && S.gz_L.NB < min_nb)))  // the second staging area does not fit
+        total = plan_layout(nd, dim, C, P, upl, cap, want_nb, nw, tiles_cap, &S.gz_L, 1);
+      if (S.gz_L.NPW == 1 && S.gz_L.NW != nw) total = plan_layout(nd, dim, C, P, upl, cap, want_nb, nw, tiles_cap, &S.gz_L, 1);
       if (total > cap || (want_nb == 0 && S.gz_L.NB < min_nb)) continue;
       S.gz_smem = (int)total;
-      S.gz_threads = 32 * (2 + S.gz_L.NW);
+      S.gz_threads = 32 * (S.gz_L.NPW + 1 + S.gz_L.NW);
       if (getenv("LMS_GZ_VERBOSE"))
         fprintf(stderr, "[gz] %s T=%d P=%d tiles=%lld items=%lld NB=%d RR=%d NW=%d smem=%d buf=%d slots<=%lld "
-                "items/tile<=%lld regions=%lld updates=%lld blob=%lld B\n", kd ? "kd" : "bins", t, P, (long long)S.gz_ntiles,
+                "items/tile<=%lld regions=%lld updates=%lld blob=%lld B meta16/tile=%lld NPW=%d\n", kd ? "kd" : "bins", t, P, (long long)S.gz_ntiles,
                 (long long)S.gz_items, S.gz_L.NB, S.gz_L.RR, S.gz_L.NW, S.gz_smem, S.gz_L.buf_bytes,
                 (long long)nd.max_slots, (long long)nd.max_items, (long long)S.gz_nreg, (long long)S.gz_nupd,
-                (long long)S.gz_bytes);
+                (long long)S.gz_bytes, (long long)nd.mean_meta16, S.gz_L.NPW);
       return true;
     }
   }
