@@ -426,3 +426,23 @@ def test_colouring_kernels_on_unaligned_grid(mode, wchunk, monkeypatch):
     with gpu_mesh(m) as gm:
         assert np.array_equal(np_(gm.colour()), om["colour"])
         assert gm.info()["C"] == om["C"]
+
+
+@pytest.mark.parametrize("producers", [1, 2])
+@pytest.mark.parametrize("kind", ["original", "bfs", "random"])
+def test_gz_region_producers(producers, kind, monkeypatch):
+    """LMS_GZ_PRODUCERS=1/2: one or two region-producer warps (two stage the
+    tiles of alternate buffers; chosen automatically when staging is heavy,
+    e.g. BFS on C4), bit-exact sweeps under three orderings, two passes."""
+    monkeypatch.setenv("LMS_GZ_PRODUCERS", str(producers))
+    m = meshgen.grid2d(181, 131, 0.3, seed=51)
+    om = oracle.prepare(m)
+    pm = oracle.permute_mesh(om, oracle.order(om, kind, 803))
+    want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 5)
+    with gpu_mesh(m) as gm:
+        gm.permute(cuda(oracle.order(om, kind, 803), torch.int32))
+        gm.set_schedule("gz", tile=500, lag=1)
+        gm.smooth(2)
+        gm.smooth(3)
+        assert gm.schedule_info()["kind"] == "gz"
+        assert bits_equal(gpu_coords(gm), want)
