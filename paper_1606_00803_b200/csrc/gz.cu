@@ -409,7 +409,16 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
                               const int32_t* __restrict__ tile_of, const uint64_t* __restrict__ reg,
                               const int64_t* __restrict__ reg_off, uint4* rec, int32_t* it_lo, int32_t* it_hi) {
   extern __shared__ uint32_t gz_rid[];  // [max region slots]
-  __shared__ uint8_t gz_banks[8 * 64 * 9];
+  // per update: one-hot bank mask of its own slot (byte 0) and neighbours
+  // 0..6 (bytes 1..7); neighbour banks packed 3 bits each (bits 0..23) and
+  // neighbour 7's one-hot bank (bits 24..31)
+  __shared__ unsigned long long gz_bml[8 * 64];
+  __shared__ uint32_t gz_bnb[8 * 64];
+  // gap masks by popcount (kGapMasks) and each one's selection pattern: byte
+  // r is the one-hot position of its r-th set bit (neighbour r's position)
+  __shared__ unsigned long long gz_gsel[256];
+  __shared__ uint8_t gz_gmsk[256];
+  __shared__ uint16_t gz_goff[10];
   __shared__ uint8_t gz_pos[8 * 64];
   __shared__ uint8_t gz_cnt[8 * 64];
   __shared__ uint8_t gz_ord[8 * 64];
@@ -420,12 +429,22 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
   const int nwib = blockDim.x >> 5;
   const int PC = P * C;
   const int U = 32 * UPL;
-  uint8_t* bk = gz_banks + wib * 64 * 9;
+  unsigned long long* bml = gz_bml + wib * 64;
+  uint32_t* bnb = gz_bnb + wib * 64;
   uint8_t* ps = gz_pos + wib * 64;
   uint8_t* cn = gz_cnt + wib * 64;
   uint8_t* od = gz_ord + wib * 64;
   uint8_t* gp = gz_gap + wib * 64;  // row positions used by each update's neighbours (rows of 8)
   uint16_t* sl8 = gz_slot + wib * 64 * 8;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const uint32_t msk = kGapMasks[i];
+    unsigned long long sel = 0;
+    for (int w = 0, r = 0; w < 8; ++w)
+      if ((msk >> w) & 1u) sel |= 1ull << (8 * r++ + w);
+    gz_gsel[i] = sel;
+    gz_gmsk[i] = (uint8_t)msk;
+  }
+  if (threadIdx.x < 10) gz_goff[threadIdx.x] = kGapOff[threadIdx.x];
   for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
     const int64_t ra = reg_off[k], rb = reg_off[k + 1];
     const int nr = (int)(rb - ra);
@@ -454,20 +473,29 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
         for (int u0 = 0; u0 < U; u0 += 32) {
           const int e = u0 + lane;
           int cnt = 0;
-          for (int w = 0; w < 9; ++w) bk[e * 9 + w] = 0xff;
+          unsigned long long ml = 0;
+          uint32_t nbw = 0;
           if (e < n) {
             const int64_t uu = kc_off[kc] + (int64_t)U * q + e;
             const int32_t v = cv[uu];
-            bk[e * 9] = (uint8_t)((ck[uu] & 0xffffull) & 7u);
+            ml = 1ull << ((ck[uu] & 0xffffull) & 7u);
             cnt = 1;
             const int32_t b = rp[v], d = rp[v + 1] - b;
             for (int w = 0; w < d && w < 8; ++w) {
               const int sl = region_slot(gz_rid, nr, (uint32_t)col[b + w]);
               sl8[e * 8 + w] = (uint16_t)sl;
-              bk[e * 9 + 1 + w] = (uint8_t)(sl & 7);
+              const uint32_t bank = (uint32_t)sl & 7u;
+              if (w < 7) {
+                ml |= 1ull << (8 * (w + 1) + bank);
+                nbw |= bank << (3 * w);
+              } else {
+                nbw |= bank << 21 | (1u << (24 + bank));
+              }
               ++cnt;
             }
           }
+          bml[e] = ml;
+          bnb[e] = nbw;
           cn[e] = (uint8_t)cnt;
         }
         __syncwarp();
@@ -487,32 +515,21 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
         }
         __syncwarp();
         const int ng = U / 8;
-        uint64_t qlo = 0;  // this lane's group (lane < ng): banks used per neighbour slot w < 8
-        uint32_t qhi = 0;  // ... and for w = 8
+        uint64_t qlo = 0;  // this lane's group (lane < ng): bank masks of slots w < 8 (bml layout)
+        uint32_t qhi = 0;  // ... and of slot 8 (bnb bits 24..31)
         int qn = 0;
         for (int r = 0; r < U; ++r) {
           const int e = od[r];
-          int pen = 1 << 20;
-          if (lane < ng && qn < 8) {
-            pen = 0;
-            for (int w = 0; w < 9; ++w) {
-              const int bb = bk[e * 9 + w];
-              if (bb != 0xff) pen += (int)((w < 8 ? (qlo >> (8 * w + bb)) : (uint64_t)(qhi >> bb)) & 1u);
-            }
-          }
-          int key = (pen << 5) | lane;
-          for (int o = 16; o; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
-          const int best = key & 31;
+          const unsigned long long ml = bml[e];
+          const uint32_t mh = bnb[e] & 0xff000000u;
+          unsigned key = (1u << 25) | lane;
+          if (lane < ng && qn < 8) key = (unsigned)(__popcll(qlo & ml) + __popc(qhi & mh)) << 5 | lane;
+          const int best = (int)(__reduce_min_sync(0xffffffffu, key) & 31u);
           if (lane == best) {
             ps[e] = (uint8_t)(8 * best + qn);
             ++qn;
-            for (int w = 0; w < 9; ++w) {
-              const int bb = bk[e * 9 + w];
-              if (bb != 0xff) {
-                if (w < 8) qlo |= 1ull << (8 * w + bb);
-                else qhi |= 1u << bb;
-              }
-            }
+            qlo |= ml;
+            qhi |= mh;
           }
         }
         __syncwarp();
@@ -530,33 +547,30 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
         __syncwarp();
         for (int a0 = 0; a0 < ng; a0 += 4) {
           const int a = a0 + (lane >> 3), sub = lane & 7;
-          uint64_t occ = 0;  // bit 8w + bank: bank already read at position w
+          uint64_t occ = 0;  // bit 8 * bank + w: bank already read at position w
           for (int j = 0; j < 8; ++j) {
             const int e = a < ng ? od[8 * a + j] : 0;
             const int dn = a < ng && cn[e] > 0 ? cn[e] - 1 : 0;
-            uint32_t nb = 0;  // neighbour k's bank at bits 3k
-            for (int kk = 0; kk < dn && kk < 8; ++kk) nb |= (uint32_t)bk[e * 9 + 1 + kk] << (3 * kk);
+            const uint32_t nb = a < ng ? bnb[e] & 0xffffffu : 0u;  // neighbour k's bank at bits 3k
             int key = 0x7fffffff;
-            if (dn > 0 && dn < 8)
-              for (int t = kGapOff[dn] + sub; t < kGapOff[dn + 1]; t += 8) {
-                const int msk = kGapMasks[t];
-                int c = 0;
-                uint32_t q = nb;
+            if (dn > 0 && dn < 8) {
+              // byte k: the positions where neighbour k's bank is already read
+              unsigned long long hit = 0;
 #pragma unroll
-                for (int w = 0; w < 8; ++w)
-                  if ((msk >> w) & 1) {
-                    c += (int)((occ >> (8 * w + (q & 7u))) & 1u);
-                    q >>= 3;
-                  }
-                key = min(key, (c << 8) | msk);
-              }
+              for (int kk = 0; kk < 7; ++kk)
+                hit |= ((occ >> (8 * ((nb >> (3 * kk)) & 7u))) & 0xffull) << (8 * kk);
+              // collisions of a mask = popc(hit & selection); the table index
+              // orders masks of one popcount ascending, so it breaks ties
+              for (int t = gz_goff[dn] + sub; t < gz_goff[dn + 1]; t += 8)
+                key = min(key, (__popcll(hit & gz_gsel[t]) << 8) | t);
+            }
             for (int o = 1; o < 8; o <<= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
-            const int best = dn >= 8 ? 0xff : (dn > 0 ? (key & 0xff) : 0);
+            const int best = dn >= 8 ? 0xff : (dn > 0 ? (int)gz_gmsk[key & 0xff] : 0);
             if (a < ng && sub == 0) gp[e] = (uint8_t)best;
             uint32_t q = nb;
             for (int w = 0; w < 8; ++w)
               if ((best >> w) & 1) {
-                occ |= 1ull << (8 * w + (q & 7u));
+                occ |= 1ull << (8 * (q & 7u) + w);
                 q >>= 3;
               }
           }
