@@ -707,8 +707,15 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
 // Two parallel passes: the first free position of every chunk, then every
 // chain start after it marks its chunk.
 __global__ void k_gc_first_free(const uint8_t* __restrict__ pstate, int64_t V, int64_t SW, int64_t* first) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < V; p += (int64_t)gridDim.x * blockDim.x)
-    if (pstate[p]) atomicMin(reinterpret_cast<unsigned long long*>(first + p / SW), (unsigned long long)p);
+  // one atomic per (warp, chunk): the lowest set position of each chunk the
+  // warp's 32 consecutive positions touch (positions ascend with the lane)
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < V; p += (int64_t)gridDim.x * blockDim.x) {
+    const bool set = pstate[p] != 0;
+    const unsigned m = __ballot_sync(__activemask(), set) & ((1u << lane) - 1u);
+    const bool lead = set && (m == 0 || (p - (lane - (31 - __clz(m)))) / SW != p / SW);
+    if (lead) atomicMin(reinterpret_cast<unsigned long long*>(first + p / SW), (unsigned long long)p);
+  }
 }
 __global__ void k_gc_bad_chunks(const uint8_t* __restrict__ pstate, const int64_t* __restrict__ first, int64_t V,
                                 int64_t SW, int* bad) {

@@ -567,12 +567,11 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
             for (int o = 1; o < 8; o <<= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
             const int best = dn >= 8 ? 0xff : (dn > 0 ? (int)gz_gmsk[key & 0xff] : 0);
             if (a < ng && sub == 0) gp[e] = (uint8_t)best;
-            uint32_t q = nb;
-            for (int w = 0; w < 8; ++w)
-              if ((best >> w) & 1) {
-                occ |= 1ull << (8 * (q & 7u) + w);
-                q >>= 3;
-              }
+            // neighbour k's position (byte k of the selection) into its bank's byte
+            const unsigned long long sel =
+                dn >= 8 ? 0x8040201008040201ull : (dn > 0 ? gz_gsel[key & 0xff] : 0ull);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) occ |= ((sel >> (8 * kk)) & 0xffull) << (8 * ((nb >> (3 * kk)) & 7u));
           }
         }
         __syncwarp();
