@@ -505,8 +505,8 @@ __device__ __forceinline__ int gc_compose(int a, int b) {  // a o b (b first)
 
 template <int RL>
 __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ rec, const int* __restrict__ ulo,
-                                                  int64_t V, int SW, int MW, int* ctr, int8_t* colpos, int* maxc,
-                                                  int* err, unsigned long long* st) {
+                                                  int64_t V, int SW, int MW, int shift, int* ctr, int8_t* colpos,
+                                                  int* maxc, int* err, unsigned long long* st) {
   extern __shared__ __align__(16) unsigned char gsm[];
   __shared__ int64_t s_base, s_mlo;
   __shared__ int s_done;
@@ -544,18 +544,33 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
       long long idle = 0;
       while (nblk > 0) {
         bool all = true;
-        for (int k = lane; k < nblk; k += 32) {
-          const int4 h = m16[k];
-          if (((h.x | h.y | h.z | h.w) & 0x80808080) == 0) continue;
-          int4 g;
-          asm volatile("ld.volatile.global.v4.s32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(g.x), "=r"(g.y), "=r"(g.z), "=r"(g.w)
-                       : "l"(g16 + k));
-          asm volatile("st.volatile.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(
-                           (uint32_t)__cvta_generic_to_shared(m16 + k)),
-                       "r"(g.x), "r"(g.y), "r"(g.z), "r"(g.w)
-                       : "memory");
-          if ((g.x | g.y | g.z | g.w) & 0x80808080) all = false;
+        // four blocks per lane per step: their global loads are in flight
+        // together, so a pass costs about one L2 round trip per 128 blocks
+        for (int k0 = lane; k0 < nblk; k0 += 128) {
+          int4 g[4];
+          bool need[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = k0 + 32 * u;
+            need[u] = false;
+            if (k < nblk) {
+              const int4 h = m16[k];
+              need[u] = ((h.x | h.y | h.z | h.w) & 0x80808080) != 0;
+            }
+            if (need[u])
+              asm volatile("ld.volatile.global.v4.s32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(g[u].x), "=r"(g[u].y), "=r"(g[u].z), "=r"(g[u].w)
+                           : "l"(g16 + k));
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (need[u]) {
+              asm volatile("st.volatile.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(
+                               (uint32_t)__cvta_generic_to_shared(m16 + k0 + 32 * u)),
+                           "r"(g[u].x), "r"(g[u].y), "r"(g[u].z), "r"(g[u].w)
+                           : "memory");
+              if ((g[u].x | g[u].y | g[u].z | g[u].w) & 0x80808080) all = false;
+            }
         }
         if (__all_sync(FULL, all)) break;
         if (*(volatile int*)&s_done == NWK) break;
@@ -565,10 +580,18 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
     }
     const int64_t a = ub + (int64_t)warp * SW;
     const int64_t b = min(a + SW, V);
-    const int nb = a < b ? (int)((b - a + 31) / 32) : 0;
+    // batch t of the chunk holds positions a0 + 32 t + lane (those in [a, b)).
+    // Chunk k starts its batches k mod 32 positions early: when a chunk's
+    // positions read the previous chunk's about one chunk back (a grid row),
+    // the last lane of batch t then reads the last lane of the previous
+    // chunk's batch t instead of the first of batch t + 1, and the wavefront
+    // across chunks advances one batch per chunk instead of two
+    const int sft = shift ? (int)((a / SW) & 31) : 0;
+    const int64_t a0 = a - sft;
+    const int nb = a < b ? (int)((b - a0 + 31) / 32) : 0;
     auto issue = [&](int t) {  // records of batch t into its ring slot (empty group past the chunk)
-      const int64_t p = a + 32 * (int64_t)t + lane;
-      if (t < nb && p < b) {
+      const int64_t p = a0 + 32 * (int64_t)t + lane;
+      if (t < nb && p >= a && p < b) {
         int4* d = ring + ((size_t)(t % G) * 32 + lane) * NV;
         const int4* src = reinterpret_cast<const int4*>(rec + p * RL);
 #pragma unroll
@@ -583,7 +606,7 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
     // seen so far (an OR: re-reads are harmless) and the first input still
     // missing (wpp; -1 = none) -- a waiting round polls only that one
     bool have = false;
-    int64_t base = 0, i = 0, wpp = -1;
+    int64_t base = 0, blo = 0, i = 0, wpp = -1;
     bool valid = false, dep_prev = false, cplx = false;
     uint32_t inb = 0;
     uint64_t used0 = 0, used1 = 0;
@@ -603,7 +626,7 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
         if (w > n) break;
         const int4 v4 = qr[w >> 2];
         const int64_t pp = (w & 3) == 0 ? v4.x : (w & 3) == 1 ? v4.y : (w & 3) == 2 ? v4.z : v4.w;
-        if (pp >= base) {  // in this batch (pp < i)
+        if (pp >= blo) {  // in this batch (pp < i)
           const int lj = (int)(pp - base);
           inb |= 1u << lj;
           if (lj == lane - 1) dep_prev = true;
@@ -623,9 +646,10 @@ __global__ void __launch_bounds__(288) k_gc_batch(const int32_t* __restrict__ re
     for (int t = 0; t < nb && !dead;) {
       if (!have) {
         cpa_wait<G - 1>();  // this lane's record of batch t landed
-        base = a + 32 * (int64_t)t;
+        base = a0 + 32 * (int64_t)t;
+        blo = base > a ? base : a;  // lower positions belong to earlier chunks
         i = base + lane;
-        valid = i < b;
+        valid = i >= a && i < b;
         const int4* r4 = ring + ((size_t)(t % G) * 32 + lane) * NV;
 #pragma unroll
         for (int w = 0; w < NV; ++w) qr[w] = valid ? r4[w] : make_int4(-1, 0, 0, 0);
@@ -834,7 +858,8 @@ static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
   void (*kern_l)(const int32_t*, const int32_t*, const int*, int64_t, int, int, int*, int8_t*, int8_t*, int*, int*,
                  unsigned long long*) =
       RL == 4 ? k_gc_seq<4, G> : RL == 8 ? k_gc_seq<8, G> : RL == 16 ? k_gc_seq<16, G> : k_gc_seq<32, G>;
-  void (*kern_b)(const int32_t*, const int*, int64_t, int, int, int*, int8_t*, int*, int*, unsigned long long*) =
+  void (*kern_b)(const int32_t*, const int*, int64_t, int, int, int, int*, int8_t*, int*, int*,
+                 unsigned long long*) =
       RL == 4 ? k_gc_batch<4> : RL == 8 ? k_gc_batch<8> : RL == 16 ? k_gc_batch<16> : k_gc_batch<32>;
   const void* kern = batched ? (const void*)kern_b : (const void*)kern_l;
   if (smem > 227 * 1024) return false;
@@ -868,7 +893,8 @@ static bool colour_in_order(lms_mesh_s* m, int* maxc, cudaStream_t s) {
   }
   int a_sw = SW;
   void* args_l[] = {&a_rec, &a_vid, &a_ulo, &a_V, &a_S, &a_mw, &a_ctr, &a_cp, &a_col, &a_max, &a_err, &a_st};
-  void* args_b[] = {&a_rec, &a_ulo, &a_V, &a_sw, &a_mw, &a_ctr, &a_cp, &a_max, &a_err, &a_st};
+  int a_shift = env_int_c("LMS_GC_SHIFT", 1, 0, 1);
+  void* args_b[] = {&a_rec, &a_ulo, &a_V, &a_sw, &a_mw, &a_shift, &a_ctr, &a_cp, &a_max, &a_err, &a_st};
   void** args = batched ? args_b : args_l;
   const bool verbose = getenv("LMS_COLOUR_VERBOSE") != nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
