@@ -1,0 +1,4 @@
+#!/bin/bash
+timeout 900 python bench.py > gpurun_out/final3_bench.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/final3_bench.log | python -c "import json,sys; b=json.loads(sys.stdin.read()); print(round(b['value']/1e9,2), b['e2e']['ms_per_step'], b['e2e']['step_ms'])"
+timeout 900 python bench.py --no-cpu 2>&1 | tail -1 | python -c "import json,sys; b=json.loads(sys.stdin.read()); print(round(b['value']/1e9,2), b['e2e']['ms_per_step'], b['e2e']['step_ms'])"
