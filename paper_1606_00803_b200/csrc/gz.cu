@@ -1531,14 +1531,36 @@ static unsigned gsz(int64_t n, int block = 256, unsigned cap = 8192) {
   return g > cap ? cap : g;
 }
 
-static void sort_keys(DBuf<uint64_t>& keys, int64_t n, int end_bit, cudaStream_t s) {
+// (tile << 32 | id) keys <-> (tile << idb | id), ids < 2^idb: the same order
+// in idb + kbits bits, so the radix sort runs fewer 8-bit passes
+__global__ void k_key_pack(uint64_t* k, int64_t n, int idb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    k[i] = ((k[i] >> 32) << idb) | (k[i] & 0xffffffffull);
+}
+__global__ void k_key_unpack(uint64_t* k, int64_t n, int idb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    k[i] = ((k[i] >> idb) << 32) | (k[i] & ((1ull << idb) - 1ull));
+}
+
+// sort (tile, id) keys: tiles < 2^kbits, ids < 2^idb
+static void sort_keys(DBuf<uint64_t>& keys, int64_t n, int kbits, int idb, cudaStream_t s) {
   if (n <= 1) return;
+  const bool pack = idb < 32;
+  if (pack) {
+    k_key_pack<<<gsz(n), 256, 0, s>>>(keys.p, n, idb);
+    LMS_CHECK_LAUNCH();
+  }
+  const int end_bit = (pack ? idb : 32) + kbits;
   DBuf<uint64_t> out(n, s);
   size_t tb = 0;
   LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.p, out.p, n, 0, end_bit, s));
   DBuf<char> tmp(tb, s);
   LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, out.p, n, 0, end_bit, s));
   keys = std::move(out);
+  if (pack) {
+    k_key_unpack<<<gsz(n), 256, 0, s>>>(keys.p, n, idb);
+    LMS_CHECK_LAUNCH();
+  }
 }
 
 static int64_t read_i64(const void* dptr, bool is64, cudaStream_t s) {
@@ -1725,6 +1747,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   const int64_t K = kd ? kd_tiles(m, T, tile_of.p, s) : spatial_tiles(m, T, tile_of.p, s);
   const int kbits = bits_for(K + 1);
   const int end_bit = 32 + kbits;
+  const int idb = bits_for(V);  // vertex ids < 2^idb
 
   mark("tiling");
   // level 0: the owned free vertices of every tile, sorted by (tile, id)
@@ -1753,7 +1776,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   for (int L = 1; L < D; ++L) {
     DBuf<uint64_t> cand;
     int64_t nc = expand(lev[L - 1], nlev[L - 1], m, 0, cand, s, L == 1 ? tile_of.p : nullptr);
-    sort_keys(cand, nc, end_bit, s);
+    sort_keys(cand, nc, kbits, idb, s);
     nc = unique_keys(cand, nc, s);
     DBuf<uint8_t> keep(nc > 0 ? nc : 1, s);
     if (nc > 0) {
@@ -1794,7 +1817,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   // the expansion skips in-tile free neighbours (the tile_of filter)
   DBuf<uint64_t> reg;
   int64_t nreg_all = expand(ukey, nU, m, 1, reg, s, tile_of.p);
-  sort_keys(reg, nreg_all, end_bit, s);
+  sort_keys(reg, nreg_all, kbits, idb, s);
   nreg_all = unique_keys(reg, nreg_all, s);
   DBuf<int64_t> reg_off(K + 1, s);
   k_gz_tile_off<<<gsz(K + 1), 256, 0, s>>>(reg.p, nreg_all, K, reg_off.p);

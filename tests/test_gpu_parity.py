@@ -428,6 +428,25 @@ def test_colouring_kernels_on_unaligned_grid(mode, wchunk, monkeypatch):
         assert gm.info()["C"] == om["C"]
 
 
+@pytest.mark.parametrize("shift", ["1", "0"])
+@pytest.mark.parametrize("shape", [(1024, 45), (500, 90), (1000, 37)])
+def test_colouring_batch_shift(shift, shape, monkeypatch):
+    """Batched colouring with and without the per-chunk batch shift
+    (LMS_GC_SHIFT): chunk k's 32-position batches start k mod 32 positions
+    early, lanes before the chunk idle and positions before it polled, not
+    scanned.  Rows of one chunk (1024, the case the shift is for), rows
+    straddling chunks (500, 1000), ragged last units; colours bit-exact
+    against the oracle's sequential greedy (reading Z2)."""
+    monkeypatch.setenv("LMS_GC", "batch")
+    monkeypatch.setenv("LMS_GC_WCHUNK", "1024")
+    monkeypatch.setenv("LMS_GC_SHIFT", shift)
+    m = meshgen.grid2d(shape[0], shape[1], 0.3, seed=61)
+    om = oracle.prepare(m)
+    with gpu_mesh(m) as gm:
+        assert np.array_equal(np_(gm.colour()), om["colour"])
+        assert gm.info()["C"] == om["C"]
+
+
 @pytest.mark.parametrize("producers", [1, 2])
 @pytest.mark.parametrize("kind", ["original", "bfs", "random"])
 def test_gz_region_producers(producers, kind, monkeypatch):
