@@ -91,6 +91,24 @@ lms_status lms_build_csr(int32_t dim, int64_t n_vertices, const double* const* d
                          int32_t verts_per_elem, int64_t n_elems, const int32_t* d_elems,
                          const uint8_t* d_fixed, lms_stream_t stream, lms_mesh_t* out);
 
+/* lms_build_csr_host -- lms_build_csr from HOST buffers, with the upload
+ *  pipelined (the end-to-end ingest path).  Same arguments and results as
+ *  lms_build_csr, except:
+ *  h_coords: host array of dim HOST pointers, double[n_vertices] each;
+ *  h_elems: host int32[n_elems * verts_per_elem]; h_fixed: host uint8[V] or NULL.
+ *  The elements (and mask) are copied to the device on `stream`; the
+ *  coordinates on a library-owned side stream, overlapping the CSR build and
+ *  the colouring, which do not read them.  `stream` waits for that upload
+ *  before the call returns its work, so later calls on `stream` see the
+ *  coordinates.  For the copies to overlap, the host buffers must be
+ *  page-locked (cudaHostAlloc / torch pin_memory); pageable buffers give the
+ *  same result without overlap.  The host buffers must stay valid and
+ *  unmodified until `stream` has passed this call's work (the copies are
+ *  asynchronous).  Errors as lms_build_csr. */
+lms_status lms_build_csr_host(int32_t dim, int64_t n_vertices, const double* const* h_coords,
+                              int32_t verts_per_elem, int64_t n_elems, const int32_t* h_elems,
+                              const uint8_t* h_fixed, lms_stream_t stream, lms_mesh_t* out);
+
 /* lms_mesh_from_csr -- build a handle from a ready CSR (test/debug entry).
  *  d_row_ptr int32[V+1], d_col_idx int32[nnz] (rows ascending, symmetric, no
  *  self loops -- not re-validated beyond index range and deg >= 1).

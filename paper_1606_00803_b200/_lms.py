@@ -24,7 +24,7 @@ LMS_STATUS = {0: "LMS_OK", -1: "LMS_E_ARG", -2: "LMS_E_INDEX", -3: "LMS_E_ISOLAT
               -5: "LMS_E_DEGENERATE", -6: "LMS_E_NOMEM", -7: "LMS_E_CUDA", -8: "LMS_E_NCCL", -9: "LMS_E_STATE"}
 
 # every symbol include/lms.h declares (tests check the library exports them all)
-EXPORTS = ["lms_build_csr", "lms_mesh_from_csr", "lms_mesh_destroy", "lms_order", "lms_permute", "lms_smooth",
+EXPORTS = ["lms_build_csr", "lms_build_csr_host", "lms_mesh_from_csr", "lms_mesh_destroy", "lms_order", "lms_permute", "lms_smooth",
            "lms_set_schedule", "lms_mesh_info", "lms_schedule_info", "lms_export_coords", "lms_import_coords",
            "lms_export_csr", "lms_export_colour", "lms_export_fixed", "lms_export_orig_id", "lms_export_elems",
            "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_cache_release", "lms_set_allocator", "lms_set_tiling", "lms_schedule_info2",
@@ -54,6 +54,7 @@ def load_library(build: bool = True):
     PP = ct.POINTER(ct.c_void_p)
     sig = {
         "lms_build_csr": [i32, i64, PP, i32, i64, P, P, P, ct.POINTER(P)],
+        "lms_build_csr_host": [i32, i64, PP, i32, i64, P, P, P, ct.POINTER(P)],
         "lms_mesh_from_csr": [i32, i64, PP, P, P, P, P, P, P, P, ct.POINTER(P)],
         "lms_mesh_destroy": [P],
         "lms_order": [P, i32, u64, P, P],
@@ -157,6 +158,18 @@ def _dev(t: torch.Tensor, dtype, n=None, name="tensor"):
     return ct.c_void_p(t.data_ptr())
 
 
+def _host(t: torch.Tensor, dtype, n=None, name="tensor"):
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a CPU tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"{name} must have {n} elements, got {t.numel()}")
+    return ct.c_void_p(t.data_ptr())
+
+
 def _ptr_array(ts):
     arr = (ct.c_void_p * 3)()
     for i, t in enumerate(ts):
@@ -186,6 +199,25 @@ class Mesh:
         h = ct.c_void_p()
         _check(lib().lms_build_csr(dim, V, pp, elems.shape[1], elems.shape[0], pe, pf, _stream(stream),
                                    ct.byref(h)), "lms_build_csr")
+        return cls(h)
+
+    @classmethod
+    def build_csr_host(cls, coords, elems: torch.Tensor, fixed: torch.Tensor | None = None, stream=None) -> "Mesh":
+        """lms_build_csr_host: coords = list of dim float64 CPU tensors [V] (pinned
+        for overlap); elems int32 CPU [n_el, k].  The tensors must stay alive and
+        unmodified until the stream has passed this call (asynchronous copies)."""
+        dim = len(coords)
+        V = coords[0].numel()
+        for c in coords:
+            _host(c, torch.float64, V, "coords")
+        if elems.dim() != 2:
+            raise ValueError("elems must be [n_elems, verts_per_elem]")
+        pe = _host(elems, torch.int32, name="elems")
+        pf = None if fixed is None else _host(fixed, torch.uint8, V, "fixed")
+        pp, keep = _ptr_array(coords)
+        h = ct.c_void_p()
+        _check(lib().lms_build_csr_host(dim, V, pp, elems.shape[1], elems.shape[0], pe, pf, _stream(stream),
+                                        ct.byref(h)), "lms_build_csr_host")
         return cls(h)
 
     @classmethod

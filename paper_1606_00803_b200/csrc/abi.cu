@@ -1,6 +1,8 @@
 // abi.cu -- the extern "C" entry points declared in include/lms.h.
 // Validation, handle lifetime, error reporting; the work is in the other .cu files.
 #include <atomic>
+#include <map>
+#include <mutex>
 #include <cstring>
 
 #include <chrono>
@@ -168,6 +170,85 @@ lms_status lms_build_csr(int32_t dim, int64_t n_vertices, const double* const* d
     mark("colouring");
     m->n_free = count_free(m, s);
     mark("count");
+  } catch (...) {
+    delete m;
+    throw;
+  }
+  *out = m;
+  return LMS_OK;
+  LMS_API_END
+}
+
+// a non-blocking side stream per device for the coordinate upload of
+// lms_build_csr_host (created on first use, kept for the process)
+static cudaStream_t side_stream(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t st = nullptr;
+  LMS_TRY_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  streams[dev] = st;
+  return st;
+}
+
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventPair() {
+    LMS_TRY_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    LMS_TRY_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+  }
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+lms_status lms_build_csr_host(int32_t dim, int64_t n_vertices, const double* const* h_coords,
+                              int32_t verts_per_elem, int64_t n_elems, const int32_t* h_elems,
+                              const uint8_t* h_fixed, lms_stream_t stream, lms_mesh_t* out) {
+  LMS_API_BEGIN
+  lms_mesh_s* m = nullptr;
+  if (!out) fail(LMS_E_ARG, "out is NULL");
+  if (dim != 2 && dim != 3) fail(LMS_E_ARG, "dim must be 2 or 3");
+  if (verts_per_elem != 3 && verts_per_elem != 4) fail(LMS_E_ARG, "verts_per_elem must be 3 or 4");
+  if (n_vertices < 1 || n_vertices >= ((int64_t)1 << 31) - 1) fail(LMS_E_ARG, "n_vertices out of range");
+  if (n_elems < 1 || !h_elems) fail(LMS_E_ARG, "need at least one element");
+  if (n_elems * verts_per_elem >= ((int64_t)1 << 31)) fail(LMS_E_ARG, "too many elements for int32 indexing");
+  check_coords(dim, h_coords);
+  cudaStream_t s = (cudaStream_t)stream;
+  m = new_mesh(dim, n_vertices, s);
+  try {
+    m->k = verts_per_elem;
+    m->n_el = n_elems;
+    // elements (and the caller's fixed mask) first, on the call's stream
+    m->elems.alloc(n_elems * verts_per_elem, s);
+    LMS_TRY_CUDA(cudaMemcpyAsync(m->elems.p, h_elems, n_elems * verts_per_elem * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, s));
+    m->fixed.alloc(n_vertices, s);
+    if (h_fixed) LMS_TRY_CUDA(cudaMemcpyAsync(m->fixed.p, h_fixed, n_vertices, cudaMemcpyHostToDevice, s));
+    for (int a = 0; a < dim; ++a) m->x[a].alloc(n_vertices, s);
+    // coordinates on the side stream, overlapping the CSR build and the
+    // colouring (neither reads them); the call's stream waits before it returns
+    EventPair ev;
+    cudaStream_t s2 = side_stream(m->device);
+    LMS_TRY_CUDA(cudaEventRecord(ev.a, s));  // the allocations above are stream-ordered on s
+    LMS_TRY_CUDA(cudaStreamWaitEvent(s2, ev.a, 0));
+    for (int a = 0; a < dim; ++a)
+      LMS_TRY_CUDA(cudaMemcpyAsync(m->x[a].p, h_coords[a], n_vertices * sizeof(double), cudaMemcpyHostToDevice, s2));
+    LMS_TRY_CUDA(cudaEventRecord(ev.b, s2));
+    try {
+      build_csr_from_elems(m, nullptr, h_fixed == nullptr, s);
+      m->orig_id.alloc(n_vertices, s);
+      fill_iota(m->orig_id.p, n_vertices, s);
+      compute_colouring(m, s);  // colour from orig_id = input label (reading Z2)
+    } catch (...) {
+      cudaStreamWaitEvent(s, ev.b, 0);  // the upload still writes m->x: order the frees after it
+      throw;
+    }
+    LMS_TRY_CUDA(cudaStreamWaitEvent(s, ev.b, 0));
+    m->n_free = count_free(m, s);
   } catch (...) {
     delete m;
     throw;

@@ -337,8 +337,10 @@ static void boundary_faces(lms_mesh_s* m, cudaStream_t s) {
 void build_csr_from_elems(lms_mesh_s* m, const int32_t* d_elems, bool want_boundary, cudaStream_t s) {
   const int k = m->k;
   const int64_t n_el = m->n_el, V = m->V;
-  m->elems.alloc(n_el * k, s);
-  LMS_TRY_CUDA(cudaMemcpyAsync(m->elems.p, d_elems, n_el * k * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  if (d_elems) {  // NULL: the caller filled m->elems (lms_build_csr_host)
+    m->elems.alloc(n_el * k, s);
+    LMS_TRY_CUDA(cudaMemcpyAsync(m->elems.p, d_elems, n_el * k * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  }
   const unsigned Ge = grid_for(n_el, 256) > 8192 ? 8192 : grid_for(n_el, 256);
   k_validate_elems<<<Ge, 256, 0, s>>>(m->elems.p, n_el, k, V, m->err.p);
   LMS_CHECK_LAUNCH();

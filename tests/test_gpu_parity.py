@@ -428,6 +428,49 @@ def test_colouring_kernels_on_unaligned_grid(mode, wchunk, monkeypatch):
         assert gm.info()["C"] == om["C"]
 
 
+@pytest.mark.parametrize("name", ["grid41x25_1025", "kuhn7", "graded"])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_build_csr_host_matches_device_build(name, pinned):
+    """lms_build_csr_host (host buffers; elements on the call's stream,
+    coordinates on the side stream overlapping the CSR build and colouring)
+    gives the handle lms_build_csr gives: CSR, fixed mask, colours, coordinates
+    and a 5-sweep smooth bit-exact against the oracle; pinned and pageable."""
+    m = dict(SMALL)[name]()
+    om = oracle.prepare(m)
+    hc = [torch.from_numpy(np.ascontiguousarray(c)) for c in m["coords"]]
+    he = torch.from_numpy(np.ascontiguousarray(m["elems"]))
+    if pinned:
+        hc = [t.pin_memory() for t in hc]
+        he = he.pin_memory()
+    gm = lms.Mesh.build_csr_host(hc, he)
+    try:
+        rp, col = gpu_csr(gm)
+        assert np.array_equal(rp, om["row_ptr"]) and np.array_equal(col, om["col"])
+        assert np.array_equal(np_(gm.fixed()), oracle.boundary(m.V, m["elems"]))
+        assert np.array_equal(np_(gm.colour()), om["colour"])
+        assert bits_equal(gpu_coords(gm), om["coords"])
+        gm.smooth(5)
+        want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 5)
+        assert bits_equal(gpu_coords(gm), want)
+    finally:
+        gm.close()
+
+
+def test_build_csr_host_errors():
+    """Host build: a bad element index is LMS_E_INDEX (raised while the
+    coordinate upload may still be in flight), device tensors are refused."""
+    m = meshgen.grid2d(20, 20, 0.2, seed=3)
+    hc = [torch.from_numpy(np.ascontiguousarray(c)).pin_memory() for c in m["coords"]]
+    el = np.ascontiguousarray(m["elems"]).copy()
+    el[5, 1] = m.V + 7
+    with pytest.raises(lms.LMSError):
+        lms.Mesh.build_csr_host(hc, torch.from_numpy(el).pin_memory())
+    with pytest.raises(TypeError):
+        lms.Mesh.build_csr_host([c.cuda() for c in hc], torch.from_numpy(np.ascontiguousarray(m["elems"])))
+    gm = lms.Mesh.build_csr_host(hc, torch.from_numpy(np.ascontiguousarray(m["elems"])))
+    gm.close()
+
+
 @pytest.mark.parametrize("shift", ["1", "0"])
 @pytest.mark.parametrize("shape", [(1024, 45), (500, 90), (1000, 37)])
 def test_colouring_batch_shift(shift, shape, monkeypatch):
