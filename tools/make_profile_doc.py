@@ -72,7 +72,7 @@ loader state (DESIGN.md 6.1).
 - roofline: achieved {b['roofline']['achieved']:.0f} GB/s of measured {b['roofline']['peak']} GB/s = **{b['roofline']['frac']:.3f}**
   ({b['roofline']['launch_ms'] * 1e3:.1f} us per sweep launch; algorithmic {bsw / 1e9:.3f} GB per sweep)
 - e2e: **{e2e['value'] / 1e9:.2f} G vertex-updates/s**, {e2e['ms_per_step']:.1f} ms per step. This covers
-  host buffers → H2D → build_csr + colouring → order + permute → schedule → 50 sweeps → D2H.
+  `{e2e["path"]}`.
   Phases (ms): {json.dumps({k: round(v, 1) for k, v in e2e['phases_ms'].items()})}
 - cpu_baseline: {(f"{b['cpu_baseline']['value'] / 1e9:.3f} G vertex-updates/s on {b['cpu_baseline']['cores']} host cores ({b['cpu_baseline']['kind']}: {b['cpu_baseline']['sample']})") if b.get('cpu_baseline') else 'not run'}
 - clocks {json.dumps(b['clocks'])}
