@@ -9,9 +9,10 @@
 
 namespace lms {
 
-__global__ void k_inverse(const int32_t* __restrict__ perm, int64_t V, int32_t* inv, int* err) {
+__global__ void k_inverse(const int32_t* __restrict__ perm, int64_t V, int32_t* inv, int* err, int* moved) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < V; k += (int64_t)gridDim.x * blockDim.x) {
     int32_t p = perm[k];
+    if (p != k && !*(volatile int*)moved) *moved = 1;
     if (p < 0 || p >= V) { raise_err(err, LMS_E_PERM); continue; }
     int32_t old = atomicExch(&inv[p], (int32_t)k);
     if (old != -1) raise_err(err, LMS_E_PERM);
@@ -53,10 +54,20 @@ void permute_mesh(lms_mesh_s* m, const int32_t* d_perm, cudaStream_t s) {
   const int64_t V = m->V, nnz = m->nnz;
   const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
   DBuf<int32_t> inv(V, s);
+  DBuf<int> moved(1, s);
   LMS_TRY_CUDA(cudaMemsetAsync(inv.p, 0xff, V * sizeof(int32_t), s));
-  k_inverse<<<Gv, 256, 0, s>>>(d_perm, V, inv.p, m->err.p);
+  LMS_TRY_CUDA(cudaMemsetAsync(moved.p, 0, sizeof(int), s));
+  k_inverse<<<Gv, 256, 0, s>>>(d_perm, V, inv.p, m->err.p, moved.p);
   LMS_CHECK_LAUNCH();
   check_err_flag(m, s, "lms_permute");  // nothing modified yet
+  int h_moved = 1;
+  LMS_TRY_CUDA(cudaMemcpyAsync(&h_moved, moved.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  if (!h_moved) {  // the identity (the original ordering): every array stays as it is
+    m->sched.valid = false;
+    soa_changed(m);
+    return;
+  }
 
   for (int a = 0; a < m->dim; ++a) {
     DBuf<double> nx(V, s);

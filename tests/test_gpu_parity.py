@@ -471,6 +471,25 @@ def test_build_csr_host_errors():
     gm.close()
 
 
+def test_permute_identity_is_noop_after_relabel():
+    """lms_permute with the identity (fast path: nothing is moved) after a
+    random relabelling keeps the relabelled mesh; the sweep stays bit-exact."""
+    m = meshgen.grid2d(90, 70, 0.3, seed=71)
+    om = oracle.prepare(m)
+    perm = oracle.order(om, "random", 803)
+    pm = oracle.permute_mesh(om, perm)
+    want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 4)
+    with gpu_mesh(m) as gm:
+        gm.permute(cuda(perm))
+        gm.smooth(2)
+        gm.permute(cuda(np.arange(m.V, dtype=np.int32)))
+        rp, col = gpu_csr(gm)
+        assert np.array_equal(rp, pm["row_ptr"]) and np.array_equal(col, pm["col"])
+        assert np.array_equal(np_(gm.orig_id()), pm["orig_id"])
+        gm.smooth(2)
+        assert bits_equal(gpu_coords(gm), want)
+
+
 @pytest.mark.parametrize("shift", ["1", "0"])
 @pytest.mark.parametrize("shape", [(1024, 45), (500, 90), (1000, 37)])
 def test_colouring_batch_shift(shift, shape, monkeypatch):
