@@ -164,14 +164,16 @@ def kuhn3d(n: int, jitter: float = 0.25, seed: int = MESH_SEED) -> Mesh:
 
 # BASELINE.json configs (index -> generator arguments, sweeps, orderings)
 CONFIGS = {
-    "C1": dict(kind="grid2d", args=dict(nx=100, ny=100, jitter=0.3), sweeps=10, orderings=["random"]),
+    "C1": dict(kind="grid2d", args=dict(nx=100, ny=100, jitter=0.3), sweeps=10, orderings=["random"],
+               desc="2D jittered-grid triangle mesh 100x100"),
     "C2": dict(kind="grid2d", args=dict(nx=1024, ny=1024, jitter=0.3), sweeps=100,
-               orderings=["random", "original", "bfs", "rdr"]),
-    "C3": dict(kind="kuhn3d", args=dict(n=128, jitter=0.25), sweeps=100, orderings=["bfs", "rdr"]),
+               orderings=["random", "original", "bfs", "rdr"], desc="2D jittered-grid triangle mesh 1024x1024"),
+    "C3": dict(kind="kuhn3d", args=dict(n=128, jitter=0.25), sweeps=100, orderings=["bfs", "rdr"],
+               desc="3D Kuhn tetrahedral mesh 128^3"),
     "C4": dict(kind="grid2d", args=dict(nx=4096, ny=4096, jitter=0.3), sweeps=50,
-               orderings=["original", "bfs", "rdr", "random"]),
+               orderings=["original", "bfs", "rdr", "random"], desc="2D jittered-grid triangle mesh 4096x4096"),
     "C5": dict(kind="grid2d", args=dict(nx=16384, ny=8192, jitter=0.3, warp_x2=True), sweeps=20,
-               orderings=["original", "bfs"]),
+               orderings=["original", "bfs"], desc="2D graded (x<-x^2) jittered-grid triangle mesh 16384x8192"),
 }
 
 

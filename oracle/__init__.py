@@ -225,11 +225,16 @@ def permute_mesh(mesh: dict, perm) -> dict:
 
 
 # --------------------------------------------------------------------------- O7-O9
-def smooth(coords, row_ptr, col, colour_arr, C: int, sweeps: int, threads: int = 0):
+def smooth(coords, row_ptr, col, colour_arr, C: int, sweeps: int, threads: int = 0, inplace: bool = False):
     """O7 (threads=0) / O8 (threads>0) -- colour-ordered Gauss-Seidel LMS sweeps,
     Eq. 1 in Alg. 1's loop.  Returns new coordinate arrays
-    (and the thread count used when threads>0)."""
-    X = [np.array(c, dtype=np.float64, copy=True) for c in coords]
+    (and the thread count used when threads>0).  inplace=True smooths the given
+    float64 arrays themselves (no copy; used by the timed baselines)."""
+    if inplace:
+        X = list(coords)
+        assert all(c.dtype == np.float64 and c.flags.c_contiguous for c in X)
+    else:
+        X = [np.array(c, dtype=np.float64, copy=True) for c in coords]
     row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
     col = np.ascontiguousarray(col, dtype=np.int32)
     colour_arr = np.ascontiguousarray(colour_arr, dtype=np.int8)

@@ -235,18 +235,29 @@ lms_status lms_build_csr_host(int32_t dim, int64_t n_vertices, const double* con
     cudaStream_t s2 = side_stream(m->device);
     LMS_TRY_CUDA(cudaEventRecord(ev.a, s));  // the allocations above are stream-ordered on s
     LMS_TRY_CUDA(cudaStreamWaitEvent(s2, ev.a, 0));
-    for (int a = 0; a < dim; ++a)
+    // Once a copy is queued on s2, every exit path (including a throw from a
+    // later copy) orders s after the upload before m's buffers can go back to
+    // s's scratch cache.
+    struct JoinUpload {
+      cudaEvent_t ev;
+      cudaStream_t s, s2;
+      bool armed = false;
+      ~JoinUpload() {
+        if (!armed) return;
+        cudaEventRecord(ev, s2);
+        cudaStreamWaitEvent(s, ev, 0);
+      }
+    } join{ev.b, s, s2};
+    for (int a = 0; a < dim; ++a) {
+      join.armed = true;
       LMS_TRY_CUDA(cudaMemcpyAsync(m->x[a].p, h_coords[a], n_vertices * sizeof(double), cudaMemcpyHostToDevice, s2));
-    LMS_TRY_CUDA(cudaEventRecord(ev.b, s2));
-    try {
-      build_csr_from_elems(m, nullptr, h_fixed == nullptr, s);
-      m->orig_id.alloc(n_vertices, s);
-      fill_iota(m->orig_id.p, n_vertices, s);
-      compute_colouring(m, s);  // colour from orig_id = input label (reading Z2)
-    } catch (...) {
-      cudaStreamWaitEvent(s, ev.b, 0);  // the upload still writes m->x: order the frees after it
-      throw;
     }
+    build_csr_from_elems(m, nullptr, h_fixed == nullptr, s);
+    m->orig_id.alloc(n_vertices, s);
+    fill_iota(m->orig_id.p, n_vertices, s);
+    compute_colouring(m, s);  // colour from orig_id = input label (reading Z2)
+    join.armed = false;
+    LMS_TRY_CUDA(cudaEventRecord(ev.b, s2));
     LMS_TRY_CUDA(cudaStreamWaitEvent(s, ev.b, 0));
     m->n_free = count_free(m, s);
   } catch (...) {
@@ -316,13 +327,15 @@ lms_status lms_mesh_from_csr(int32_t dim, int64_t n_vertices, const double* cons
 
 void lms_mesh_destroy(lms_mesh_t m) {
   if (!m) return;
-  cudaDeviceSynchronize();  // buffers may have been used on any stream
+  DevGuard dg(m);
+  cudaDeviceSynchronize();  // buffers may have been used on any stream of m's device
   delete m;
 }
 
 lms_status lms_order(lms_mesh_t m, lms_order_kind kind, uint64_t seed, int32_t* d_perm, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m || !d_perm) fail(LMS_E_ARG, "NULL handle or perm");
+  DevGuard dg(m);
   cudaStream_t s = (cudaStream_t)stream;
   switch (kind) {
     case LMS_ORDER_ORIGINAL:
@@ -348,6 +361,7 @@ lms_status lms_order(lms_mesh_t m, lms_order_kind kind, uint64_t seed, int32_t* 
 lms_status lms_permute(lms_mesh_t m, const int32_t* d_perm, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m || !d_perm) fail(LMS_E_ARG, "NULL handle or perm");
+  DevGuard dg(m);
   permute_mesh(m, d_perm, (cudaStream_t)stream);
   return LMS_OK;
   LMS_API_END
@@ -356,6 +370,7 @@ lms_status lms_permute(lms_mesh_t m, const int32_t* d_perm, lms_stream_t stream)
 lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   if (sweeps < 0) fail(LMS_E_ARG, "sweeps < 0");
   if (sweeps == 0 || m->n_free == 0) return LMS_OK;
   cudaStream_t s = (cudaStream_t)stream;
@@ -363,6 +378,7 @@ lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream) {
     sync_soa(m, s);
     build_schedule(m, s);
   }
+  m->coords_moved = true;
   run_sweeps(m, sweeps, s);
   return LMS_OK;
   LMS_API_END
@@ -371,6 +387,7 @@ lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream) {
 lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, int32_t lag) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   if (kind != LMS_SCHED_AUTO && kind != LMS_SCHED_S1 && kind != LMS_SCHED_S3 && kind != LMS_SCHED_GZ)
     fail(LMS_E_ARG, "unknown schedule");
   if (kind == LMS_SCHED_GZ && lag > 8) fail(LMS_E_ARG, "GZ: at most 8 sweeps per pass");
@@ -387,6 +404,7 @@ lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, 
 lms_status lms_set_tiling(lms_mesh_t m, lms_tiling_kind kind) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   if (kind != LMS_TILING_AUTO && kind != LMS_TILING_STORAGE && kind != LMS_TILING_SPATIAL)
     fail(LMS_E_ARG, "unknown tiling");
   m->tiling_req = kind;
@@ -398,6 +416,7 @@ lms_status lms_set_tiling(lms_mesh_t m, lms_tiling_kind kind) {
 lms_status lms_schedule_info2(lms_mesh_t m, int32_t* tiling, int64_t* n_tiles, int32_t* max_reach) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   const bool gz = m->sched.valid && m->sched.kind == LMS_SCHED_GZ;
   if (tiling) *tiling = m->sched.valid ? (gz ? (int)LMS_TILING_SPATIAL : m->sched.tiling) : 0;
   if (n_tiles) *n_tiles = m->sched.valid ? (gz ? m->sched.gz_K : m->sched.K) : 0;
@@ -409,6 +428,7 @@ lms_status lms_schedule_info2(lms_mesh_t m, int32_t* tiling, int64_t* n_tiles, i
 lms_status lms_mesh_info(lms_mesh_t m, int64_t* V, int64_t* nnz, int32_t* n_colours, int32_t* dim) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   if (V) *V = m->V;
   if (nnz) *nnz = m->nnz;
   if (n_colours) *n_colours = m->C;
@@ -420,6 +440,7 @@ lms_status lms_mesh_info(lms_mesh_t m, int64_t* V, int64_t* nnz, int32_t* n_colo
 lms_status lms_schedule_info(lms_mesh_t m, int64_t* n_free, int32_t* sched_kind, int32_t* tile, int32_t* lag) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   if (n_free) *n_free = m->n_free;
   if (sched_kind) *sched_kind = m->sched.valid ? m->sched.kind : m->sched_req;
   const bool gz = m->sched.valid && m->sched.kind == LMS_SCHED_GZ;
@@ -432,6 +453,7 @@ lms_status lms_schedule_info(lms_mesh_t m, int64_t* n_free, int32_t* sched_kind,
 lms_status lms_export_coords(lms_mesh_t m, double* const* d_out, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   check_coords(m->dim, d_out);
   sync_soa(m, (cudaStream_t)stream);
   for (int a = 0; a < m->dim; ++a)
@@ -443,10 +465,12 @@ lms_status lms_export_coords(lms_mesh_t m, double* const* d_out, lms_stream_t st
 lms_status lms_import_coords(lms_mesh_t m, const double* const* d_in, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   check_coords(m->dim, d_in);
   for (int a = 0; a < m->dim; ++a)
     LMS_TRY_CUDA(cudaMemcpyAsync(m->x[a].p, d_in[a], m->V * sizeof(double), cudaMemcpyDefault, (cudaStream_t)stream));
   soa_changed(m);
+  m->coords_moved = true;
   return LMS_OK;
   LMS_API_END
 }
@@ -454,6 +478,7 @@ lms_status lms_import_coords(lms_mesh_t m, const double* const* d_in, lms_stream
 lms_status lms_export_csr(lms_mesh_t m, int32_t* d_row_ptr, int32_t* d_col_idx, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
   cudaStream_t s = (cudaStream_t)stream;
   if (d_row_ptr)
     LMS_TRY_CUDA(cudaMemcpyAsync(d_row_ptr, m->row_ptr.p, (m->V + 1) * sizeof(int32_t), cudaMemcpyDefault, s));
@@ -466,6 +491,7 @@ lms_status lms_export_csr(lms_mesh_t m, int32_t* d_row_ptr, int32_t* d_col_idx, 
 lms_status lms_export_colour(lms_mesh_t m, int8_t* d_colour, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m || !d_colour) fail(LMS_E_ARG, "NULL argument");
+  DevGuard dg(m);
   LMS_TRY_CUDA(cudaMemcpyAsync(d_colour, m->colour.p, m->V, cudaMemcpyDefault, (cudaStream_t)stream));
   return LMS_OK;
   LMS_API_END
@@ -474,6 +500,7 @@ lms_status lms_export_colour(lms_mesh_t m, int8_t* d_colour, lms_stream_t stream
 lms_status lms_export_fixed(lms_mesh_t m, uint8_t* d_fixed, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m || !d_fixed) fail(LMS_E_ARG, "NULL argument");
+  DevGuard dg(m);
   LMS_TRY_CUDA(cudaMemcpyAsync(d_fixed, m->fixed.p, m->V, cudaMemcpyDefault, (cudaStream_t)stream));
   return LMS_OK;
   LMS_API_END
@@ -482,6 +509,7 @@ lms_status lms_export_fixed(lms_mesh_t m, uint8_t* d_fixed, lms_stream_t stream)
 lms_status lms_export_orig_id(lms_mesh_t m, int32_t* d_orig_id, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m || !d_orig_id) fail(LMS_E_ARG, "NULL argument");
+  DevGuard dg(m);
   LMS_TRY_CUDA(cudaMemcpyAsync(d_orig_id, m->orig_id.p, m->V * sizeof(int32_t), cudaMemcpyDefault, (cudaStream_t)stream));
   return LMS_OK;
   LMS_API_END
@@ -490,6 +518,7 @@ lms_status lms_export_orig_id(lms_mesh_t m, int32_t* d_orig_id, lms_stream_t str
 lms_status lms_export_elems(lms_mesh_t m, int32_t* d_elems, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m || !d_elems) fail(LMS_E_ARG, "NULL argument");
+  DevGuard dg(m);
   if (!m->k) fail(LMS_E_STATE, "mesh has no elements");
   LMS_TRY_CUDA(cudaMemcpyAsync(d_elems, m->elems.p, m->n_el * m->k * sizeof(int32_t), cudaMemcpyDefault, (cudaStream_t)stream));
   return LMS_OK;
@@ -499,9 +528,15 @@ lms_status lms_export_elems(lms_mesh_t m, int32_t* d_elems, lms_stream_t stream)
 lms_status lms_export_quality(lms_mesh_t m, double* d_quality, lms_stream_t stream) {
   LMS_API_BEGIN
   if (!m || !d_quality) fail(LMS_E_ARG, "NULL argument");
+  DevGuard dg(m);
   cudaStream_t s = (cudaStream_t)stream;
-  compute_quality(m, s);
-  LMS_TRY_CUDA(cudaMemcpyAsync(d_quality, m->quality.p, m->V * sizeof(double), cudaMemcpyDefault, s));
+  if (m->quality_external) {
+    LMS_TRY_CUDA(cudaMemcpyAsync(d_quality, m->quality.p, m->V * sizeof(double), cudaMemcpyDefault, s));
+  } else {
+    DBuf<double> q(m->V, s);
+    compute_quality(m, q.p, s);
+    LMS_TRY_CUDA(cudaMemcpyAsync(d_quality, q.p, m->V * sizeof(double), cudaMemcpyDefault, s));
+  }
   return LMS_OK;
   LMS_API_END
 }

@@ -35,7 +35,12 @@ UserAlloc& user() {
 }
 struct Cache {
   std::mutex mu;
-  std::unordered_map<void*, size_t> live;                         // block -> bytes
+  // block -> (bytes, owning device); bytes 0 = the caller's allocator.  The
+  // device is recorded at allocation: a block may be freed while another
+  // device is current (a Mesh collected by Python, one process driving several
+  // GPUs), and it must go back to its own device's bucket and pool.
+  struct Live { size_t bytes; int dev; };
+  std::unordered_map<void*, Live> live;
   // (device, stream, bytes) -> blocks: the legacy default stream has the same
   // handle on every device, so the device is part of the key
   std::map<std::tuple<int, cudaStream_t, size_t>, std::vector<void*>> free_;
@@ -72,7 +77,7 @@ void* ws_alloc(size_t bytes, cudaStream_t s) {
     void* p = user().alloc(rb, (lms_stream_t)s, user().ctx);
     if (!p) fail(LMS_E_NOMEM, "lms_set_allocator: the caller's allocator returned NULL");
     std::lock_guard<std::mutex> g(c.mu);
-    c.live[p] = 0;  // 0 = the caller's block
+    c.live[p] = Cache::Live{0, dev};  // 0 = the caller's block
     return p;
   }
   {
@@ -91,7 +96,7 @@ void* ws_alloc(size_t bytes, cudaStream_t s) {
         void* p = it->second.back();
         it->second.pop_back();
         c.cached -= std::get<2>(it->first);
-        c.live[p] = std::get<2>(it->first);
+        c.live[p] = Cache::Live{std::get<2>(it->first), dev};
         if (it->second.empty()) c.free_.erase(it);
         return p;
       }
@@ -106,7 +111,7 @@ void* ws_alloc(size_t bytes, cudaStream_t s) {
   }
   LMS_TRY_CUDA(e);
   std::lock_guard<std::mutex> g(c.mu);
-  c.live[p] = rb;
+  c.live[p] = Cache::Live{rb, dev};
   return p;
 }
 
@@ -115,20 +120,21 @@ void ws_free(void* p, cudaStream_t s) {
   Cache& c = cache();
   std::lock_guard<std::mutex> g(c.mu);
   auto it = c.live.find(p);
-  const size_t b = it == c.live.end() ? 0 : it->second;
-  const bool mine = it != c.live.end() && it->second != 0;
-  if (it != c.live.end() && it->second == 0) {  // the caller's allocator
-    c.live.erase(it);
-    if (user().free) user().free(p, (lms_stream_t)s, user().ctx);
-    return;
-  }
-  if (it != c.live.end()) c.live.erase(it);
-  if (!mine || !c.cap || b > c.cap) {
+  if (it == c.live.end()) {  // not ours (never expected): hand it to the pool
     cudaFreeAsync(p, s);
     return;
   }
-  int dev = 0;
-  cudaGetDevice(&dev);
+  const size_t b = it->second.bytes;
+  const int dev = it->second.dev;
+  c.live.erase(it);
+  if (b == 0) {  // the caller's allocator
+    if (user().free) user().free(p, (lms_stream_t)s, user().ctx);
+    return;
+  }
+  if (!c.cap || b > c.cap) {
+    free_on(dev, s, p);
+    return;
+  }
   c.free_[std::make_tuple(dev, s, b)].push_back(p);
   c.cached += b;
   while (c.cached > c.cap && !c.free_.empty()) {  // over the cap: blocks back to the pool

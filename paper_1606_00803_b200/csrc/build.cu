@@ -459,8 +459,7 @@ __global__ void k_mark_untouched(const unsigned long long* __restrict__ keys, in
   }
 }
 
-void compute_quality(lms_mesh_s* m, cudaStream_t s) {
-  if (m->quality_external) return;
+void compute_quality(lms_mesh_s* m, double* out, cudaStream_t s) {
   if (!m->k) fail(LMS_E_STATE, "quality needs elements (or a quality given to lms_mesh_from_csr)");
   sync_soa(m, s);
   const int64_t n_el = m->n_el, V = m->V;
@@ -484,13 +483,23 @@ void compute_quality(lms_mesh_s* m, cudaStream_t s) {
     DBuf<char> tmp(tb, s);
     LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, sorted.p, n, 0, eb + vb, s));
   }
-  if (m->quality.n != (size_t)V) m->quality.alloc(V, s);
   k_mark_untouched<<<Gn, 256, 0, s>>>(sorted.p, n, eb, V, m->err.p);
   LMS_CHECK_LAUNCH();
-  k_vertex_quality<<<Gn, 256, 0, s>>>(sorted.p, n, eb, qe.p, m->quality.p, m->err.p);
+  k_vertex_quality<<<Gn, 256, 0, s>>>(sorted.p, n, eb, qe.p, out, m->err.p);
   LMS_CHECK_LAUNCH();
   check_err_flag(m, s, "quality");
+}
+
+const double* initial_quality(lms_mesh_s* m, cudaStream_t s) {
+  if (m->has_quality) return m->quality.p;  // cached, or given to lms_mesh_from_csr (permuted with the mesh)
+  if (m->coords_moved)
+    fail(LMS_E_STATE, "RDR orders by the INITIAL vertex qualities (P:262-265, reading Z13), but the coordinates "
+                      "changed since the build: call lms_order before lms_smooth / lms_import_coords");
+  DBuf<double> q(m->V, s);
+  compute_quality(m, q.p, s);
+  m->quality = std::move(q);
   m->has_quality = true;
+  return m->quality.p;
 }
 
 // -------------------------------------------------------------- per-row sort

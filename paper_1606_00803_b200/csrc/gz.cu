@@ -829,25 +829,43 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "r"(a), "r"(parity)
         : "memory");
 }
-// Watchdog for every wait of k_sweep_gz: a wait that outlives ~2^25 polls
-// (seconds) raises LMS_E_CUDA in the handle's error flag and every waiter
-// then leaves the kernel, so a schedule bug surfaces as an error instead of a
-// hung GPU.
+// Watchdog for every wait of k_sweep_gz: a single wait that lasts longer
+// than GZ_WAIT_NS of wall time (%globaltimer, checked every 256 polls; the
+// clock restarts at each wait's start()) raises LMS_E_CUDA in the handle's
+// error flag and every waiter then leaves the kernel, so a schedule bug
+// surfaces as an error instead of a hung GPU.  The deadline is per wait, not
+// per pass: a long pass (a large mesh, slow orderings, a sanitizer or ncu
+// replay) never trips it while its waits keep completing.
+constexpr unsigned long long GZ_WAIT_NS = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 struct GzGuard {
   int* gabort;          // global error flag (the handle's)
   volatile int* sabort; // CTA-local copy
-  long long n = 0;
-  __device__ bool ok() {
-    ++n;
-    if ((n & 255) == 0 && (*sabort || *(volatile int*)gabort)) {
+  unsigned n = 0;
+  unsigned long long t0 = 0;
+  __device__ void start() { n = 0; t0 = 0; }
+  __device__ bool check() {
+    if (*sabort || *(volatile int*)gabort) {
       *sabort = 1;
       return false;
     }
-    if (n > (1ll << 25)) {
+    const unsigned long long t = gtimer();
+    if (t0 == 0) {
+      t0 = t;
+    } else if (t - t0 > GZ_WAIT_NS) {
       atomicCAS(gabort, 0, (int)LMS_E_CUDA);
       *sabort = 1;
       return false;
     }
+    return true;
+  }
+  __device__ bool ok() {
+    ++n;
+    if ((n & 255) == 0 && !check()) return false;
     __nanosleep(n < 64 ? 20 : 128);
     return true;
   }
@@ -855,20 +873,12 @@ struct GzGuard {
   // until the phase completes (or a time limit), so no sleep on top of it
   __device__ bool ok_spin() {
     ++n;
-    if ((n & 255) == 0 && (*sabort || *(volatile int*)gabort)) {
-      *sabort = 1;
-      return false;
-    }
-    if (n > (1ll << 25)) {
-      atomicCAS(gabort, 0, (int)LMS_E_CUDA);
-      *sabort = 1;
-      return false;
-    }
-    return true;
+    return (n & 255) != 0 || check();
   }
 };
 __device__ __forceinline__ bool mbar_wait_g(uint64_t* b, uint32_t parity, GzGuard& g) {
   const uint32_t a = smem_u32(b);
+  g.start();
   for (;;) {
     uint32_t done = 0;
     asm volatile(
@@ -1408,9 +1418,11 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
         rring + ((size_t)slot * L.BS + (kc & (L.BS - 1))) * L.rec_bytes;
     int alive = 1;
     if (lane == 0) {
+      guard.start();
       while (alive && rbat[slot] != bat) alive = guard.ok_spin();
       alive = alive && mbar_wait_g(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u, guard);
       if (alive && !tile_ready) {  // the region of the item's tile
+        guard.start();
         while (alive && buf_tile[tb & 0xffff] != i) alive = guard.ok();
         alive = alive && mbar_wait_g(full + (tb & 0xffff), (uint32_t)(tb >> 16), guard);
       }
@@ -1454,17 +1466,22 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
 #pragma unroll
       for (int u = 0; u < UPL; ++u) {
         const int dep = (int)(r[u].pb >> 16);
-        if (dep != 0xffff && dep >= item0)
+        if (dep != 0xffff && dep >= item0) {
+          guard.start();
           while (alive && flags[dep] != i + 1) alive = guard.ok();
+        }
         const int d2 = d2v[u];
-        if (d2 != 0xffff && d2 >= item0)
+        if (d2 != 0xffff && d2 >= item0) {
+          guard.start();
           while (alive && flags[d2] != i + 1) alive = guard.ok();
+        }
       }
     } else if (lane == 0) {
       const uint32_t* hdr = reinterpret_cast<const uint32_t*>(buf);
       const int s0 = max(sg - C, j0 * C);
       for (int s2 = s0; s2 < sg && alive; ++s2) {
         const int need = (int)(hdr[4 + s2 + 1] - hdr[4 + s2]);
+        guard.start();
         while (alive && *(volatile int*)(cnt + s2) != need) alive = guard.ok();
       }
     }

@@ -59,11 +59,13 @@ extern "C" {
 lms_status lms_smooth_colour(lms_mesh_t m, int32_t colour, lms_stream_t stream) {
   try {
     if (!m) fail(LMS_E_ARG, "NULL handle");
+    DevGuard dg(m);
     if (colour < 0 || colour >= m->C) fail(LMS_E_ARG, "colour out of range");
     if (m->n_free == 0) return LMS_OK;
     cudaStream_t s = (cudaStream_t)stream;
     sync_soa(m, s);
     if (!m->sched.valid) build_schedule(m, s);
+    m->coords_moved = true;
     run_colour_stage(m, colour, s);
     return LMS_OK;
   } catch (const Err& e) {
@@ -75,6 +77,7 @@ lms_status lms_smooth_colour(lms_mesh_t m, int32_t colour, lms_stream_t stream) 
 lms_status lms_gather_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, double* d_out, lms_stream_t stream) {
   try {
     if (!m || (n > 0 && (!d_idx || !d_out)) || n < 0) fail(LMS_E_ARG, "bad argument");
+    DevGuard dg(m);
     if (n == 0) return LMS_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const unsigned G = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
@@ -95,6 +98,7 @@ lms_status lms_scatter_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, con
                               lms_stream_t stream) {
   try {
     if (!m || (n > 0 && (!d_idx || !d_in)) || n < 0) fail(LMS_E_ARG, "bad argument");
+    DevGuard dg(m);
     if (n == 0) return LMS_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const unsigned G = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
@@ -108,6 +112,7 @@ lms_status lms_scatter_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, con
       LMS_CHECK_LAUNCH();
     }
     if (m->aos_state == 0) soa_changed(m);
+    m->coords_moved = true;
     return LMS_OK;
   } catch (const Err& e) {
     set_error(e.msg);

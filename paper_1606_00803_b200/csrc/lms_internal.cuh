@@ -189,14 +189,28 @@ struct lms_mesh_s {
   lms::DBuf<int32_t> orig_id;
   lms::DBuf<int32_t> elems;
   lms::DBuf<double> quality;   // valid if has_quality
-  bool has_quality = false;    // externally supplied (from_csr) or cached
+  bool has_quality = false;    // m->quality holds the INITIAL qualities (RDR input)
   bool quality_external = false;
+  bool coords_moved = false;   // coordinates changed since the build (smooth / import)
   int sched_req = LMS_SCHED_AUTO, tile_req = 0, lag_req = 0, tiling_req = LMS_TILING_AUTO;
   lms::Schedule sched;
   lms::DBuf<int> err;          // device error flag
 };
 
 namespace lms {
+
+// Makes the handle's device current for the scope of an API call (and
+// restores the caller's): buffers, pools and streams belong to m->device.
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const lms_mesh_s* m) {
+    if (!m) return;
+    if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; return; }
+    if (prev == m->device) prev = -1;
+    else cudaSetDevice(m->device);
+  }
+  ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
 
 // Device-side error flag helpers (error codes are lms_status values).
 __device__ __forceinline__ void raise_err(int* flag, int code) { atomicCAS(flag, 0, code); }
@@ -212,7 +226,10 @@ inline unsigned grid_for(int64_t n, int block) {
 // Pipeline pieces (implemented in build.cu, colour.cu, order.cu, permute.cu, smooth.cu)
 void build_csr_from_elems(lms_mesh_s* m, const int32_t* d_elems, bool want_boundary, cudaStream_t s);
 void compute_colouring(lms_mesh_s* m, cudaStream_t s);
-void compute_quality(lms_mesh_s* m, cudaStream_t s);
+// q_v of the CURRENT coordinates into out[V] (A4)
+void compute_quality(lms_mesh_s* m, double* out, cudaStream_t s);
+// the initial qualities RDR orders by (reading Z13), cached in m->quality
+const double* initial_quality(lms_mesh_s* m, cudaStream_t s);
 void order_random(lms_mesh_s* m, uint64_t seed, int32_t* d_perm, cudaStream_t s);
 void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s);
 void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s);

@@ -255,14 +255,14 @@ __global__ void k_unsorted_flags(const uint8_t* __restrict__ sorted, int64_t V, 
 
 void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s) {
   const int64_t V = m->V, nnz = m->nnz;
-  compute_quality(m, s);
+  const double* q = initial_quality(m, s);
   const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
   // rows presorted by (q, label): stable segmented sort of (q bits, col) pairs
   DBuf<int32_t> scol(nnz, s);
   {
     DBuf<unsigned long long> k1(nnz, s), k2(nnz, s);
     const unsigned Gn = grid_for(nnz, 256) > 8192 ? 8192 : grid_for(nnz, 256);
-    k_row_qkeys<<<Gn, 256, 0, s>>>(m->col.p, nnz, m->quality.p, k1.p);
+    k_row_qkeys<<<Gn, 256, 0, s>>>(m->col.p, nnz, q, k1.p);
     LMS_CHECK_LAUNCH();
     size_t tb = 0;
     LMS_TRY_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, k1.p, k2.p, m->col.p, scol.p, nnz, V,
@@ -279,7 +279,7 @@ void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s) {
     DBuf<int32_t> ids(V, s);
     DBuf<int> n(1, s);
     LMS_TRY_CUDA(cudaMemsetAsync(n.p, 0, sizeof(int), s));
-    k_free_qkeys<<<Gv, 256, 0, s>>>(m->fixed.p, m->quality.p, V, k1.p, ids.p, n.p);
+    k_free_qkeys<<<Gv, 256, 0, s>>>(m->fixed.p, q, V, k1.p, ids.p, n.p);
     LMS_CHECK_LAUNCH();
     size_t tb = 0;
     LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, k1.p, k2.p, ids.p, outer.p, V, 0, 64, s));
