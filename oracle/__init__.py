@@ -68,6 +68,8 @@ def lib():
         L.o_smooth.argtypes = [i32, i64, P, P, P, P, i32, i32]
         L.o_smooth_omp.argtypes = [i32, i64, P, P, P, P, i32, i32, i32]
         L.o_smooth_partitioned.argtypes = [i32, i64, P, P, P, P, i32, i32, i32, P]
+        L.o_smooth_jacobi.argtypes = [i32, i64, P, P, P, P, i32]
+        L.o_smooth_seq.argtypes = [i32, i64, P, P, P, P, i32]
         L.o_free.argtypes = [P]
         _lib = L
     return _lib
@@ -293,3 +295,81 @@ def order(mesh: dict, kind: str, seed: int = 0) -> np.ndarray:
             q = quality(mesh["coords"], mesh["elems"])
         return order_rdr(mesh["row_ptr"], mesh["col"], mesh["fixed"], q)
     raise ValueError(kind)
+
+
+# --------------------------------------------------------------------------- N3 schedule variants
+def smooth_jacobi(coords, row_ptr, col, fixed, sweeps: int):
+    """N3 Jacobi: every free vertex from the previous sweep's
+    snapshot (Eq. 1; CSR-order sums, IEEE division)."""
+    X = [np.array(c, dtype=np.float64, copy=True) for c in coords]
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    fixed = np.ascontiguousarray(fixed, dtype=np.uint8)
+    _chk(lib().o_smooth_jacobi(len(X), X[0].shape[0], _ptrs(X), _p(row_ptr), _p(col), _p(fixed), sweeps),
+         "o_smooth_jacobi")
+    return X
+
+
+def smooth_seq(coords, row_ptr, col, fixed, sweeps: int):
+    """N3 Alg. 1 literally: storage-order, in-place Gauss-Seidel."""
+    X = [np.array(c, dtype=np.float64, copy=True) for c in coords]
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    fixed = np.ascontiguousarray(fixed, dtype=np.uint8)
+    _chk(lib().o_smooth_seq(len(X), X[0].shape[0], _ptrs(X), _p(row_ptr), _p(col), _p(fixed), sweeps),
+         "o_smooth_seq")
+    return X
+
+
+# --------------------------------------------------------------------------- N1 convergence loop
+def global_quality_exact(q_v) -> float:
+    """Alg. 1 lines 4-8: Global_quality = (1/|V|) * sum_i q_{V[i]},
+    with the sum taken EXACTLY and rounded once (math.fsum is correctly
+    rounded), then one IEEE division by |V| (reading Z24: the value
+    cannot depend on the storage order, so an ordering cannot change it)."""
+    q = np.asarray(q_v, dtype=np.float64)
+    return float(np.float64(exact_sum(q)) / np.float64(q.shape[0]))
+
+
+def exact_sum(a) -> float:
+    """The exact sum of float64 values rounded once to nearest-even (math.fsum)."""
+    import math
+    return math.fsum(np.asarray(a, dtype=np.float64).tolist())
+
+
+STOP_GOAL, STOP_CONVERGED, STOP_MAX = 1, 2, 3
+
+
+def smooth_until(coords, mesh: dict, goal: float, eps: float, max_sweeps: int, method: str = "colour"):
+    """N1, Alg. 1's outer loop with the paper's stopping rule (P:517-519,
+    "if the quality has improved by less than this criterion, the execution
+    stops") and a maximum iteration count, step by step:
+        Q[0] = Global_quality(X)
+        k = 0
+        loop: if Q[k] >= goal: stop (goal)          -- the while condition
+              if k == max_sweeps: stop (max)
+              one sweep; k += 1; Q[k] = Global_quality(X)   -- quality per iteration
+              if Q[k] - Q[k-1] < eps: stop (converged)
+    `method`: "colour" (the colour-GS schedule, reading Z1), "jacobi" or "seq" (N3).
+    Returns (X, Q list of length k + 1, stop reason)."""
+    X = [np.array(c, dtype=np.float64, copy=True) for c in coords]
+    el = mesh["elems"]
+    qs = [global_quality_exact(quality(X, el))]
+    k = 0
+    while True:
+        if qs[k] >= goal:
+            return X, qs, STOP_GOAL
+        if k == max_sweeps:
+            return X, qs, STOP_MAX
+        if method == "colour":
+            X = smooth(X, mesh["row_ptr"], mesh["col"], mesh["colour"], mesh["C"], 1)
+        elif method == "jacobi":
+            X = smooth_jacobi(X, mesh["row_ptr"], mesh["col"], mesh["fixed"], 1)
+        elif method == "seq":
+            X = smooth_seq(X, mesh["row_ptr"], mesh["col"], mesh["fixed"], 1)
+        else:
+            raise ValueError(method)
+        k += 1
+        qs.append(global_quality_exact(quality(X, el)))
+        if qs[k] - qs[k - 1] < eps:
+            return X, qs, STOP_CONVERGED

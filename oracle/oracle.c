@@ -30,7 +30,11 @@
  *   o_smooth_omp         same sweep, OpenMP static split per colour
  *   o_smooth_partitioned P contiguous parts with ghost copies refreshed after
  *                        every colour (multi-GPU replay; reading Z22)
- *   o_global_quality     Alg. 1 Global_quality = (1/|V|) sum q_v
+ *   o_global_quality     Alg. 1 Global_quality = (1/|V|) sum q_v,
+ *                        left to right (the exactly rounded sum used by the
+ *                        convergence loop is oracle/__init__.py global_quality_exact)
+ *   o_smooth_jacobi      N3: Jacobi variant, snapshot reads
+ *   o_smooth_seq         N3: Alg. 1 literally, storage-order in-place GS
  *
  * Parity pins for every function live in tests/test_oracle_*.py.
  *
@@ -540,5 +544,54 @@ int o_smooth_partitioned(int32_t dim, int64_t V, double* const* X, const int64_t
             for (int a = 0; a < dim; ++a) X[a][v] = priv[p * 3 + a][v];
     for (int32_t p = 0; p < P; ++p) for (int a = 0; a < dim; ++a) free(priv[p * 3 + a]);
     free(priv);
+    return O_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* N3: Jacobi sweep ("reads all neighbor positions from the
+ * start-of-iteration snapshot"): every free vertex moves to the mean of its
+ * neighbours' PREVIOUS-sweep coordinates (Eq. 1), CSR-order sums,
+ * IEEE division; fixed vertices (colour < 0) keep their value.  An explicitly
+ * named schedule variant (reading Z1): NOT the colour-GS result.             */
+int o_smooth_jacobi(int32_t dim, int64_t V, double* const* X, const int64_t* row_ptr, const int32_t* col,
+                    const uint8_t* fixed, int32_t sweeps) {
+    if (sweeps < 0 || dim < 1 || dim > 3) return O_E_ARG;
+    double* old = (double*)malloc((size_t)(V > 0 ? V : 1) * sizeof(double));
+    if (!old) return O_E_NOMEM;
+    for (int32_t s = 0; s < sweeps; ++s)
+        for (int a = 0; a < dim; ++a) {
+            memcpy(old, X[a], (size_t)V * sizeof(double));          /* the snapshot */
+            for (int64_t v = 0; v < V; ++v) {
+                if (fixed[v]) continue;
+                int64_t b = row_ptr[v], e = row_ptr[v + 1];
+                if (e == b) { free(old); return O_E_ISOLATED; }
+                double acc = old[col[b]];
+                for (int64_t i = b + 1; i < e; ++i) acc = acc + old[col[i]];
+                X[a][v] = acc / (double)(e - b);
+            }
+        }
+    free(old);
+    return O_OK;
+}
+
+/* N3: Alg. 1 literally: "for i in {interior vertices}: smooth V[i]
+ * using Eq. 1", sequentially and in place, in STORAGE order -- each vertex
+ * reads the current values, so the result depends on the ordering (reading
+ * Z21).  CPU only (the GPU cannot run a sequential loop); used to compare
+ * convergence with the colour schedule.                                       */
+int o_smooth_seq(int32_t dim, int64_t V, double* const* X, const int64_t* row_ptr, const int32_t* col,
+                 const uint8_t* fixed, int32_t sweeps) {
+    if (sweeps < 0 || dim < 1 || dim > 3) return O_E_ARG;
+    for (int32_t s = 0; s < sweeps; ++s)
+        for (int64_t v = 0; v < V; ++v) {
+            if (fixed[v]) continue;
+            int64_t b = row_ptr[v], e = row_ptr[v + 1];
+            if (e == b) return O_E_ISOLATED;
+            for (int a = 0; a < dim; ++a) {
+                double acc = X[a][col[b]];
+                for (int64_t i = b + 1; i < e; ++i) acc = acc + X[a][col[i]];
+                X[a][v] = acc / (double)(e - b);
+            }
+        }
     return O_OK;
 }
