@@ -63,10 +63,13 @@ typedef enum {
     LMS_SCHED_AUTO = 0,     /* pick per mesh: GZ for 2D meshes with <= 8 colours, else S1 */
     LMS_SCHED_S1 = 1,       /* one launch per colour (CUDA-graph captured sweep) */
     LMS_SCHED_S3 = 3,       /* persistent colour-pipelined sweep with per-tile progress flags */
-    LMS_SCHED_GZ = 4        /* ghost-zone tiled sweep: one launch per P sweeps; each CTA stages a
+    LMS_SCHED_GZ = 4,       /* ghost-zone tiled sweep: one launch per P sweeps; each CTA stages a
                                spatial tile plus every vertex within C*P hops in shared memory,
                                runs the P sweeps' colour stages there and writes its owned vertices
                                to a second coordinate buffer (no inter-CTA synchronisation) */
+    LMS_SCHED_JACOBI = 5    /* N3 VARIANT, not the colour-GS result: every free vertex moves to the mean
+                               of its neighbours' PREVIOUS-sweep coordinates (Eq. 1,
+                               CSR-order sums, IEEE division), double-buffered; for convergence studies */
 } lms_schedule_kind;
 
 /* ---------------------------------------------------------------------------
@@ -157,7 +160,8 @@ lms_status lms_permute(lms_mesh_t m, const int32_t* d_perm, lms_stream_t stream)
  * P:244-251, inside Alg. 1's loop over interior vertices, under
  * the colour-ordered Gauss-Seidel schedule of DESIGN.md reading Z1).  Fixed
  * vertices never move.  sweeps == 0 is a no-op; sweeps < 0 -> LMS_E_ARG.
- * The schedule (S1/S3) is chosen by lms_set_schedule; all are bit-identical. */
+ * The schedule (S1/S3/GZ) is chosen by lms_set_schedule; all are bit-identical.
+ * LMS_SCHED_JACOBI instead runs the named Jacobi variant (a different method). */
 lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream);
 
 /* lms_set_schedule -- choose the sweep kernel.  tile: vertices per tile
@@ -214,6 +218,38 @@ lms_status lms_smooth_colour(lms_mesh_t m, int32_t colour, lms_stream_t stream);
 lms_status lms_gather_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, double* d_out, lms_stream_t stream);
 lms_status lms_scatter_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, const double* d_in,
                               lms_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Convergence-driven LMS: Alg. 1's outer loop.
+ *
+ * lms_global_quality -- Global_quality of the CURRENT coordinates (Alg. 1 lines
+ *  4-8): q_e = edge-length ratio of each element, q_v =
+ *  mean of q_e over the elements containing v in ascending element order
+ *  (P:234-236), Global_quality = RN(exact sum of q_v) / |V| -- the vertex sum
+ *  is exact and rounded once (reading Z24), so it does not depend on
+ *  the storage order.  *h_quality (host) receives it; d_vertex_quality
+ *  (device double[V], or NULL) receives q_v.  Synchronises `stream`.  Needs
+ *  elements (LMS_E_STATE for a CSR-only handle); LMS_E_DEGENERATE on an
+ *  element with all edge lengths zero.  The vertex -> element incidence is
+ *  built on first use and kept until the mesh is relabelled.
+ *
+ * lms_smooth_until -- the loop, with the paper's stopping rule and
+ *  an iteration cap:
+ *      Q[0] = Global_quality;  k = 0
+ *      loop: if Q[k] >= goal: stop (LMS_STOP_GOAL)
+ *            if k == max_sweeps: stop (LMS_STOP_MAX)
+ *            one sweep of the current schedule (lms_smooth(m, 1)); k += 1
+ *            Q[k] = Global_quality
+ *            if Q[k] - Q[k-1] < eps: stop (LMS_STOP_CONVERGED)
+ *  *sweeps_run = k; h_quality_history (host double[max_sweeps + 1], or NULL)
+ *  receives Q[0..k]; *stop_reason one of lms_stop_reason.  One host
+ *  synchronisation per sweep (the stop decision is taken on the host, on the
+ *  same value the oracle computes).  Errors as lms_smooth / lms_global_quality;
+ *  max_sweeps < 0 -> LMS_E_ARG. */
+typedef enum { LMS_STOP_GOAL = 1, LMS_STOP_CONVERGED = 2, LMS_STOP_MAX = 3 } lms_stop_reason;
+lms_status lms_global_quality(lms_mesh_t m, double* h_quality, double* d_vertex_quality, lms_stream_t stream);
+lms_status lms_smooth_until(lms_mesh_t m, double goal, double eps, int32_t max_sweeps, int32_t* sweeps_run,
+                            double* h_quality_history, int32_t* stop_reason, lms_stream_t stream);
 
 /* Thread-local message for the last non-OK status of this thread. */
 const char* lms_last_error(void);

@@ -15,7 +15,8 @@ from . import build_lib
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 ORDERINGS = {"original": 0, "random": 1, "bfs": 2, "rdr": 3}
-SCHEDULES = {"auto": 0, "s1": 1, "s3": 3, "gz": 4}
+SCHEDULES = {"auto": 0, "s1": 1, "s3": 3, "gz": 4, "jacobi": 5}
+STOP_REASONS = {1: "goal", 2: "converged", 3: "max_sweeps"}
 SCHED_NAMES = {v: k for k, v in SCHEDULES.items()}
 TILINGS = {"auto": 0, "storage": 1, "spatial": 2}
 TILING_NAMES = {v: k for k, v in TILINGS.items()}
@@ -28,7 +29,8 @@ EXPORTS = ["lms_build_csr", "lms_build_csr_host", "lms_mesh_from_csr", "lms_mesh
            "lms_set_schedule", "lms_mesh_info", "lms_schedule_info", "lms_export_coords", "lms_import_coords",
            "lms_export_csr", "lms_export_colour", "lms_export_fixed", "lms_export_orig_id", "lms_export_elems",
            "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_cache_release", "lms_set_allocator", "lms_set_tiling", "lms_schedule_info2",
-           "lms_smooth_colour", "lms_gather_coords", "lms_scatter_coords"]
+           "lms_smooth_colour", "lms_gather_coords", "lms_scatter_coords",
+           "lms_global_quality", "lms_smooth_until"]
 
 
 class LMSError(RuntimeError):
@@ -76,6 +78,9 @@ def load_library(build: bool = True):
         "lms_smooth_colour": [P, i32, P],
         "lms_gather_coords": [P, P, i64, P, P],
         "lms_scatter_coords": [P, P, i64, P, P],
+        "lms_global_quality": [P, ct.POINTER(ct.c_double), P, P],
+        "lms_smooth_until": [P, ct.c_double, ct.c_double, i32, ct.POINTER(i32), ct.POINTER(ct.c_double),
+                             ct.POINTER(i32), P],
         "lms_last_error": [],
         "lms_kernel_launches": [],
         "lms_cache_release": [],
@@ -291,6 +296,23 @@ class Mesh:
 
     def smooth(self, sweeps: int, stream=None):
         _check(lib().lms_smooth(self._h, sweeps, _stream(stream)), "lms_smooth")
+
+    def global_quality(self, vertex_quality: torch.Tensor | None = None, stream=None) -> float:
+        """lms_global_quality: Alg. 1's Global_quality of the current coordinates
+        (exact vertex sum rounded once, / |V|); optionally q_v into vertex_quality."""
+        q = ct.c_double()
+        vq = _dev(vertex_quality, torch.float64, self.V, "vertex_quality") if vertex_quality is not None else None
+        _check(lib().lms_global_quality(self._h, ct.byref(q), vq, _stream(stream)), "lms_global_quality")
+        return q.value
+
+    def smooth_until(self, goal: float = 1.0, eps: float = 5e-6, max_sweeps: int = 1000, stream=None):
+        """lms_smooth_until: Alg. 1's loop with the paper's stopping rule.
+        Returns (sweeps run, quality history Q[0..k], stop reason name)."""
+        k, why = ct.c_int32(), ct.c_int32()
+        hist = (ct.c_double * (max_sweeps + 1))()
+        _check(lib().lms_smooth_until(self._h, goal, eps, max_sweeps, ct.byref(k), hist, ct.byref(why),
+                                      _stream(stream)), "lms_smooth_until")
+        return k.value, [hist[i] for i in range(k.value + 1)], STOP_REASONS[why.value]
 
     def smooth_colour(self, colour: int, stream=None):
         """lms_smooth_colour: one colour stage of the sweep."""

@@ -388,7 +388,8 @@ lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, 
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
   DevGuard dg(m);
-  if (kind != LMS_SCHED_AUTO && kind != LMS_SCHED_S1 && kind != LMS_SCHED_S3 && kind != LMS_SCHED_GZ)
+  if (kind != LMS_SCHED_AUTO && kind != LMS_SCHED_S1 && kind != LMS_SCHED_S3 && kind != LMS_SCHED_GZ &&
+      kind != LMS_SCHED_JACOBI)
     fail(LMS_E_ARG, "unknown schedule");
   if (kind == LMS_SCHED_GZ && lag > 8) fail(LMS_E_ARG, "GZ: at most 8 sweeps per pass");
   if (tile < 0 || lag < 0) fail(LMS_E_ARG, "tile/lag < 0");

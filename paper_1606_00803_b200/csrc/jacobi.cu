@@ -1,0 +1,92 @@
+// jacobi.cu -- the Jacobi sweep, an explicitly named schedule variant
+// (LMS_SCHED_JACOBI).
+//
+// Every free vertex moves to the mean of its neighbours' coordinates from the
+// PREVIOUS sweep (Eq. 1): X'[v] = (sum over the CSR row of
+// X[u], in CSR order) / deg(v), IEEE binary64 adds and division, no FMA.  Fixed
+// vertices keep their value.  This is NOT the colour-ordered Gauss-Seidel
+// result of lms_smooth's other schedules (reading Z1): it is offered
+// to compare convergence (the paper's loop is in place).
+//
+// Kernel: one CTA of 256 threads per 256 consecutive vertices.  The CTA's
+// column indices (one contiguous CSR range) are staged into shared memory by
+// coalesced 16-byte loads, so the index stream is read once at full width;
+// each thread then gathers its neighbours' (x, y[, z]) from the previous
+// buffer through the read-only path and writes the new value to the other
+// buffer (ping-pong; both buffers hold the fixed vertices).  Bytes per sweep:
+// row_ptr + col read once, coordinates read (gathers mostly hit L1/L2 for
+// banded orderings), free coordinates written once -- B_sweep of SURVEY 8(d).
+#include "lms_internal.cuh"
+
+namespace lms {
+
+constexpr int JB = 256;          // vertices (threads) per CTA
+constexpr int JCAP = JB * 12;    // staged column indices per CTA (avg degree <= 12); longer ranges read global
+
+template <int DIM>
+__global__ void __launch_bounds__(JB) k_jacobi(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                               const uint8_t* __restrict__ fixed, int64_t V,
+                                               const double* __restrict__ x0, const double* __restrict__ y0,
+                                               const double* __restrict__ z0, double* __restrict__ x1,
+                                               double* __restrict__ y1, double* __restrict__ z1) {
+  __shared__ __align__(16) int32_t sc[JCAP + 8];
+  for (int64_t base = (int64_t)blockIdx.x * JB; base < V; base += (int64_t)gridDim.x * JB) {
+    const int64_t v = base + threadIdx.x;
+    const int64_t vend = base + JB < V ? base + JB : V;
+    const int32_t c0 = rp[base], c1 = rp[vend];
+    const int32_t a0 = c0 & ~3;  // 16-byte aligned start
+    const bool staged = c1 - a0 <= JCAP;
+    __syncthreads();  // the previous chunk's reads of sc are done
+    if (staged) {
+      const int n4 = (c1 - a0 + 3) >> 2;
+      const int4* src = reinterpret_cast<const int4*>(col + a0);
+      for (int i = threadIdx.x; i < n4; i += JB) reinterpret_cast<int4*>(sc)[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    if (v < V && !fixed[v]) {
+      const int32_t b = rp[v], e = rp[v + 1];
+      const int32_t* row = staged ? sc + (b - a0) : col + b;
+      int32_t u = row[0];
+      double sx = __ldg(x0 + u), sy = __ldg(y0 + u), sz = DIM == 3 ? __ldg(z0 + u) : 0.0;
+      for (int32_t i = 1; i < e - b; ++i) {
+        u = row[i];
+        sx = __dadd_rn(sx, __ldg(x0 + u));
+        sy = __dadd_rn(sy, __ldg(y0 + u));
+        if (DIM == 3) sz = __dadd_rn(sz, __ldg(z0 + u));
+      }
+      const double d = (double)(e - b);
+      x1[v] = __ddiv_rn(sx, d);
+      y1[v] = __ddiv_rn(sy, d);
+      if (DIM == 3) z1[v] = __ddiv_rn(sz, d);
+    }
+  }
+}
+
+void run_jacobi(lms_mesh_s* m, int sweeps, cudaStream_t s) {
+  const int64_t V = m->V;
+  sync_soa(m, s);
+  soa_changed(m);
+  // the second buffer carries the fixed vertices too (never written)
+  for (int a = 0; a < m->dim; ++a) {
+    if (!m->xalt[a].p || m->xalt[a].n != (size_t)V) m->xalt[a].alloc(V, s);
+    LMS_TRY_CUDA(cudaMemcpyAsync(m->xalt[a].p, m->x[a].p, V * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t chunks = (V + JB - 1) / JB;
+  const unsigned G = (unsigned)(chunks < (int64_t)sms * 8 ? chunks : (int64_t)sms * 8);
+  for (int i = 0; i < sweeps; ++i) {
+    if (m->dim == 2)
+      k_jacobi<2><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, nullptr,
+                                   m->xalt[0].p, m->xalt[1].p, nullptr);
+    else
+      k_jacobi<3><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, m->x[2].p,
+                                   m->xalt[0].p, m->xalt[1].p, m->xalt[2].p);
+    LMS_CHECK_LAUNCH();
+    for (int a = 0; a < m->dim; ++a) std::swap(m->x[a], m->xalt[a]);
+  }
+  ++m->coord_gen;  // xalt no longer mirrors x for the GZ 3D ping-pong
+}
+
+}  // namespace lms

@@ -189,6 +189,10 @@ struct lms_mesh_s {
   lms::DBuf<int32_t> orig_id;
   lms::DBuf<int32_t> elems;
   lms::DBuf<double> quality;   // valid if has_quality
+  // vertex -> element incidence (ascending element id per vertex) for the
+  // per-sweep global quality (quality.cu); dropped when the mesh is relabelled
+  lms::DBuf<int32_t> v2e_ptr, v2e;
+  bool v2e_valid = false;
   bool has_quality = false;    // m->quality holds the INITIAL qualities (RDR input)
   bool quality_external = false;
   bool coords_moved = false;   // coordinates changed since the build (smooth / import)
@@ -238,6 +242,7 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s);
 int64_t spatial_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s);
 bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s);  // gz.cu
 void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s);                     // gz.cu
+void run_jacobi(lms_mesh_s* m, int sweeps, cudaStream_t s);                 // jacobi.cu
 void sync_soa(lms_mesh_s* m, cudaStream_t s);   // make x[] current (gz.cu)
 void soa_changed(lms_mesh_s* m);                // x[] was written outside a sweep
 void run_sweeps(lms_mesh_s* m, int sweeps, cudaStream_t s);

@@ -119,6 +119,7 @@ void permute_mesh(lms_mesh_s* m, const int32_t* d_perm, cudaStream_t s) {
     LMS_CHECK_LAUNCH();
   }
   m->sched.valid = false;
+  m->v2e_valid = false;  // vertex labels changed (elements keep their order)
   soa_changed(m);
 }
 

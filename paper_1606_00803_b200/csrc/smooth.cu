@@ -493,6 +493,11 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   Schedule& S = m->sched;
   S.valid = false;
   S.base_valid = false;
+  if (m->sched_req == LMS_SCHED_JACOBI) {  // N3 variant (jacobi.cu): no schedule tables
+    S.kind = LMS_SCHED_JACOBI;
+    S.valid = true;
+    return;
+  }
   // GZ (gz.cu): the default for 2D meshes with few colours, where the
   // C-hop ghost zone of a tile is a small fraction of it
   if (m->sched_req == LMS_SCHED_GZ || (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->C <= 8)) {
@@ -1408,6 +1413,10 @@ void run_sweeps(lms_mesh_s* m, int sweeps, cudaStream_t s) {
   Schedule& S = m->sched;
   if (S.kind == LMS_SCHED_GZ) {
     run_gz(m, sweeps, s);
+    return;
+  }
+  if (S.kind == LMS_SCHED_JACOBI) {
+    run_jacobi(m, sweeps, s);
     return;
   }
   sync_soa(m, s);
