@@ -48,7 +48,7 @@ typedef enum {
     LMS_E_DEGENERATE = -5, /* element whose vertices all coincide (quality undefined) */
     LMS_E_NOMEM = -6,      /* device allocation failed */
     LMS_E_CUDA = -7,       /* CUDA runtime error (message in lms_last_error) */
-    LMS_E_NCCL = -8,       /* reserved for the multi-GPU path */
+    LMS_E_NCCL = -8,       /* NCCL failure or NCCL unavailable (multi-GPU calls) */
     LMS_E_STATE = -9       /* handle not in a state that allows the call (e.g. RDR without quality) */
 } lms_status;
 
@@ -250,6 +250,62 @@ typedef enum { LMS_STOP_GOAL = 1, LMS_STOP_CONVERGED = 2, LMS_STOP_MAX = 3 } lms
 lms_status lms_global_quality(lms_mesh_t m, double* h_quality, double* d_vertex_quality, lms_stream_t stream);
 lms_status lms_smooth_until(lms_mesh_t m, double goal, double eps, int32_t max_sweeps, int32_t* sweeps_run,
                             double* h_quality_history, int32_t* stop_reason, lms_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU sweep: one process per GPU, one rank each.
+ *
+ * Partition (the paper's "static ... evenly dividing the vertices";
+ * DESIGN.md reading Z22): the mesh AS RELABELLED is split into `nranks`
+ * contiguous label ranges [first, first + count) with ceil(n_free / nranks)
+ * free vertices each; rank r owns range r.  Each rank keeps every vertex
+ * within D = C * sweeps_per_exchange hops (through free vertices) of its
+ * range, in ascending label (so every row keeps its CSR order), and the
+ * library-owned NCCL communicator refreshes the ghost values once per pass
+ * of sweeps_per_exchange sweeps; the rank then runs the pass on its local
+ * mesh (GZ in 2D).  The owned coordinates are bit-identical to lms_smooth on
+ * one GPU.
+ *
+ * lms_nccl_unique_id -- ncclGetUniqueId into out[128] (call on rank 0 and
+ *  broadcast the bytes, e.g. over torch.distributed).  LMS_E_NCCL if NCCL
+ *  (libnccl.so.2, bound at run time) is unavailable.
+ * lms_dist_create -- every rank calls it with its handle of the SAME mesh
+ *  (built and relabelled identically on every rank), its rank, nranks and the
+ *  shared uid; collective (ncclCommInitRank, then the ghost lists go to their
+ *  owners).  Builds the rank's plan on its GPU from its own range only:
+ *  O(V) memsets and one O(V) scan, O(V/P + halo) otherwise.  `m` is only read:
+ *  it may be destroyed afterwards.  sweeps_per_exchange in [1, 8]; tile = the
+ *  local GZ tile (0 = default).  *out is a new handle (lms_dist_destroy).
+ * lms_smooth_dist -- `sweeps` colour-GS sweeps (Eq. 1): per pass
+ *  of up to sweeps_per_exchange sweeps, pack -> grouped ncclSend/ncclRecv
+ *  on `stream` -> unpack, then the local pass.  Collective: every rank calls
+ *  it with the same `sweeps`.
+ * lms_dist_export_owned -- the owned coordinates into d_out (host array of dim
+ *  device pointers, double[count] each; NULL = sizes only): *first = first
+ *  owned label, *count = number of owned labels.
+ * lms_dist_info -- local vertices, ghost values sent / received per pass
+ *  (vertices), peers exchanged with, ghost-zone depth D.
+ * lms_dist_export_local_ids -- the labels of the rank's local vertices
+ *  (int32[n_local], ascending).
+ * lms_dist_create_local / lms_smooth_dist_local -- the same plans for all
+ *  nranks ranks in ONE process on one device, exchanged by device copies
+ *  (testing the partition without NCCL; the ranks are stepped in turn and no
+ *  kernel waits on another rank).  outs: lms_dist_t[nranks], in rank order.
+ * Errors: LMS_E_ARG (bad rank / nranks / sweeps), LMS_E_NCCL, LMS_E_CUDA,
+ *  LMS_E_NOMEM, LMS_E_STATE (inconsistent peers). */
+typedef struct lms_dist_s* lms_dist_t;
+lms_status lms_nccl_unique_id(uint8_t out[128]);
+lms_status lms_dist_create(lms_mesh_t m, int32_t rank, int32_t nranks, const uint8_t nccl_uid[128],
+                           int32_t sweeps_per_exchange, int32_t tile, lms_stream_t stream, lms_dist_t* out);
+lms_status lms_smooth_dist(lms_dist_t d, int32_t sweeps, lms_stream_t stream);
+lms_status lms_dist_export_owned(lms_dist_t d, double* const* d_out, int64_t* first, int64_t* count,
+                                 lms_stream_t stream);
+lms_status lms_dist_info(lms_dist_t d, int64_t* n_local, int64_t* n_send, int64_t* n_recv, int32_t* n_peers,
+                         int32_t* depth);
+lms_status lms_dist_export_local_ids(lms_dist_t d, int32_t* d_ids, lms_stream_t stream);
+lms_status lms_dist_create_local(lms_mesh_t m, int32_t nranks, int32_t sweeps_per_exchange, int32_t tile,
+                                 lms_stream_t stream, lms_dist_t* outs);
+lms_status lms_smooth_dist_local(lms_dist_t* ds, int32_t nranks, int32_t sweeps, lms_stream_t stream);
+void lms_dist_destroy(lms_dist_t d);
 
 /* Thread-local message for the last non-OK status of this thread. */
 const char* lms_last_error(void);

@@ -7,8 +7,9 @@ PyTorch provides device memory and streams only.  There is no CPU fallback:
 if the CUDA library or a GPU is missing, calls raise.
 """
 from ._lms import (  # noqa: F401
-    LMSError, Mesh, ORDERINGS, SCHEDULES, cache_release, lib, load_library, kernel_launches, use_torch_allocator,
+    Dist, LMSError, Mesh, ORDERINGS, SCHEDULES, cache_release, lib, load_library, kernel_launches, nccl_unique_id,
+    use_torch_allocator,
 )
 
-__all__ = ["LMSError", "Mesh", "ORDERINGS", "SCHEDULES", "cache_release", "lib", "load_library", "kernel_launches",
-           "use_torch_allocator"]
+__all__ = ["Dist", "LMSError", "Mesh", "ORDERINGS", "SCHEDULES", "cache_release", "lib", "load_library",
+           "kernel_launches", "nccl_unique_id", "use_torch_allocator"]

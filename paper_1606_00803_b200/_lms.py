@@ -30,7 +30,9 @@ EXPORTS = ["lms_build_csr", "lms_build_csr_host", "lms_mesh_from_csr", "lms_mesh
            "lms_export_csr", "lms_export_colour", "lms_export_fixed", "lms_export_orig_id", "lms_export_elems",
            "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_cache_release", "lms_set_allocator", "lms_set_tiling", "lms_schedule_info2",
            "lms_smooth_colour", "lms_gather_coords", "lms_scatter_coords",
-           "lms_global_quality", "lms_smooth_until"]
+           "lms_global_quality", "lms_smooth_until",
+           "lms_nccl_unique_id", "lms_dist_create", "lms_smooth_dist", "lms_dist_export_owned", "lms_dist_info",
+           "lms_dist_export_local_ids", "lms_dist_create_local", "lms_smooth_dist_local", "lms_dist_destroy"]
 
 
 class LMSError(RuntimeError):
@@ -81,6 +83,15 @@ def load_library(build: bool = True):
         "lms_global_quality": [P, ct.POINTER(ct.c_double), P, P],
         "lms_smooth_until": [P, ct.c_double, ct.c_double, i32, ct.POINTER(i32), ct.POINTER(ct.c_double),
                              ct.POINTER(i32), P],
+        "lms_nccl_unique_id": [P],
+        "lms_dist_create": [P, i32, i32, P, i32, i32, P, ct.POINTER(P)],
+        "lms_smooth_dist": [P, i32, P],
+        "lms_dist_export_owned": [P, PP, ct.POINTER(i64), ct.POINTER(i64), P],
+        "lms_dist_info": [P, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i32), ct.POINTER(i32)],
+        "lms_dist_export_local_ids": [P, P, P],
+        "lms_dist_create_local": [P, i32, i32, i32, P, ct.POINTER(P)],
+        "lms_smooth_dist_local": [ct.POINTER(P), i32, i32, P],
+        "lms_dist_destroy": [P],
         "lms_last_error": [],
         "lms_kernel_launches": [],
         "lms_cache_release": [],
@@ -91,6 +102,7 @@ def load_library(build: bool = True):
         f.argtypes = args
         f.restype = i32
     L.lms_mesh_destroy.restype = None
+    L.lms_dist_destroy.restype = None
     L.lms_last_error.restype = ct.c_char_p
     L.lms_kernel_launches.restype = i64
     L.lms_cache_release.restype = None
@@ -385,3 +397,91 @@ class Mesh:
         out = torch.empty(self.V, dtype=torch.float64, device="cuda")
         _check(lib().lms_export_quality(self._h, ct.c_void_p(out.data_ptr()), _stream(stream)), "lms_export_quality")
         return out
+
+
+# ---------------------------------------------------------------------------- multi-GPU
+def nccl_unique_id() -> bytes:
+    """lms_nccl_unique_id: 128 bytes to broadcast from rank 0."""
+    buf = (ct.c_uint8 * 128)()
+    _check(lib().lms_nccl_unique_id(ct.cast(buf, ct.c_void_p)), "lms_nccl_unique_id")
+    return bytes(buf)
+
+
+class Dist:
+    """Owner of an lms_dist_t handle: one rank of the multi-GPU sweep."""
+
+    def __init__(self, handle: ct.c_void_p, dim: int, group=None):
+        self._h = handle
+        self.dim = dim
+        self._group = group  # local-group emulation: the list of all ranks' handles
+
+    @classmethod
+    def create(cls, mesh: "Mesh", rank: int, nranks: int, uid: bytes, sweeps_per_exchange: int = 1,
+               tile: int = 0, stream=None) -> "Dist":
+        """lms_dist_create (collective over the nranks processes)."""
+        if len(uid) != 128:
+            raise ValueError("uid must be 128 bytes")
+        ub = (ct.c_uint8 * 128).from_buffer_copy(uid)
+        h = ct.c_void_p()
+        _check(lib().lms_dist_create(mesh._h, rank, nranks, ct.cast(ub, ct.c_void_p), sweeps_per_exchange, tile,
+                                     _stream(stream), ct.byref(h)), "lms_dist_create")
+        return cls(h, mesh.info()["dim"])
+
+    @classmethod
+    def create_local(cls, mesh: "Mesh", nranks: int, sweeps_per_exchange: int = 1, tile: int = 0,
+                     stream=None) -> list:
+        """lms_dist_create_local: all ranks in this process (device-copy exchange)."""
+        arr = (ct.c_void_p * nranks)()
+        _check(lib().lms_dist_create_local(mesh._h, nranks, sweeps_per_exchange, tile, _stream(stream), arr),
+               "lms_dist_create_local")
+        dim = mesh.info()["dim"]
+        ds = [cls(ct.c_void_p(arr[r]), dim) for r in range(nranks)]
+        for d in ds:
+            d._group = ds
+        return ds
+
+    @staticmethod
+    def smooth_local(ds: list, sweeps: int, stream=None):
+        arr = (ct.c_void_p * len(ds))(*[d._h.value for d in ds])
+        _check(lib().lms_smooth_dist_local(arr, len(ds), sweeps, _stream(stream)), "lms_smooth_dist_local")
+
+    def smooth(self, sweeps: int, stream=None):
+        _check(lib().lms_smooth_dist(self._h, sweeps, _stream(stream)), "lms_smooth_dist")
+
+    def owned_range(self):
+        f, c = ct.c_int64(), ct.c_int64()
+        _check(lib().lms_dist_export_owned(self._h, None, ct.byref(f), ct.byref(c), None), "lms_dist_export_owned")
+        return f.value, c.value
+
+    def export_owned(self, stream=None):
+        """-> (first, [dim float64 CUDA tensors of the owned coordinates])."""
+        first, count = self.owned_range()
+        out = [torch.empty(count, dtype=torch.float64, device="cuda") for _ in range(self.dim)]
+        pp, keep = _ptr_array(out)
+        f, c = ct.c_int64(), ct.c_int64()
+        _check(lib().lms_dist_export_owned(self._h, pp, ct.byref(f), ct.byref(c), _stream(stream)),
+               "lms_dist_export_owned")
+        return first, out
+
+    def info(self):
+        nl, ns, nr, npr, dp = ct.c_int64(), ct.c_int64(), ct.c_int64(), ct.c_int32(), ct.c_int32()
+        _check(lib().lms_dist_info(self._h, ct.byref(nl), ct.byref(ns), ct.byref(nr), ct.byref(npr), ct.byref(dp)),
+               "lms_dist_info")
+        return dict(n_local=nl.value, n_send=ns.value, n_recv=nr.value, peers=npr.value, depth=dp.value)
+
+    def local_ids(self, stream=None):
+        out = torch.empty(max(self.info()["n_local"], 1), dtype=torch.int32, device="cuda")
+        _check(lib().lms_dist_export_local_ids(self._h, ct.c_void_p(out.data_ptr()), _stream(stream)),
+               "lms_dist_export_local_ids")
+        return out[:self.info()["n_local"]]
+
+    def close(self):
+        if self._h:
+            lib().lms_dist_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

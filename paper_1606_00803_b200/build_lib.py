@@ -17,6 +17,20 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC,-O2",
          "--expt-relaxed-constexpr", "-cudart", "static", "-I" + os.path.join(ROOT, "include")]
+# NCCL: headers only at build time (the library dlopens libnccl.so.2 at run time)
+def _nccl_include():
+    cands = []
+    try:
+        import nvidia.nccl
+        cands += [os.path.join(p, "include") for p in nvidia.nccl.__path__]
+    except Exception:
+        pass
+    cands.append("/usr/include")
+    return [p for p in cands if os.path.exists(os.path.join(p, "nccl.h"))]
+
+
+_NCCL_INC = _nccl_include()
+FLAGS += ["-I" + _NCCL_INC[0]] if _NCCL_INC else []
 
 
 def sources():
@@ -57,7 +71,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(f"--- {s}\n{o}" for s, o in failed))
     tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -50,6 +50,34 @@ __global__ void k_scatter_coords(double* __restrict__ x, double* __restrict__ y,
   }
 }
 
+// halo pack: out[a*n + i] = x_a[idx[i]] from whichever copy is current
+void halo_pack(lms_mesh_s* m, const int32_t* idx, int64_t n, double* out, cudaStream_t s) {
+  if (n == 0) return;
+  const unsigned G = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
+  if (m->aos_state == 1) {  // the interleaved copy is current: no conversion of the whole mesh
+    k_gather_aos<<<G, 256, 0, s>>>(reinterpret_cast<const double2*>(m->xy[m->xy_cur].p), idx, n, out);
+  } else {
+    k_gather_coords<<<G, 256, 0, s>>>(m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, idx, n, out);
+  }
+  LMS_CHECK_LAUNCH();
+}
+
+// halo unpack: x_a[idx[i]] = in[a*n + i], into every live copy
+void halo_unpack(lms_mesh_s* m, const int32_t* idx, int64_t n, const double* in, cudaStream_t s) {
+  if (n == 0) return;
+  const unsigned G = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
+  if (m->aos_state != 0) {  // keep the interleaved ping-pong copies current
+    k_scatter_aos<<<G, 256, 0, s>>>(reinterpret_cast<double2*>(m->xy[0].p), reinterpret_cast<double2*>(m->xy[1].p),
+                                    idx, n, in);
+    LMS_CHECK_LAUNCH();
+  }
+  if (m->aos_state != 1) {
+    k_scatter_coords<<<G, 256, 0, s>>>(m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, idx, n, in);
+    LMS_CHECK_LAUNCH();
+  }
+  if (m->aos_state == 0) soa_changed(m);
+}
+
 }  // namespace lms
 
 using namespace lms;
@@ -78,15 +106,7 @@ lms_status lms_gather_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, doub
   try {
     if (!m || (n > 0 && (!d_idx || !d_out)) || n < 0) fail(LMS_E_ARG, "bad argument");
     DevGuard dg(m);
-    if (n == 0) return LMS_OK;
-    cudaStream_t s = (cudaStream_t)stream;
-    const unsigned G = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
-    if (m->aos_state == 1) {  // the interleaved copy is current: no conversion of the whole mesh
-      k_gather_aos<<<G, 256, 0, s>>>(reinterpret_cast<const double2*>(m->xy[m->xy_cur].p), d_idx, n, d_out);
-    } else {
-      k_gather_coords<<<G, 256, 0, s>>>(m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_out);
-    }
-    LMS_CHECK_LAUNCH();
+    halo_pack(m, d_idx, n, d_out, (cudaStream_t)stream);
     return LMS_OK;
   } catch (const Err& e) {
     set_error(e.msg);
@@ -99,19 +119,7 @@ lms_status lms_scatter_coords(lms_mesh_t m, const int32_t* d_idx, int64_t n, con
   try {
     if (!m || (n > 0 && (!d_idx || !d_in)) || n < 0) fail(LMS_E_ARG, "bad argument");
     DevGuard dg(m);
-    if (n == 0) return LMS_OK;
-    cudaStream_t s = (cudaStream_t)stream;
-    const unsigned G = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
-    if (m->aos_state != 0) {  // keep the interleaved ping-pong copies current
-      k_scatter_aos<<<G, 256, 0, s>>>(reinterpret_cast<double2*>(m->xy[0].p), reinterpret_cast<double2*>(m->xy[1].p),
-                                      d_idx, n, d_in);
-      LMS_CHECK_LAUNCH();
-    }
-    if (m->aos_state != 1) {
-      k_scatter_coords<<<G, 256, 0, s>>>(m->x[0].p, m->x[1].p, m->dim == 3 ? m->x[2].p : nullptr, d_idx, n, d_in);
-      LMS_CHECK_LAUNCH();
-    }
-    if (m->aos_state == 0) soa_changed(m);
+    halo_unpack(m, d_idx, n, d_in, (cudaStream_t)stream);
     m->coords_moved = true;
     return LMS_OK;
   } catch (const Err& e) {

@@ -243,6 +243,8 @@ int64_t spatial_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s);
 bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s);  // gz.cu
 void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s);                     // gz.cu
 void run_jacobi(lms_mesh_s* m, int sweeps, cudaStream_t s);                 // jacobi.cu
+void halo_pack(lms_mesh_s* m, const int32_t* idx, int64_t n, double* out, cudaStream_t s);        // halo.cu
+void halo_unpack(lms_mesh_s* m, const int32_t* idx, int64_t n, const double* in, cudaStream_t s);  // halo.cu
 void sync_soa(lms_mesh_s* m, cudaStream_t s);   // make x[] current (gz.cu)
 void soa_changed(lms_mesh_s* m);                // x[] was written outside a sweep
 void run_sweeps(lms_mesh_s* m, int sweeps, cudaStream_t s);
