@@ -50,7 +50,7 @@ def load_library(build: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    path = build_lib.build() if build else build_lib.LIB
+    path = os.environ.get("LMS_LIB_PATH") or (build_lib.build() if build else build_lib.LIB)  # env: dev A/B builds
     if not os.path.exists(path):
         raise RuntimeError(f"liblms.so not found at {path}; run __graft_entry__.build()")
     L = ct.CDLL(path)

@@ -76,7 +76,13 @@ namespace lms {
 
 constexpr int GZ_MAX_C = 15;    // colours: 4 bits of the update sort key
 constexpr int GZ_MAX_P = 8;     // sweeps per pass: 3 bits of the update sort key
-constexpr uint16_t GZ_PAD = 0xFFFF;
+constexpr uint16_t GZ_PAD = 0xFFFF;  // 3D row padding (predicated gathers)
+// 2D rows pad with the region's PAD SLOT (slot n_slots, staged as (-0.0, -0.0):
+// the identity of IEEE addition), so every gather is unpredicated.  The
+// update's degree then comes from the record: the second dependency word of
+// each position is (d << 12) | dependency, d = 0 when d > 15 (count instead),
+// dependency 0xFFF = none (a tile with 4095+ items waits for whole stages).
+constexpr uint16_t GZ_DNONE = 0xFFF;
 constexpr int GZ_MAX_REGION = 32767;  // slots are 15 bits (bit 15 = owned flag)
 // An item is U = 32 * UPL updates of one stage of one tile (UPL updates per
 // lane: 2 in 2D, 1 in 3D); its dependency list has at most U entries (more ->
@@ -407,7 +413,8 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
                               const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
                               const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                               const int32_t* __restrict__ tile_of, const uint64_t* __restrict__ reg,
-                              const int64_t* __restrict__ reg_off, uint4* rec, int32_t* it_lo, int32_t* it_hi) {
+                              const int64_t* __restrict__ reg_off, uint4* rec, int32_t* it_lo, int32_t* it_hi,
+                              int dim, int padbase) {
   extern __shared__ uint32_t gz_rid[];  // [max region slots]
   // per update: one-hot bank mask of its own slot (byte 0) and neighbours
   // 0..6 (bytes 1..7); neighbour banks packed 3 bits each (bits 0..23) and
@@ -453,6 +460,7 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
     __syncthreads();
     const GzTile t = tab[k];
     const int R = (int)t.R;
+    const uint16_t padv = dim == 2 ? (uint16_t)padbase : GZ_PAD;  // 2D: the first pad slot
     const int64_t i0 = sfirst[k * PC], i1 = sfirst[(k + 1) * PC];
     for (int64_t it = i0 + wib; it < i1; it += nwib) {
       const int64_t ks = it_ks[it];
@@ -468,6 +476,7 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
       uint32_t* pb = reinterpret_cast<uint32_t*>(base + 2 * U * R);
       int32_t* gid = reinterpret_cast<int32_t*>(base + 2 * U * R + 4 * U);
       uint32_t* desc = reinterpret_cast<uint32_t*>(base + 2 * U * R + 8 * U);
+      uint16_t* dep2 = reinterpret_cast<uint16_t*>(base + gz_dep2_off(R, U));
       // bank groups of each update (position-independent), then the placement
       if (R == 8) {
         for (int u0 = 0; u0 < U; u0 += 32) {
@@ -585,6 +594,7 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
         const int pos = ps[e];
         uint32_t p = 0xffff0000u | 0x7fffu;  // slot 0x7fff = empty position
         int32_t g = -1;
+        uint16_t dg = GZ_DNONE;  // degree bits (0 for an empty position)
         if (e < n) {
           const int64_t uu = kc_off[kc] + (int64_t)U * q + e;
           const int32_t v = cv[uu];
@@ -594,9 +604,10 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
           lo = min(lo, lv);
           hi = max(hi, lv);
           const int32_t b = rp[v], d = rp[v + 1] - b;
+          dg = (uint16_t)(((d <= 15 ? d : 0) << 12) | GZ_DNONE);
           const int gm = R == 8 ? gp[e] : 0;
           for (int w = 0, kk = 0; w < R; ++w) {
-            uint16_t li = GZ_PAD;
+            uint16_t li = padv;
             const bool use = R == 8 ? (((gm >> w) & 1) && kk < d) : w < d;
             if (use) {
               const int sl = R == 8 ? sl8[e * 8 + kk] : region_slot(gz_rid, nr, (uint32_t)col[b + kk]);
@@ -608,12 +619,34 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
             rows[pos * R + w] = li;
           }
         } else {
-          for (int w = 0; w < R; ++w) rows[pos * R + w] = GZ_PAD;
+          for (int w = 0; w < R; ++w) rows[pos * R + w] = padv;
         }
         pb[pos] = p;
         gid[pos] = g;
+        dep2[pos] = dg;
       }
       __syncwarp();
+      if (dim == 2 && R == 8) {
+        // Padding reads one of the 8 pad slots padbase .. padbase + 7 (one per
+        // bank group of 16-byte slots; padbase = the largest region rounded up
+        // to 8, so slot padbase + g is in bank group g).  A quarter-warp gathers position w of its 8
+        // positions at once; its pads all read the pad slot in a bank group
+        // none of its real gathers use (one exists whenever there is a pad),
+        // so padding adds no shared-memory wavefront.
+        for (int pr = lane; pr < (U / 8) * 8; pr += 32) {
+          const int a = pr >> 3, w = pr & 7;
+          uint32_t used = 0;
+          for (int j = 0; j < 8; ++j) {
+            const uint16_t x = rows[(8 * a + j) * R + w];
+            if (x < padv) used |= 1u << (x & 7u);
+          }
+          const uint32_t g = (uint32_t)__ffs(~used & 0xffu) - 1u;  // lowest free bank group
+          const uint16_t pslot = (uint16_t)(padv + g);
+          for (int j = 0; j < 8; ++j)
+            if (rows[(8 * a + j) * R + w] == padv) rows[(8 * a + j) * R + w] = pslot;
+        }
+        __syncwarp();
+      }
       for (int o = 16; o; o >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
         hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
@@ -651,17 +684,19 @@ __global__ void k_gzd_deps(const int32_t* __restrict__ it_ks, int64_t NI, int C,
     const int lo = it_lo[it], hi = it_hi[it];
     const int64_t a = sfirst[k * PC + (sg - C > 0 ? sg - C : 0)], b = sfirst[k * PC + sg];
     uint16_t* dep2 = reinterpret_cast<uint16_t*>(base + gz_dep2_off(t.R, U));
-    for (int e = 0; e < U; ++e) dep2[e] = 0xffffu;
+    for (int e = 0; e < U; ++e) dep2[e] = (uint16_t)((dep2[e] & 0xF000u) | GZ_DNONE);  // keep the degree bits
     int nd = 0;
     for (int64_t o = a; o < b; ++o)
       if (it_lo[o] <= hi && it_hi[o] >= lo) {
         if (nd < U) pb[nd] = (pb[nd] & 0xffffu) | ((uint32_t)(o - f0) << 16);
-        else if (nd < 2 * U) dep2[nd - U] = (uint16_t)(o - f0);
+        else if (nd < 2 * U) dep2[nd - U] = (uint16_t)((dep2[nd - U] & 0xF000u) | ((uint32_t)(o - f0) & 0xFFFu));
         ++nd;
       }
-    desc[1] = nd > 2 * U ? 1u : 0u;
+    // dependencies are 12-bit item indices: a tile with 4095+ items waits for whole stages
+    const bool whole = nd > 2 * U || t.n_items >= GZ_DNONE;
+    desc[1] = whole ? 1u : 0u;
     desc[3] = (uint32_t)nd;  // (informational: the number of overlapping earlier items)
-    if (nd > 2 * U) atomicOr(&tneed[k], 1);
+    if (whole) atomicOr(&tneed[k], 1);
   }
 }
 
@@ -741,8 +776,8 @@ __global__ void k_gzd_permute(const int32_t* __restrict__ it_ks, const int32_t* 
     for (int e = lane; e < U; e += 32) {
       const uint32_t d = pb[e] >> 16;
       if (d != 0xffffu) pb[e] = (pb[e] & 0xffffu) | ((uint32_t)(newpos[f0 + d] - f0) << 16);
-      const uint32_t d2 = dep2[e];
-      if (d2 != 0xffffu) dep2[e] = (uint16_t)(newpos[f0 + d2] - f0);
+      const uint32_t d2 = dep2[e] & 0xFFFu;
+      if (d2 != GZ_DNONE) dep2[e] = (uint16_t)((dep2[e] & 0xF000u) | ((uint32_t)(newpos[f0 + d2] - f0) & 0xFFFu));
     }
   }
 }
@@ -760,9 +795,9 @@ __global__ void k_gzd_check_order(const int32_t* __restrict__ it_ks, int64_t NI,
     const uint32_t* pb = reinterpret_cast<const uint32_t*>(base + 2 * U * t.R);
     const uint16_t* dep2 = reinterpret_cast<const uint16_t*>(base + gz_dep2_off(t.R, U));
     for (int e = 0; e < U; ++e) {
-      const uint32_t d = pb[e] >> 16, d2 = dep2[e];
+      const uint32_t d = pb[e] >> 16, d2 = dep2[e] & 0xFFFu;
       if (d != 0xffffu && (int64_t)d >= loc) atomicAdd(bad, 1ull);
-      if (d2 != 0xffffu && (int64_t)d2 >= loc) atomicAdd(bad, 1ull);
+      if (d2 != GZ_DNONE && (int64_t)d2 >= loc) atomicAdd(bad, 1ull);
     }
   }
 }
@@ -971,12 +1006,35 @@ __device__ __forceinline__ double gz_div(double x, double d, double r) {
   return __fma_rn(e, r, q);
 }
 
+#ifdef LMS_BOUNDS
+__device__ int gz_bounds_code = 0;
+__device__ __noinline__ void gz_bounds_fail(int code) { atomicCAS(&gz_bounds_code, 0, code); }
+#endif
+__device__ __forceinline__ double2 lds_f64x2_all(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+
+// x / d for Eq. 1: the Markstein quotient when its preconditions hold (see
+// gz_div), else __ddiv_rn -- both correctly rounded
+__device__ __forceinline__ double2 gz_div2(double sx, double sy, int d, const double* rcp) {
+  const double dd = (double)d;
+  if (d >= 1 && d <= GZ_RCP_MAX && gz_div_ok(sx) && gz_div_ok(sy)) {
+    const double rr = rcp[d];
+    return make_double2(gz_div(sx, dd, rr), gz_div(sy, dd, rr));
+  }
+  return make_double2(__ddiv_rn(d ? sx : 0.0, dd), __ddiv_rn(d ? sy : 0.0, dd));
+}
+
 // Eq. 1 for this lane's update: neighbours (CSR order) from shared memory,
 // ordered IEEE adds, correctly rounded division, result back to shared
-// memory; returns the new value through (ox, oy, oz).
+// memory; returns the new value through (ox, oy, oz).  2D rows pad with the
+// pad slot (unpredicated gathers); dbits = the update's degree (0: count).
 template <int DIM, int RMAX>
 __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uint4* __restrict__ rowg, double* sc,
-                                          const double* rcp, int nr4, double& ox, double& oy, double& oz) {
+                                          const double* rcp, int nr4, uint32_t padv, int dbits, double& ox,
+                                          double& oy, double& oz) {
   const int v = (int)(r.pb & 0x7fffu);
   uint16_t u[RMAX];
 #pragma unroll
@@ -987,11 +1045,10 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
   if (DIM == 2) {
     double2 g[RMAX];
 #pragma unroll
-    for (int w = 0; w < RMAX; ++w) {
-      const bool ok = u[w] != GZ_PAD;
-      g[w] = lds_f64x2(sb + 16u * u[w], ok);
-      d += ok;
-    }
+    for (int w = 0; w < RMAX; ++w) g[w] = lds_f64x2_all(sb + 16u * u[w]);
+    if (dbits == 0)
+#pragma unroll
+      for (int w = 0; w < RMAX; ++w) d += u[w] < padv;
     sx = g[0].x;
     sy = g[0].y;
 #pragma unroll
@@ -1000,26 +1057,21 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
       sy = __dadd_rn(sy, g[w].y);
     }
     const double2* s2 = reinterpret_cast<const double2*>(sc);
-    for (int p = RMAX / 8; p * 8 < R; ++p) {  // rows longer than RMAX: ordered tail from global
+    for (int p = RMAX / 8; p * 8 < R; ++p) {  // rows longer than RMAX: ordered tail from the record
       uint16_t t[8];
       unpack8(rowg[p], t);
-      for (int q = 0; q < 8 && t[q] != GZ_PAD; ++q) {
+      for (int q = 0; q < 8 && t[q] < padv; ++q) {
         const double2 e = s2[t[q]];
         sx = __dadd_rn(sx, e.x);
         sy = __dadd_rn(sy, e.y);
         ++d;
       }
     }
-    const double dd = (double)d;
-    const double rr = rcp[d <= GZ_RCP_MAX ? d : 0];
-    if (d >= 1 && d <= GZ_RCP_MAX && gz_div_ok(sx) && gz_div_ok(sy)) {
-      ox = gz_div(sx, dd, rr);
-      oy = gz_div(sy, dd, rr);
-    } else {
-      ox = __ddiv_rn(d ? sx : 0.0, dd);
-      oy = __ddiv_rn(d ? sy : 0.0, dd);
-    }
-    reinterpret_cast<double2*>(sc)[v] = make_double2(ox, oy);
+    if (dbits) d = dbits;
+    const double2 o = gz_div2(sx, sy, d, rcp);
+    ox = o.x;
+    oy = o.y;
+    reinterpret_cast<double2*>(sc)[v] = o;
   } else {
     double gx[RMAX], gy[RMAX], gz[RMAX];
 #pragma unroll
@@ -1068,11 +1120,14 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
 
 // Two updates per lane (2D): the lane's update of item A and of item B, with
 // all gathers of both issued before the two ordered sums (more loads in flight
-// per warp, two independent FP64 add chains per axis).
+// per warp, two independent FP64 add chains per axis).  Every gather is
+// unpredicated: padding reads the pad slot's (-0.0, -0.0), the exact identity
+// of IEEE addition; the degrees come from the record (da, db; 0 = count).
 template <int RMAX>
-__device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const GzRec<RMAX>& rb, bool vb, int R,
-                                           const uint4* __restrict__ rowgA, const uint4* __restrict__ rowgB,
-                                           double* sc, const double* rcp, double2& oa, double2& ob) {
+__device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, int da, const GzRec<RMAX>& rb, bool vb,
+                                           int db, int R, const uint4* __restrict__ rowgA,
+                                           const uint4* __restrict__ rowgB, double* sc, const double* rcp,
+                                           uint32_t padv, double2& oa, double2& ob) {
   double2* s2 = reinterpret_cast<double2*>(sc);
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sc);
   uint16_t ua[RMAX], ub[RMAX];
@@ -1082,15 +1137,22 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
     unpack8(rb.row[p], ub + 8 * p);
   }
   double2 ga[RMAX], gb[RMAX];
-  int da = 0, db = 0;
 #pragma unroll
   for (int w = 0; w < RMAX; ++w) {
-    const bool oka = va && ua[w] != GZ_PAD, okb = vb && ub[w] != GZ_PAD;
-    ga[w] = lds_f64x2(sb + 16u * ua[w], oka);
-    gb[w] = lds_f64x2(sb + 16u * ub[w], okb);
-    da += oka;
-    db += okb;
+    ga[w] = lds_f64x2_all(sb + 16u * ua[w]);
+    gb[w] = lds_f64x2_all(sb + 16u * ub[w]);
   }
+#ifdef LMS_BOUNDS
+  // bounds-checked build: every gather inside the region or the pad slots,
+  // every pad slot still (-0.0, -0.0)
+#pragma unroll
+  for (int w = 0; w < RMAX; ++w) {
+    if (ua[w] >= padv + 8 || ub[w] >= padv + 8) gz_bounds_fail(-101);
+    if (ua[w] >= padv && (__double_as_longlong(ga[w].x) != (long long)0x8000000000000000ull ||
+                          __double_as_longlong(ga[w].y) != (long long)0x8000000000000000ull))
+      gz_bounds_fail(-102);
+  }
+#endif
   double ax = ga[0].x, ay = ga[0].y, bx = gb[0].x, by = gb[0].y;
 #pragma unroll
   for (int w = 1; w < RMAX; ++w) {
@@ -1099,43 +1161,43 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, const
     bx = __dadd_rn(bx, gb[w].x);
     by = __dadd_rn(by, gb[w].y);
   }
-  for (int p = RMAX / 8; p * 8 < R; ++p) {  // rows longer than RMAX: ordered tails
-    uint16_t t[8];
-    if (va) {
-      unpack8(rowgA[p], t);
-      for (int q = 0; q < 8 && t[q] != GZ_PAD; ++q) {
-        const double2 e = s2[t[q]];
-        ax = __dadd_rn(ax, e.x);
-        ay = __dadd_rn(ay, e.y);
-        ++da;
+  if (R > RMAX || da == 0 || db == 0) {  // long rows (tail from the record) or degrees > 15: count
+    int ca = 0, cb = 0;
+#pragma unroll
+    for (int w = 0; w < RMAX; ++w) {
+      ca += ua[w] < padv;
+      cb += ub[w] < padv;
+    }
+    for (int p = RMAX / 8; p * 8 < R; ++p) {  // rows longer than RMAX: ordered tails
+      uint16_t t[8];
+      if (va) {
+        unpack8(rowgA[p], t);
+        for (int q = 0; q < 8 && t[q] < padv; ++q) {
+          const double2 e = s2[t[q]];
+          ax = __dadd_rn(ax, e.x);
+          ay = __dadd_rn(ay, e.y);
+          ++ca;
+        }
+      }
+      if (vb) {
+        unpack8(rowgB[p], t);
+        for (int q = 0; q < 8 && t[q] < padv; ++q) {
+          const double2 e = s2[t[q]];
+          bx = __dadd_rn(bx, e.x);
+          by = __dadd_rn(by, e.y);
+          ++cb;
+        }
       }
     }
-    if (vb) {
-      unpack8(rowgB[p], t);
-      for (int q = 0; q < 8 && t[q] != GZ_PAD; ++q) {
-        const double2 e = s2[t[q]];
-        bx = __dadd_rn(bx, e.x);
-        by = __dadd_rn(by, e.y);
-        ++db;
-      }
-    }
+    if (da == 0) da = ca;
+    if (db == 0) db = cb;
   }
   if (va) {
-    const double dd = (double)da;
-    const double rr = rcp[da <= GZ_RCP_MAX ? da : 0];
-    if (da >= 1 && da <= GZ_RCP_MAX && gz_div_ok(ax) && gz_div_ok(ay))
-      oa = make_double2(gz_div(ax, dd, rr), gz_div(ay, dd, rr));
-    else
-      oa = make_double2(__ddiv_rn(da ? ax : 0.0, dd), __ddiv_rn(da ? ay : 0.0, dd));
+    oa = gz_div2(ax, ay, da, rcp);
     s2[ra.pb & 0x7fffu] = oa;
   }
   if (vb) {
-    const double dd = (double)db;
-    const double rr = rcp[db <= GZ_RCP_MAX ? db : 0];
-    if (db >= 1 && db <= GZ_RCP_MAX && gz_div_ok(bx) && gz_div_ok(by))
-      ob = make_double2(gz_div(bx, dd, rr), gz_div(by, dd, rr));
-    else
-      ob = make_double2(__ddiv_rn(db ? bx : 0.0, dd), __ddiv_rn(db ? by : 0.0, dd));
+    ob = gz_div2(bx, by, db, rcp);
     s2[rb.pb & 0x7fffu] = ob;
   }
 }
@@ -1219,6 +1281,11 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
   for (int b = 0; b < NB; ++b) {
     int* f = reinterpret_cast<int*>(sm + L.off_ring + (size_t)b * L.buf_bytes + L.flag_off);
     for (int q = threadIdx.x; q < (L.cnt_off - L.flag_off) / 4; q += blockDim.x) f[q] = 0;
+    // 2D: the pad slots (-0.0, -0.0), the exact identity of IEEE addition;
+    // regions never reach them, so they are written once per launch
+    if (DIM == 2 && threadIdx.x < 8)
+      reinterpret_cast<double2*>(sm + L.off_ring + (size_t)b * L.buf_bytes + L.coord_off)[L.padbase + threadIdx.x] =
+          make_double2(-0.0, -0.0);
   }
   for (int i = threadIdx.x; i < n_my; i += blockDim.x) {
     const int k = tiles[blockIdx.x + (long long)i * gridDim.x];
@@ -1449,8 +1516,9 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
     const int sg = (int)(desc.x >> 16);
     // this item's dependencies
     alive = 1;
+    // second dependency + degree bits of each of the lane's positions
     int d2v[UPL];
-    if (desc.y == 0) {
+    {
       const uint16_t* dep2 = reinterpret_cast<const uint16_t*>(rbase + gz_dep2_off(R, U));
 #pragma unroll
       for (int u = 0; u < UPL; ++u) d2v[u] = dep2[lane + 32 * u];
@@ -1460,6 +1528,21 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
     // rather than items in progress (rows longer than RMAX read their tail
     // from the record during the update: those release at completion)
     const bool early = R <= RMAX;
+    // The release must follow the COMPLETION of every lane's record loads:
+    // an arrive does not wait for this warp's shared-memory loads still in
+    // flight, and the loader's next TMA fill of the slot could land before
+    // them (observed: stale records on C4 under the random ordering).  So
+    // each lane folds all its record registers into one word and stores it
+    // (the store cannot issue before the loads return); __syncwarp orders the
+    // lanes' stores before lane 0's release-arrive.
+    uint32_t fold = desc.x ^ desc.y ^ desc.z ^ desc.w;
+#pragma unroll
+    for (int u = 0; u < UPL; ++u) {
+      fold ^= r[u].pb ^ (uint32_t)r[u].gid ^ (uint32_t)d2v[u];
+#pragma unroll
+      for (int p = 0; p < RMAX / 8; ++p) fold ^= r[u].row[p].x ^ r[u].row[p].y ^ r[u].row[p].z ^ r[u].row[p].w;
+    }
+    reinterpret_cast<volatile uint32_t*>(rcp + GZ_RCP_MAX + 1)[warp] = fold;
     __syncwarp();
     if (early && lane == 0) mbar_arrive(rempty + slot);
     if (desc.y == 0) {
@@ -1470,8 +1553,8 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
           guard.start();
           while (alive && flags[dep] != i + 1) alive = guard.ok();
         }
-        const int d2 = d2v[u];
-        if (d2 != 0xffff && d2 >= item0) {
+        const int d2 = d2v[u] & 0xFFF;
+        if (d2 != GZ_DNONE && d2 >= item0) {
           guard.start();
           while (alive && flags[d2] != i + 1) alive = guard.ok();
         }
@@ -1490,11 +1573,13 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
     const long long c2 = STATS ? clock64() : 0;
     double* sc = reinterpret_cast<double*>(buf + L.coord_off);
     const bool last = j == P - 1;
+    const uint32_t padv = DIM == 2 ? (uint32_t)L.padbase : (uint32_t)GZ_PAD;  // the first pad slot
     if (UPL == 2 && DIM == 2) {
       const bool va = (r[0].pb & 0x7fffu) != 0x7fffu, vb = (r[UPL - 1].pb & 0x7fffu) != 0x7fffu;
       double2 oa, ob;
-      gz_update2<RMAX>(r[0], va, r[UPL - 1], vb, R, reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3),
-                       reinterpret_cast<const uint4*>(rbase) + (lane + 32) * (R >> 3), sc, rcp, oa, ob);
+      gz_update2<RMAX>(r[0], va, d2v[0] >> 12, r[UPL - 1], vb, d2v[UPL - 1] >> 12, R,
+                       reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3),
+                       reinterpret_cast<const uint4*>(rbase) + (lane + 32) * (R >> 3), sc, rcp, padv, oa, ob);
       if (last) {  // owned vertices, final values of the pass
         if (va && (r[0].pb & 0x8000u)) a1[r[0].gid] = oa;
         if (vb && (r[UPL - 1].pb & 0x8000u)) a1[r[UPL - 1].gid] = ob;
@@ -1506,7 +1591,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
           const int nr4 = DIM == 3 ? (int)r4(reinterpret_cast<const uint32_t*>(buf)[1]) : 0;
           double ox, oy, oz;
           gz_update<DIM, RMAX>(r[u], R, reinterpret_cast<const uint4*>(rbase) + (lane + 32 * u) * (R >> 3), sc,
-                               rcp, nr4, ox, oy, oz);
+                               rcp, nr4, padv, DIM == 2 ? (d2v[u] >> 12) : 0, ox, oy, oz);
           if (last && (r[u].pb & 0x8000u)) {
             if (DIM == 2) {
               a1[r[u].gid] = make_double2(ox, oy);
@@ -1930,7 +2015,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   out->max_meta16 = mx[2];
   out->mean_meta16 = K > 0 ? meta16_all / K : 0;
   out->max_row = mx[3];
-  if (mx[0] > GZ_MAX_REGION || mx[1] > 65534) return false;
+  if (mx[0] + 8 > GZ_MAX_REGION || mx[1] > 65534) return false;  // + the 2D pad slots
   if (!fits(*out)) return false;
   mark("sizes");
   // the blobs
@@ -1951,7 +2036,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
     LMS_TRY_CUDA(cudaFuncSetAttribute(k_gzd_records, cudaFuncAttributeMaxDynamicSharedMemorySize, rid_bytes));
     k_gzd_records<<<(unsigned)std::min<int64_t>(K, 1 << 20), 256, rid_bytes, s>>>(
         K, it_ks.p, it_q.p, C, P, upl, kc_off.p, cntj.p, ck2.p, cv2.p, tab.p, sfirst.p, m->row_ptr.p, m->col.p,
-        tile_of.p, reg.p, reg_off.p, rec.p, it_lo.p, it_hi.p);
+        tile_of.p, reg.p, reg_off.p, rec.p, it_lo.p, it_hi.p, m->dim, (int)((mx[0] + 7) & ~7LL));
     LMS_CHECK_LAUNCH();
     DBuf<int> tneed(K > 0 ? K : 1, s);
     LMS_TRY_CUDA(cudaMemsetAsync(tneed.p, 0, (K > 0 ? K : 1) * sizeof(int), s));
@@ -2089,7 +2174,8 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   L->flag_off = L->hdr_bytes;
   L->cnt_off = L->flag_off + r16i(4 * nd.max_items);
   L->coord_off = (L->cnt_off + r16i(4 * (int64_t)P * C) + 127) & ~127;
-  const int64_t coords = dim == 2 ? 16 * nd.max_slots : 24 * r4(nd.max_slots);
+  L->padbase = (int)((nd.max_slots + 7) & ~(int64_t)7);  // 2D pad slots padbase .. padbase + 7
+  const int64_t coords = dim == 2 ? 16 * ((int64_t)L->padbase + 8) : 24 * r4(nd.max_slots);
   L->buf_bytes = (int)((L->coord_off + coords + 127) & ~(int64_t)127);
   L->stage_bytes = r16i(16 * nd.max_meta16);
   L->tiles_cap = tiles_cap;
@@ -2100,7 +2186,7 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
     L->NPW = (npw == 2 && nb % 2 == 0) ? 2 : 1;
     const int ctl = (2 * nb + 2 * L->RR + L->NPW) * 8 + (1 + 2 * nb + L->RR) * 4;
     L->off_rcp = r16i(ctl);
-    L->off_tab = L->off_rcp + r16i(8 * (GZ_RCP_MAX + 1));
+    L->off_tab = L->off_rcp + r16i(8 * (GZ_RCP_MAX + 1) + 4 * 32);  // + a word per warp (record release)
     const int tab_bytes = r16i((int64_t)tiles_cap * (8 + 4 + 4 + 4 + 4) + 4 * ((int64_t)tiles_cap + 1));
     L->off_stage = L->off_tab + tab_bytes;
     L->off_rec = L->off_stage + L->NPW * L->stage_bytes;
@@ -2309,6 +2395,17 @@ void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s) {
   }
   // the kernel's watchdog reports a stuck wait through the handle's error flag
   check_err_flag(m, s, "lms_smooth (GZ watchdog: a wait exceeded its budget)");
+#ifdef LMS_BOUNDS
+  int code = 0;
+  LMS_TRY_CUDA(cudaMemcpyFromSymbolAsync(&code, gz_bounds_code, sizeof(int), 0, cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  if (code) {
+    const int zero = 0;
+    LMS_TRY_CUDA(cudaMemcpyToSymbolAsync(gz_bounds_code, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+    fail(LMS_E_CUDA, "GZ bounds check failed: code " + std::to_string(code) +
+                         (code == -101 ? " (gather outside the region and pad slots)" : " (a pad slot is not -0.0)"));
+  }
+#endif
 }
 
 }  // namespace lms

@@ -103,6 +103,7 @@ struct GzLayout {
   int tiles_cap = 0;            // tiles per CTA (table size)
   int off_rcp = 0;              // RN(1/d) table for the division (d <= 32)
   int off_tab = 0, off_stage = 0, off_ring = 0;  // region offsets
+  int padbase = 0;              // 2D: first of the 8 pad slots of every region buffer
 };
 
 // ----------------------------------------------------------------- schedule
