@@ -83,6 +83,10 @@ constexpr uint16_t GZ_PAD = 0xFFFF;  // 3D row padding (predicated gathers)
 // each position is (d << 12) | dependency, d = 0 when d > 15 (count instead),
 // dependency 0xFFF = none (a tile with 4095+ items waits for whole stages).
 constexpr uint16_t GZ_DNONE = 0xFFF;
+#ifndef LMS_GZ_REGS
+#define LMS_GZ_REGS 96
+#endif
+constexpr int GZ_REGS2 = LMS_GZ_REGS;  // register budget of the 2D two-updates-per-lane sweep
 constexpr int GZ_MAX_REGION = 32767;  // slots are 15 bits (bit 15 = owned flag)
 // An item is U = 32 * UPL updates of one stage of one tile (UPL updates per
 // lane: 2 in 2D, 1 in 3D); its dependency list has at most U entries (more ->
@@ -882,6 +886,7 @@ struct GzGuard {
   volatile int* sabort; // CTA-local copy
   unsigned n = 0;
   unsigned long long t0 = 0;
+  int s0 = 20, s1 = 128;  // poll back-off (ns): first 64 polls, then
   __device__ void start() { n = 0; t0 = 0; }
   __device__ bool check() {
     if (*sabort || *(volatile int*)gabort) {
@@ -901,7 +906,11 @@ struct GzGuard {
   __device__ bool ok() {
     ++n;
     if ((n & 255) == 0 && !check()) return false;
-    __nanosleep(n < 64 ? 20 : 128);
+    if (n < 64) {
+      if (s0) __nanosleep(s0);
+    } else {
+      __nanosleep(s1);
+    }
     return true;
   }
   // for mbarrier waits: try_wait already suspends the thread in hardware
@@ -924,6 +933,14 @@ __device__ __forceinline__ bool mbar_wait_g(uint64_t* b, uint32_t parity, GzGuar
     if (done) return true;
     if (!g.ok_spin()) return false;
   }
+}
+// with an L2 cache policy (records and meta are streamed once per pass: evict_first)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -1211,7 +1228,7 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, int d
 template <int DIM, int RMAX, int UPL, bool STATS>
 // register budget per thread for the CTA's threads (2D 64-update items: 21
 // warps x 96; 32-update items: 25 x 80; 3D: 13 x 152)
-__global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
+__global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
                                                                       const GzTile* __restrict__ tab,
                                                                       const int32_t* __restrict__ item_sweep,
                                                                       const uint4* __restrict__ meta,
@@ -1306,6 +1323,8 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
   __syncthreads();
   const int total = t_pre[n_my];
   GzGuard guard{gabort, &s_abort};
+  guard.s0 = L.sleep0;
+  guard.s1 = L.sleep1;
 
   if (warp < NPW) {  // -------------------------------------------- region producers
     const long long p0 = STATS ? clock64() : 0;
@@ -1390,6 +1409,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
       // dependent lookups per batch made this thread the kernel's bottleneck
       const int BS = L.BS;
       const int nbat = (total + BS - 1) / BS;
+      const uint64_t pol_first = policy_evict_first();
       int ti = 0, lo = 0, hi = 0, r16 = 0;
       const uint4* tsrc = rec;  // record of claim lo
       auto load_tile = [&](int j) {
@@ -1428,7 +1448,10 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
           const uint32_t rb = (uint32_t)r16 * 16u;
           const uint4* src = tsrc + (long long)(kc - lo) * r16;
           if ((int)rb == L.rec_bytes) {
-            bulk_g2s(dst + (size_t)(kc - k0) * L.rec_bytes, src, (uint32_t)(kend - kc) * rb, rfull + slot);
+            if (L.hint_rec)
+              bulk_g2s_hint(dst + (size_t)(kc - k0) * L.rec_bytes, src, (uint32_t)(kend - kc) * rb, rfull + slot, pol_first);
+            else
+              bulk_g2s(dst + (size_t)(kc - k0) * L.rec_bytes, src, (uint32_t)(kend - kc) * rb, rfull + slot);
           } else {
             for (int q = kc; q < kend; ++q)
               bulk_g2s(dst + (size_t)(q - k0) * L.rec_bytes, src + (long long)(q - kc) * r16, rb, rfull + slot);
@@ -1462,7 +1485,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
     tb = t_buf[ti];
     buf = sm + L.off_ring + (size_t)(tb & 0xffff) * L.buf_bytes;
   };
-  unsigned long long w_wait = 0, w_dep = 0, w_comp = 0, w_items = 0;
+  unsigned long long w_wait = 0, w_dep = 0, w_comp = 0, w_items = 0, w_rec = 0;
   bool tile_ready = false;
   constexpr int U = 32 * UPL;  // updates per item; lane l handles positions l, l + 32
   const int bs_log2 = L.BS_log2;
@@ -1488,6 +1511,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
       guard.start();
       while (alive && rbat[slot] != bat) alive = guard.ok_spin();
       alive = alive && mbar_wait_g(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u, guard);
+      if (STATS) w_rec += clock64() - c0;
       if (alive && !tile_ready) {  // the region of the item's tile
         guard.start();
         while (alive && buf_tile[tb & 0xffff] != i) alive = guard.ok();
@@ -1624,6 +1648,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? 96 : 80) : 152) k_sweep_gz(co
     atomicAdd(stats + 1, w_dep);
     atomicAdd(stats + 2, w_comp);
     atomicAdd(stats + 3, w_items);
+    atomicAdd(stats + 8, w_rec);
   }
 }
 
@@ -2175,6 +2200,9 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   L->cnt_off = L->flag_off + r16i(4 * nd.max_items);
   L->coord_off = (L->cnt_off + r16i(4 * (int64_t)P * C) + 127) & ~127;
   L->padbase = (int)((nd.max_slots + 7) & ~(int64_t)7);  // 2D pad slots padbase .. padbase + 7
+  L->sleep0 = env_int("LMS_GZ_SLEEP0", 20, 0, 1000);
+  L->hint_rec = env_int("LMS_GZ_HINT", 0, 0, 1);
+  L->sleep1 = env_int("LMS_GZ_SLEEP1", 128, 0, 10000);
   const int64_t coords = dim == 2 ? 16 * ((int64_t)L->padbase + 8) : 24 * r4(nd.max_slots);
   L->buf_bytes = (int)((L->coord_off + coords + 127) & ~(int64_t)127);
   L->stage_bytes = r16i(16 * nd.max_meta16);
@@ -2217,7 +2245,7 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   // CTA's warps are spread over 4 schedulers, so at the kernel's register
   // budget (__maxnreg__) at most 20 warps (96 regs, 64-update items), 24 (80)
   // or 12 (3D, 152)
-  const int cap_warps = m->dim == 2 ? (upl == 2 ? 20 : 24) : 12;
+  const int cap_warps = m->dim == 2 ? (upl == 2 ? 65536 / (GZ_REGS2 * 32) : 24) : 12;
   const int maxw = cap_warps;  // producers + loader + workers
   // workers measured best on C4: 18 with 2 updates per lane, 22 with 1 (more
   // warps only lengthen every item: the shared-memory pipe is the shared
@@ -2298,8 +2326,8 @@ static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
   static unsigned long long* stats = nullptr;
   const bool want_stats = getenv("LMS_GZ_STATS") != nullptr;
   if (want_stats) {
-    if (!stats) LMS_TRY_CUDA(cudaMalloc(&stats, 8 * sizeof(unsigned long long)));
-    LMS_TRY_CUDA(cudaMemsetAsync(stats, 0, 8 * sizeof(unsigned long long), s));
+    if (!stats) LMS_TRY_CUDA(cudaMalloc(&stats, 9 * sizeof(unsigned long long)));
+    LMS_TRY_CUDA(cudaMemsetAsync(stats, 0, 9 * sizeof(unsigned long long), s));
   }
   const double2* a0 = DIM == 2 ? reinterpret_cast<const double2*>(m->xy[m->xy_cur].p) : nullptr;
   double2* a1 = DIM == 2 ? reinterpret_cast<double2*>(m->xy[1 - m->xy_cur].p) : nullptr;
@@ -2310,12 +2338,12 @@ static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
       want_stats ? stats : nullptr, m->err.p);
   LMS_CHECK_LAUNCH();
   if (want_stats) {
-    unsigned long long h[8];
+    unsigned long long h[9];
     LMS_TRY_CUDA(cudaMemcpyAsync(h, stats, sizeof(h), cudaMemcpyDeviceToHost, s));
     LMS_TRY_CUDA(cudaStreamSynchronize(s));
     const double it = h[3] ? (double)h[3] : 1.0;
-    fprintf(stderr, "[gz stats] per item cycles: wait_tile=%.0f wait_deps=%.0f compute=%.0f (items=%.0f)\n",
-            h[0] / it, h[1] / it, h[2] / it, it);
+    fprintf(stderr, "[gz stats] per item cycles: wait_tile=%.0f (record %.0f) wait_deps=%.0f compute=%.0f (items=%.0f)\n",
+            h[0] / it, h[8] / it, h[1] / it, h[2] / it, it);
     fprintf(stderr, "[gz stats] per CTA kcycles: producer wait_empty=%.1f of %.1f, record loader wait_empty=%.1f of %.1f\n",
             h[4] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid, h[7] / 1e3 / grid);
   }

@@ -104,6 +104,8 @@ struct GzLayout {
   int off_rcp = 0;              // RN(1/d) table for the division (d <= 32)
   int off_tab = 0, off_stage = 0, off_ring = 0;  // region offsets
   int padbase = 0;              // 2D: first of the 8 pad slots of every region buffer
+  int sleep0 = 20, sleep1 = 128;  // dependency-poll back-off (ns), first 64 polls / later
+  int hint_rec = 0;             // records TMA'd with an L2 evict_first policy
 };
 
 // ----------------------------------------------------------------- schedule
