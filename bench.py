@@ -78,8 +78,6 @@ def parse():
     p.add_argument("--cpu-sweeps", type=int, default=2)
     p.add_argument("--force-dist", action="store_true",
                    help="take the multi-GPU path even at one rank (tests its plumbing under torchrun)")
-    p.add_argument("--dist", default="auto", choices=["auto", "deep", "colour"],
-                   help="N>1: deep halo + GZ (2D default) or per-colour exchange + S1")
     return p.parse_args()
 
 
@@ -244,6 +242,9 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 or args.force_dist:
+        # communicator sizes in the log (the library's own NCCL communicator included)
+        os.environ["NCCL_DEBUG"] = "INFO"
+        os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -440,54 +441,57 @@ def run_ours(args):
 
 
 def run_ours_dist(args, m, cfg, sweeps, world, rank, dev):
-    """N > 1: contiguous vertex ranges of the relabelled mesh, one rank per GPU.
-    2D (default): deep halo -- C*P-hop ghost zones, one ghost exchange per
-    pass of P sweeps (NCCL send/recv over NVLink), the GZ kernel on each
-    rank's local mesh.  3D / --dist colour: per-colour exchange + S1 stages."""
+    """N > 1 (or --force-dist): the multi-GPU C ABI (include/lms.h lms_dist_*).
+    Every rank builds the mesh on its GPU (lms_build_csr), relabels it, and
+    calls lms_dist_create with the NCCL uid broadcast from rank 0: the
+    library builds the rank's plan from its own contiguous range
+    and owns the NCCL communicator.  One timed step = lms_smooth_dist(sweeps):
+    per pass of P sweeps one halo exchange (ncclSend/ncclRecv over NVLink),
+    then the GZ pass on the rank's local mesh.  Weak/strong: the mesh is
+    fixed, so this is strong scaling; value = all ranks' updates / max time."""
     import torch
     import torch.distributed as dist
 
     import paper_1606_00803_b200 as lms
-    from paper_1606_00803_b200.dist import (CudaLocal, CudaLocalDeep, DeepPlan, Plan, smooth_dist,
-                                            smooth_dist_deep)
     stream = torch.cuda.current_stream()
     dim, V = m["dim"], m.V
-    gm = lms.Mesh.build_csr([torch.from_numpy(c).to(dev) for c in m["coords"]], torch.from_numpy(m["elems"]).to(dev))
-    gm.permute(gm.order(args.ordering, meshgen.RANDOM_ORDER_SEED if args.ordering == "random" else 0))
-    rp, col = gm.csr()
-    fixed, colour = gm.fixed().cpu().numpy(), gm.colour().cpu().numpy()
-    coords = [c.cpu().numpy() for c in gm.coords()]
+    P = max(1, args.lag)
+    seed = meshgen.RANDOM_ORDER_SEED if args.ordering == "random" else 0
+
+    def uid():
+        obj = [lms.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def make_dist(g):
+        g.permute(g.order(args.ordering, seed))
+        return lms.Dist.create(g, rank, world, uid(), sweeps_per_exchange=P, tile=args.tile)
+
+    coords_d = [torch.from_numpy(c).to(dev) for c in m["coords"]]
+    elems_d = torch.from_numpy(m["elems"]).to(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    gm = lms.Mesh.build_csr(coords_d, elems_d)
     info = gm.info()
+    vfree = gm.schedule_info()["n_free"]
+    d = make_dist(gm)
     gm.close()
-    deep = args.dist == "deep" or (args.dist == "auto" and dim == 2)
-    P = max(1, args.lag) if deep else 0
-    if deep:
-        plan = DeepPlan(rp.cpu().numpy(), col.cpu().numpy(), fixed, colour, world, info["C"] * P)
-        rplan = plan.rank_plan(rank)
-        local = CudaLocalDeep(rplan, coords, dev, P=P, tile=args.tile)
-        step = lambda: smooth_dist_deep(local, rplan, sweeps, P)  # noqa: E731
-        how = f"contiguous vertex ranges x{world}, deep halo ({info['C'] * P} hops), one exchange per {P}-sweep pass"
-        kname = "k_sweep_gz + halo pack/unpack"
-    else:
-        plan = Plan(rp.cpu().numpy(), col.cpu().numpy(), fixed, colour, world)
-        rplan = plan.rank_plan(rank)
-        local = CudaLocal(rplan, coords, dev)
-        step = lambda: smooth_dist(local, rplan, plan.C, sweeps)  # noqa: E731
-        how = f"contiguous vertex ranges x{world}, per-colour halo exchange (NCCL p2p)"
-        kname = "k_sweep_s1 (per colour) + halo pack/unpack"
-    vfree = int((fixed == 0).sum())
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    dinfo = d.info()
     bsw = b_sweep(dim, V, info["nnz"], vfree)
     for _ in range(args.warmup):
-        step()
+        d.smooth(sweeps)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
     launches0 = lms.kernel_launches()
     with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
-        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(args.steps):
-            step()
+            d.smooth(sweeps)
         b.record(stream)
         torch.cuda.synchronize()
     launches = lms.kernel_launches() - launches0
@@ -496,22 +500,69 @@ def run_ours_dist(args, m, cfg, sweeps, world, rank, dev):
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_ms = float(tt.item())
     value = vfree * sweeps * args.steps / (t_ms / 1e3)
+    # e2e: per step every rank ingests the mesh from pinned host buffers,
+    # builds, orders, relabels, re-plans (lms_dist_replan: the communicator
+    # is a once-per-job set-up, kept), smooths and reads its owned result back
+    e2e = None
+    if not args.no_e2e:
+        del coords_d, elems_d
+        hc = [torch.from_numpy(c).pin_memory() for c in m["coords"]]
+        he = torch.from_numpy(m["elems"]).pin_memory()
+        first, count = None, None
+
+        first_, count_ = d.owned_range()
+        outs = [torch.empty(count_, dtype=torch.float64).pin_memory() for _ in range(dim)]
+
+        def e2e_step():
+            g = lms.Mesh.build_csr_host(hc, he)
+            g.permute(g.order(args.ordering, seed))
+            d.replan(g, tile=args.tile)
+            g.close()
+            d.smooth(sweeps)
+            f, xs = d.export_owned()
+            for o, x in zip(outs, xs):
+                o.copy_(x, non_blocking=True)
+            torch.cuda.synchronize()
+            return f, xs[0].numel()
+        for _ in range(2):
+            first, count = e2e_step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        n_e2e = max(2, min(args.steps, 3))
+        ea = torch.cuda.Event(enable_timing=True)
+        eb = torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        e_ms = ea.elapsed_time(eb) / n_e2e
+        et = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item())
+        h2d = sum(c.nbytes for c in m["coords"]) + m["elems"].nbytes
+        e2e = {"value": vfree * sweeps / (e_ms / 1e3), "unit": "vertex-updates/s", "h2d_bytes_per_step": h2d,
+               "note": "host buffers are the whole mesh on every rank (each rank builds the full mesh)",
+               "d2h_bytes_per_step": 8 * dim * count, "ms_per_step": e_ms, "steps": n_e2e,
+               "path": "per rank: build_csr_host (whole mesh) -> order -> permute -> lms_dist_replan (plan + NCCL "
+                       "ghost lists) -> lms_smooth_dist(%d) -> lms_dist_export_owned -> D2H; max over ranks" % sweeps}
+    d.close()
     peak, peak_src = peaks()
     achieved = bsw * sweeps * args.steps / (t_ms / 1e3) / 1e9 / world
     if rank == 0:
+        how = (f"contiguous vertex ranges x{world} (lms_dist_*), deep halo {dinfo['depth']} hops, one NCCL "
+               f"exchange per {P}-sweep pass")
         line = {
-            "metric": "vertex-updates/sec per LMS sweep (and % of HBM roofline)",
+            "metric": METRIC,
             "value": value, "unit": "vertex-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfg['args']}, {args.ordering} ordering, {sweeps} sweeps per step",
-                       "config": args.config, "ordering": args.ordering, "sweeps_per_step": sweeps,
-                       "V": V, "V_free": vfree, "nnz": info["nnz"], "colours": plan.C,
-                       "parallelism": how, "l2": "inputs larger than L2; no flush"},
+            "config": workload_config(args, cfg, sweeps, V, vfree, info["nnz"], info["C"], dim, world, how),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-                         "kernel": kname, "per_gpu": True},
-            "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk.record(),
+                         "kernel": "k_sweep_gz + halo pack/unpack (per GPU)", "per_gpu": True},
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk.record(),
+            "dist": dict(dinfo, plan_s_rank0=plan_s),
         }
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -275,6 +275,10 @@ lms_status lms_smooth_until(lms_mesh_t m, double goal, double eps, int32_t max_s
  *  O(V) memsets and one O(V) scan, O(V/P + halo) otherwise.  `m` is only read:
  *  it may be destroyed afterwards.  sweeps_per_exchange in [1, 8]; tile = the
  *  local GZ tile (0 = default).  *out is a new handle (lms_dist_destroy).
+ * lms_dist_replan -- a new mesh (same rank / nranks, every rank calls it)
+ *  on the handle's existing communicator: the plan is rebuilt as in
+ *  lms_dist_create, without a new ncclCommInitRank (communicator set-up is a
+ *  once-per-job cost).  The previous plan and local mesh are released.
  * lms_smooth_dist -- `sweeps` colour-GS sweeps (Eq. 1): per pass
  *  of up to sweeps_per_exchange sweeps, pack -> grouped ncclSend/ncclRecv
  *  on `stream` -> unpack, then the local pass.  Collective: every rank calls
@@ -296,6 +300,7 @@ typedef struct lms_dist_s* lms_dist_t;
 lms_status lms_nccl_unique_id(uint8_t out[128]);
 lms_status lms_dist_create(lms_mesh_t m, int32_t rank, int32_t nranks, const uint8_t nccl_uid[128],
                            int32_t sweeps_per_exchange, int32_t tile, lms_stream_t stream, lms_dist_t* out);
+lms_status lms_dist_replan(lms_dist_t d, lms_mesh_t m, int32_t tile, lms_stream_t stream);
 lms_status lms_smooth_dist(lms_dist_t d, int32_t sweeps, lms_stream_t stream);
 lms_status lms_dist_export_owned(lms_dist_t d, double* const* d_out, int64_t* first, int64_t* count,
                                  lms_stream_t stream);

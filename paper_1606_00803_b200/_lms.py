@@ -31,7 +31,7 @@ EXPORTS = ["lms_build_csr", "lms_build_csr_host", "lms_mesh_from_csr", "lms_mesh
            "lms_export_quality", "lms_last_error", "lms_kernel_launches", "lms_cache_release", "lms_set_allocator", "lms_set_tiling", "lms_schedule_info2",
            "lms_smooth_colour", "lms_gather_coords", "lms_scatter_coords",
            "lms_global_quality", "lms_smooth_until",
-           "lms_nccl_unique_id", "lms_dist_create", "lms_smooth_dist", "lms_dist_export_owned", "lms_dist_info",
+           "lms_nccl_unique_id", "lms_dist_create", "lms_dist_replan", "lms_smooth_dist", "lms_dist_export_owned", "lms_dist_info",
            "lms_dist_export_local_ids", "lms_dist_create_local", "lms_smooth_dist_local", "lms_dist_destroy"]
 
 
@@ -86,6 +86,7 @@ def load_library(build: bool = True):
         "lms_nccl_unique_id": [P],
         "lms_dist_create": [P, i32, i32, P, i32, i32, P, ct.POINTER(P)],
         "lms_smooth_dist": [P, i32, P],
+        "lms_dist_replan": [P, P, i32, P],
         "lms_dist_export_owned": [P, PP, ct.POINTER(i64), ct.POINTER(i64), P],
         "lms_dist_info": [P, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i32), ct.POINTER(i32)],
         "lms_dist_export_local_ids": [P, P, P],
@@ -447,6 +448,10 @@ class Dist:
 
     def smooth(self, sweeps: int, stream=None):
         _check(lib().lms_smooth_dist(self._h, sweeps, _stream(stream)), "lms_smooth_dist")
+
+    def replan(self, mesh: "Mesh", tile: int = 0, stream=None):
+        """lms_dist_replan: a new mesh on the same NCCL communicator (collective)."""
+        _check(lib().lms_dist_replan(self._h, mesh._h, tile, _stream(stream)), "lms_dist_replan")
 
     def owned_range(self):
         f, c = ct.c_int64(), ct.c_int64()

@@ -552,6 +552,28 @@ lms_status lms_dist_create(lms_mesh_t m, int32_t rank, int32_t nranks, const uin
   }
 }
 
+lms_status lms_dist_replan(lms_dist_t d, lms_mesh_t m, int32_t tile, lms_stream_t stream) {
+  try {
+    if (!d || !m) fail(LMS_E_ARG, "NULL argument");
+    if (d->local_group) fail(LMS_E_STATE, "lms_dist_replan: not for local-group handles");
+    if (m->device != d->device) fail(LMS_E_ARG, "lms_dist_replan: the mesh is on another device");
+    DevGuard dg(m);
+    cudaStream_t s = (cudaStream_t)stream;
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));  // the previous plan's work is done before it is freed
+    if (d->local) lms_mesh_destroy(d->local);
+    d->local = nullptr;
+    d->peers.clear();
+    d->local_ids.release();
+    plan_rank(m, d, tile, s);
+    if (d->nranks > 1) exchange_lists(d, s);
+    finish(d, s);
+    return LMS_OK;
+  } catch (const Err& e) {
+    set_error(e.msg);
+    return e.st;
+  }
+}
+
 lms_status lms_dist_create_local(lms_mesh_t m, int32_t nranks, int32_t sweeps_per_exchange, int32_t tile,
                                  lms_stream_t stream, lms_dist_t* outs) {
   std::vector<lms_dist_s*> ds;

@@ -2245,7 +2245,9 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   // CTA's warps are spread over 4 schedulers, so at the kernel's register
   // budget (__maxnreg__) at most 20 warps (96 regs, 64-update items), 24 (80)
   // or 12 (3D, 152)
-  const int cap_warps = m->dim == 2 ? (upl == 2 ? 65536 / (GZ_REGS2 * 32) : 24) : 12;
+  // (one warp below the register file's quotient: 21 x 96 registers fails
+  // to launch with "too many resources")
+  const int cap_warps = m->dim == 2 ? (upl == 2 ? 65536 / (GZ_REGS2 * 32) - 1 : 24) : 12;
   const int maxw = cap_warps;  // producers + loader + workers
   // workers measured best on C4: 18 with 2 updates per lane, 22 with 1 (more
   // warps only lengthen every item: the shared-memory pipe is the shared

@@ -131,3 +131,27 @@ def test_dist_errors():
         with pytest.raises(lms.LMSError) as e:
             lms.Dist.create(gm, 0, 1, uid, sweeps_per_exchange=9)
         assert e.value.name == "LMS_E_ARG"
+
+
+def test_nccl_replan_new_mesh():
+    """lms_dist_replan: a second mesh on the same communicator, bit-exact."""
+    uid = lms.nccl_unique_id()
+    m1 = meshgen.grid2d(90, 70, 0.3, seed=14)
+    pm1, g1 = _setup(m1, "original")
+    d = lms.Dist.create(g1, 0, 1, uid)
+    g1.close()
+    try:
+        d.smooth(2)
+        _, xs = d.export_owned()
+        want1 = oracle.smooth(pm1["coords"], pm1["row_ptr"], pm1["col"], pm1["colour"], pm1["C"], 2)
+        assert bits_equal([np_(x) for x in xs], want1)
+        m2 = meshgen.grid2d(130, 50, 0.3, seed=15)
+        pm2, g2 = _setup(m2, "bfs")
+        d.replan(g2)
+        g2.close()
+        d.smooth(3)
+        first, xs = d.export_owned()
+        want2 = oracle.smooth(pm2["coords"], pm2["row_ptr"], pm2["col"], pm2["colour"], pm2["C"], 3)
+        assert first == 0 and bits_equal([np_(x) for x in xs], want2)
+    finally:
+        d.close()
