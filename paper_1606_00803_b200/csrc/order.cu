@@ -190,65 +190,84 @@ __global__ void k_free_qkeys(const uint8_t* __restrict__ fixed, const double* __
   }
 }
 
+// The walk keeps Alg. 2's two flags as one state byte per vertex (0 = not
+// sorted, 1 = sorted, 2 = processed; processed implies sorted).  Only this
+// warp reads and writes them, so they are plain (L1-cached) accesses ordered
+// by __syncwarp, not volatile L2 round trips.  A step over `cur` loads, per
+// lane, one presorted neighbour u, its state and its row bounds in ONE round
+// of independent loads; the next vertex l0 = l[0] then has its row bounds in
+// a register already, so a step costs two dependent rounds (the row, then its
+// states and bounds) instead of four.
 __global__ void k_rdr_walk(const int32_t* __restrict__ rp, const int32_t* __restrict__ scol,
-                           const int32_t* __restrict__ outer, int64_t n_outer, uint8_t* processed,
-                           uint8_t* sorted, int32_t* perm, long long* stats /* [next, walks] */) {
+                           const int32_t* __restrict__ outer, int64_t n_outer, uint8_t* st,
+                           int32_t* perm, long long* stats /* [next, walks] */) {
   const int lane = threadIdx.x;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
   long long next = 0, walks = 0;
-  volatile uint8_t* P = processed;
-  volatile uint8_t* S = sorted;
   int64_t oi = 0;
   while (oi < n_outer) {
     const int64_t idx = oi + lane;
-    const int32_t i_l = idx < n_outer ? outer[idx] : -1;
-    const int p_l = i_l >= 0 ? P[i_l] : 1;
-    const unsigned bal = __ballot_sync(FULL, p_l == 0);
+    const int32_t i_l = idx < n_outer ? __ldg(outer + idx) : -1;
+    const int p_l = i_l >= 0 ? st[i_l] : 2;
+    const unsigned bal = __ballot_sync(FULL, p_l < 2);
     if (bal == 0) { oi += 32; continue; }
     const int first = __ffs(bal) - 1;
     const int32_t i = __shfl_sync(FULL, i_l, first);
+    const int si = __shfl_sync(FULL, p_l, first);
     oi += first + 1;
-    // Alg. 2 lines: if not sorted[i]: append; processed[i] <- True
-    const int si = S[i];
+    // Alg. 2: if not sorted[i]: append i; processed[i] <- True
     if (lane == 0) {
-      if (!si) { perm[next] = i; S[i] = 1; }
-      P[i] = 1;
+      if (si == 0) perm[next] = i;
+      st[i] = 2;
     }
-    next += si ? 0 : 1;
+    next += si == 0 ? 1 : 0;
     ++walks;
-    __syncwarp();
     int32_t cur = i;
+    int32_t b = __ldg(rp + cur), e = __ldg(rp + cur + 1);
+    __syncwarp();
     for (;;) {
-      const int32_t b = rp[cur], e = rp[cur + 1];
-      int32_t l0 = -1;
+      int32_t l0 = -1, nb = 0, ne = 0;
       for (int32_t base = b; base < e; base += 32) {
         const int32_t j = base + lane;
-        const int32_t u = j < e ? scol[j] : -1;
-        const int pu = u >= 0 ? P[u] : 1;
-        const int su = u >= 0 ? S[u] : 1;
-        const unsigned unp = __ballot_sync(FULL, pu == 0);
-        if (unp && l0 < 0) l0 = __shfl_sync(FULL, u, __ffs(unp) - 1);
-        const unsigned app = __ballot_sync(FULL, pu == 0 && su == 0);
-        if (pu == 0 && su == 0) {
+        const int32_t u = j < e ? __ldg(scol + j) : -1;
+        int su = 2;
+        int32_t ub = 0, ue = 0;
+        if (u >= 0) {  // one round of independent loads: state and row bounds
+          su = st[u];
+          ub = __ldg(rp + u);
+          ue = __ldg(rp + u + 1);
+        }
+        const unsigned unp = __ballot_sync(FULL, su < 2);
+        if (unp && l0 < 0) {
+          const int src = __ffs(unp) - 1;
+          l0 = __shfl_sync(FULL, u, src);
+          nb = __shfl_sync(FULL, ub, src);
+          ne = __shfl_sync(FULL, ue, src);
+        }
+        const unsigned app = __ballot_sync(FULL, su == 0);
+        if (su == 0) {
           perm[next + __popc(app & lt)] = u;
-          S[u] = 1;
+          st[u] = 1;
         }
         next += __popc(app);
       }
-      __syncwarp();
       if (l0 < 0) break;
-      if (lane == 0) P[l0] = 1;
+      __syncwarp();
+      if (lane == 0) st[l0] = 2;
       __syncwarp();
       cur = l0;
+      b = nb;
+      e = ne;
     }
+    __syncwarp();
   }
   if (lane == 0) { stats[0] = next; stats[1] = walks; }
 }
 
-__global__ void k_unsorted_flags(const uint8_t* __restrict__ sorted, int64_t V, uint8_t* flags, int32_t* ids) {
+__global__ void k_state_unsorted(const uint8_t* __restrict__ st, int64_t V, uint8_t* flags, int32_t* ids) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
-    flags[v] = sorted[v] ? 0 : 1;
+    flags[v] = st[v] == 0 ? 1 : 0;
     ids[v] = (int32_t)v;
   }
 }
@@ -290,11 +309,10 @@ void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s) {
     LMS_TRY_CUDA(cudaStreamSynchronize(s));
     n_outer = hn;
   }
-  DBuf<uint8_t> processed(V, s), sorted(V, s);
-  LMS_TRY_CUDA(cudaMemsetAsync(processed.p, 0, V, s));
-  LMS_TRY_CUDA(cudaMemsetAsync(sorted.p, 0, V, s));
+  DBuf<uint8_t> state(V, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(state.p, 0, V, s));
   DBuf<long long> stats(2, s);
-  k_rdr_walk<<<1, 32, 0, s>>>(m->row_ptr.p, scol.p, outer.p, n_outer, processed.p, sorted.p, d_perm, stats.p);
+  k_rdr_walk<<<1, 32, 0, s>>>(m->row_ptr.p, scol.p, outer.p, n_outer, state.p, d_perm, stats.p);
   LMS_CHECK_LAUNCH();
   long long hs[2] = {0, 0};
   LMS_TRY_CUDA(cudaMemcpyAsync(hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
@@ -303,7 +321,7 @@ void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s) {
     DBuf<uint8_t> flags(V, s);
     DBuf<int32_t> ids(V, s);
     DBuf<int> nsel(1, s);
-    k_unsorted_flags<<<Gv, 256, 0, s>>>(sorted.p, V, flags.p, ids.p);
+    k_state_unsorted<<<Gv, 256, 0, s>>>(state.p, V, flags.p, ids.p);
     LMS_CHECK_LAUNCH();
     size_t tb = 0;
     LMS_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, ids.p, flags.p, d_perm + hs[0], nsel.p, V, s));
