@@ -70,6 +70,9 @@ def lib():
         L.o_smooth_partitioned.argtypes = [i32, i64, P, P, P, P, i32, i32, i32, P]
         L.o_smooth_jacobi.argtypes = [i32, i64, P, P, P, P, i32]
         L.o_smooth_seq.argtypes = [i32, i64, P, P, P, P, i32]
+        L.o_trace.argtypes = [i64, P, P, P, P]
+        L.o_trace.restype = i64
+        L.o_reuse_distance.argtypes = [i64, P, i64, P]
         L.o_free.argtypes = [P]
         _lib = L
     return _lib
@@ -373,3 +376,90 @@ def smooth_until(coords, mesh: dict, goal: float, eps: float, max_sweeps: int, m
         qs.append(global_quality_exact(quality(X, el)))
         if qs[k] - qs[k - 1] < eps:
             return X, qs, STOP_CONVERGED
+
+
+# --------------------------------------------------------------------------- N2 reuse distance
+def trace(row_ptr, col, fixed) -> np.ndarray:
+    """Canonical access trace of one sequential sweep (Alg. 1's loop, P:211-214;
+    SPEC trace_iteration): per free vertex v in storage order: v, N(v) in CSR
+    order, v."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    fixed = np.ascontiguousarray(fixed, dtype=np.uint8)
+    V = row_ptr.shape[0] - 1
+    n = lib().o_trace(V, _p(row_ptr), _p(col), _p(fixed), None)
+    out = np.zeros(max(n, 1), dtype=np.int32)
+    lib().o_trace(V, _p(row_ptr), _p(col), _p(fixed), _p(out))
+    return out[:n]
+
+
+def reuse_distance(tr, n_ids: int | None = None) -> np.ndarray:
+    """Reuse distance of every access (P:183-186), -1 = COLD (first access);
+    Fenwick-tree algorithm (SPEC reuse_distances)."""
+    tr = np.ascontiguousarray(tr, dtype=np.int32)
+    n_ids = int(tr.max()) + 1 if n_ids is None and tr.size else (n_ids or 0)
+    out = np.zeros(max(tr.shape[0], 1), dtype=np.int64)
+    _chk(lib().o_reuse_distance(tr.shape[0], _p(tr), n_ids, _p(out)), "o_reuse_distance")
+    return out[:tr.shape[0]]
+
+
+def reuse_distance_brute(tr) -> np.ndarray:
+    """SPEC reuse_distances_oracle: direct set counting between occurrences
+    (quadratic; small traces only)."""
+    last, out = {}, []
+    for t, x in enumerate(tr):
+        x = int(x)
+        if x in last:
+            out.append(len(set(int(y) for y in tr[last[x] + 1:t])))
+        else:
+            out.append(-1)
+        last[x] = t
+    return np.array(out, dtype=np.int64)
+
+
+def quantile(dist, q: float) -> int:
+    """Table III quantile ("the smallest value such that there at
+    least a proportion X of the population below it"), over the finite
+    distances: the smallest v with |{d <= v}| / |finite| >= q."""
+    d = np.sort(np.asarray(dist)[np.asarray(dist) >= 0])
+    if d.size == 0:
+        raise ValueError("no finite distances")
+    import math
+    k = max(1, math.ceil(q * d.size - 1e-12))  # need at least k values <= v
+    return int(d[k - 1])
+
+
+def mean_distance(dist) -> float:
+    d = np.asarray(dist)
+    d = d[d >= 0]
+    if d.size == 0:
+        raise ValueError("no finite distances")
+    return float(d.mean())
+
+
+def element_capacity(cache_bytes: int, element_bytes: int = 66) -> int:
+    """a node of ~66 bytes; below a reuse distance of
+    cache_bytes / 66 elements there is no miss (floor; SPEC element_capacity)."""
+    if element_bytes < 1:
+        raise ValueError("element_bytes >= 1")
+    return cache_bytes // element_bytes
+
+
+def miss_model(dist, capacities):
+    """Reuse-based misses per level (P:183-193 model: distance >= capacity
+    misses; SPEC model_misses) and the cold accesses."""
+    d = np.asarray(dist)
+    fin = d[d >= 0]
+    n = [int((fin >= e).sum()) for e in capacities]
+    return n, int((d < 0).sum())
+
+
+def eq2_cost(n_access: int, n_miss, latencies) -> float:
+    """Eq. 2: (m1 c2 + m1 m2 c3 + m1 m2 m3 cm) * #accesses with
+    m1 = n1/#accesses, m2 = n2/n1, m3 = n3/n2 (conditional rates)."""
+    n1, n2, n3 = n_miss
+    c2, c3, cm = latencies
+    m1 = n1 / n_access if n_access else 0.0
+    m2 = n2 / n1 if n1 else 0.0
+    m3 = n3 / n2 if n2 else 0.0
+    return (m1 * c2 + m1 * m2 * c3 + m1 * m2 * m3 * cm) * n_access

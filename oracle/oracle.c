@@ -35,6 +35,8 @@
  *                        convergence loop is oracle/__init__.py global_quality_exact)
  *   o_smooth_jacobi      N3: Jacobi variant, snapshot reads
  *   o_smooth_seq         N3: Alg. 1 literally, storage-order in-place GS
+ *   o_trace              N2: canonical access trace of one sequential sweep
+ *   o_reuse_distance     N2: reuse distance of every access, Fenwick
  *
  * Parity pins for every function live in tests/test_oracle_*.py.
  *
@@ -593,5 +595,62 @@ int o_smooth_seq(int32_t dim, int64_t V, double* const* X, const int64_t* row_pt
                 X[a][v] = acc / (double)(e - b);
             }
         }
+    return O_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* N2: the paper's reuse-distance instrument (Sec. 3.1; Table III,
+ * P:646-702).  o_trace: the canonical access trace of ONE sequential sweep
+ * (Alg. 1's loop over interior vertices) at vertex granularity
+ * (SPEC trace_iteration): for each free vertex v in storage order: v, its
+ * neighbours in CSR order, v again (the write of Eq. 1).  Returns the length;
+ * trace may be NULL (length only).                                           */
+int64_t o_trace(int64_t V, const int64_t* row_ptr, const int32_t* col, const uint8_t* fixed, int32_t* trace) {
+    int64_t n = 0;
+    for (int64_t v = 0; v < V; ++v) {
+        if (fixed[v]) continue;
+        if (trace) trace[n] = (int32_t)v;
+        ++n;
+        for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
+            if (trace) trace[n] = col[e];
+            ++n;
+        }
+        if (trace) trace[n] = (int32_t)v;
+        ++n;
+    }
+    return n;
+}
+
+/* Reuse distance of every access ("between two accesses to the same
+ * data, what are the number of distinct piece of data that were accessed"):
+ * the number of DISTINCT elements accessed since the previous access to the
+ * same element, -1 (COLD) for a first access.  The O(N log N) algorithm of
+ * SPEC reuse_distances: last-access times, and a Fenwick tree over time
+ * holding a 1 at the last access of every element seen so far; the distance
+ * of access t to an element last seen at time p is the number of 1s in
+ * (p, t).  n_ids bounds the element identifiers.                             */
+int o_reuse_distance(int64_t n, const int32_t* trace, int64_t n_ids, int64_t* dist) {
+    int64_t* last = (int64_t*)malloc((size_t)(n_ids > 0 ? n_ids : 1) * sizeof(int64_t));
+    int64_t* bit = (int64_t*)calloc((size_t)n + 1, sizeof(int64_t));
+    if (!last || !bit) { free(last); free(bit); return O_E_NOMEM; }
+    for (int64_t k = 0; k < n_ids; ++k) last[k] = -1;
+    for (int64_t t = 0; t < n; ++t) {
+        int32_t x = trace[t];
+        if (x < 0 || x >= n_ids) { free(last); free(bit); return O_E_INDEX; }
+        int64_t p = last[x];
+        if (p < 0) {
+            dist[t] = -1;
+        } else {
+            /* ones in (p, t) = prefix(t - 1) - prefix(p) (Fenwick prefix sums, 1-based) */
+            int64_t a = 0, b = 0;
+            for (int64_t i = t; i > 0; i -= i & (-i)) a += bit[i];
+            for (int64_t i = p + 1; i > 0; i -= i & (-i)) b += bit[i];
+            dist[t] = a - b;
+            for (int64_t i = p + 1; i <= n; i += i & (-i)) bit[i] -= 1;  /* p is no longer a last access */
+        }
+        for (int64_t i = t + 1; i <= n; i += i & (-i)) bit[i] += 1;
+        last[x] = t;
+    }
+    free(last); free(bit);
     return O_OK;
 }
