@@ -312,6 +312,37 @@ lms_status lms_dist_create_local(lms_mesh_t m, int32_t nranks, int32_t sweeps_pe
 lms_status lms_smooth_dist_local(lms_dist_t* ds, int32_t nranks, int32_t sweeps, lms_stream_t stream);
 void lms_dist_destroy(lms_dist_t d);
 
+/* ---------------------------------------------------------------------------
+ * The paper's reuse-distance instrument (Fig. 1
+ * P:64-69, Table III, Eq. 2).
+ *
+ * lms_trace -- the canonical access trace of ONE sequential sweep of the mesh
+ *  in its current storage order (Alg. 1's loop over interior vertices,
+ *  P:211-214; SPEC trace_iteration): for each free vertex v in storage order:
+ *  v, its neighbours in CSR order, v again (the write of Eq. 1).  Elements are
+ *  vertex labels.  d_trace: int32[*n_out] device buffer, or NULL to query the
+ *  length only (*n_out = sum over free v of deg(v) + 2).  Synchronises.
+ * lms_reuse_distance -- d_dist[t] (int64, device) = the number of DISTINCT
+ *  elements accessed between access t and the previous access to the same
+ *  element, -1 if t is the element's first access (COLD).
+ *  d_trace int32[n] with identifiers in [0, n_ids) (else LMS_E_INDEX);
+ *  n < 2^31.  Exact (a wavelet matrix of previous-access times on the GPU).
+ *  Synchronises.
+ * lms_reuse_stats -- over the finite distances of d_dist[n]: for each of the
+ *  nq proportions h_q[k] in (0, 1], h_quantile[k] = the smallest value v with
+ *  at least a proportion h_q[k] of the distances <= v; *h_mean =
+ *  their mean; *h_n_cold = the number of -1 entries; for each of the ncap
+ *  capacities h_capacity[k], h_n_ge[k] = the number of distances >= it (the
+ *  model's reuse misses for a cache holding that many elements).  Host
+ *  outputs; NULL outputs are skipped.  LMS_E_STATE if quantiles or counts are
+ *  asked of a trace with no finite distance.  Synchronises. */
+lms_status lms_trace(lms_mesh_t m, int32_t* d_trace, int64_t* n_out, lms_stream_t stream);
+lms_status lms_reuse_distance(const int32_t* d_trace, int64_t n, int64_t n_ids, int64_t* d_dist,
+                              lms_stream_t stream);
+lms_status lms_reuse_stats(const int64_t* d_dist, int64_t n, const double* h_q, int32_t nq, int64_t* h_quantile,
+                           double* h_mean, int64_t* h_n_cold, const int64_t* h_capacity, int32_t ncap,
+                           int64_t* h_n_ge, lms_stream_t stream);
+
 /* Thread-local message for the last non-OK status of this thread. */
 const char* lms_last_error(void);
 /* Number of CUDA kernels this library launched on this thread since load

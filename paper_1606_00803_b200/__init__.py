@@ -8,8 +8,8 @@ if the CUDA library or a GPU is missing, calls raise.
 """
 from ._lms import (  # noqa: F401
     Dist, LMSError, Mesh, ORDERINGS, SCHEDULES, cache_release, lib, load_library, kernel_launches, nccl_unique_id,
-    use_torch_allocator,
+    reuse_distance, reuse_stats, use_torch_allocator,
 )
 
 __all__ = ["Dist", "LMSError", "Mesh", "ORDERINGS", "SCHEDULES", "cache_release", "lib", "load_library",
-           "kernel_launches", "nccl_unique_id", "use_torch_allocator"]
+           "kernel_launches", "nccl_unique_id", "reuse_distance", "reuse_stats", "use_torch_allocator"]

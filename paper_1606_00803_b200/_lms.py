@@ -32,7 +32,8 @@ EXPORTS = ["lms_build_csr", "lms_build_csr_host", "lms_mesh_from_csr", "lms_mesh
            "lms_smooth_colour", "lms_gather_coords", "lms_scatter_coords",
            "lms_global_quality", "lms_smooth_until",
            "lms_nccl_unique_id", "lms_dist_create", "lms_dist_replan", "lms_smooth_dist", "lms_dist_export_owned", "lms_dist_info",
-           "lms_dist_export_local_ids", "lms_dist_create_local", "lms_smooth_dist_local", "lms_dist_destroy"]
+           "lms_dist_export_local_ids", "lms_dist_create_local", "lms_smooth_dist_local", "lms_dist_destroy",
+           "lms_trace", "lms_reuse_distance", "lms_reuse_stats"]
 
 
 class LMSError(RuntimeError):
@@ -93,6 +94,9 @@ def load_library(build: bool = True):
         "lms_dist_create_local": [P, i32, i32, i32, P, ct.POINTER(P)],
         "lms_smooth_dist_local": [ct.POINTER(P), i32, i32, P],
         "lms_dist_destroy": [P],
+        "lms_trace": [P, P, ct.POINTER(i64), P],
+        "lms_reuse_distance": [P, i64, i64, P, P],
+        "lms_reuse_stats": [P, i64, P, i32, P, ct.POINTER(ct.c_double), ct.POINTER(i64), P, i32, P, P],
         "lms_last_error": [],
         "lms_kernel_launches": [],
         "lms_cache_release": [],
@@ -327,6 +331,14 @@ class Mesh:
                                       _stream(stream)), "lms_smooth_until")
         return k.value, [hist[i] for i in range(k.value + 1)], STOP_REASONS[why.value]
 
+    def trace(self, stream=None) -> torch.Tensor:
+        """lms_trace: the canonical access trace of one sequential sweep (int32 CUDA tensor)."""
+        n = ct.c_int64()
+        _check(lib().lms_trace(self._h, None, ct.byref(n), _stream(stream)), "lms_trace")
+        out = torch.empty(max(n.value, 1), dtype=torch.int32, device="cuda")
+        _check(lib().lms_trace(self._h, ct.c_void_p(out.data_ptr()), ct.byref(n), _stream(stream)), "lms_trace")
+        return out[:n.value]
+
     def smooth_colour(self, colour: int, stream=None):
         """lms_smooth_colour: one colour stage of the sweep."""
         _check(lib().lms_smooth_colour(self._h, colour, _stream(stream)), "lms_smooth_colour")
@@ -490,3 +502,28 @@ class Dist:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------- reuse distance (N2)
+def reuse_distance(trace: torch.Tensor, n_ids: int, stream=None) -> torch.Tensor:
+    """lms_reuse_distance: int64 CUDA tensor, -1 = first access."""
+    n = trace.numel()
+    out = torch.empty(max(n, 1), dtype=torch.int64, device="cuda")
+    _check(lib().lms_reuse_distance(_dev(trace, torch.int32, n, "trace") if n else None, n, n_ids,
+                                    ct.c_void_p(out.data_ptr()), _stream(stream)), "lms_reuse_distance")
+    return out[:n]
+
+
+def reuse_stats(dist: torch.Tensor, quantiles=(0.5, 0.75, 0.9, 1.0), capacities=(), stream=None) -> dict:
+    """lms_reuse_stats: quantiles, mean, cold count, counts >= capacities."""
+    n = dist.numel()
+    q = (ct.c_double * max(len(quantiles), 1))(*quantiles)
+    qo = (ct.c_int64 * max(len(quantiles), 1))()
+    cap = (ct.c_int64 * max(len(capacities), 1))(*capacities)
+    ge = (ct.c_int64 * max(len(capacities), 1))()
+    mean, cold = ct.c_double(), ct.c_int64()
+    _check(lib().lms_reuse_stats(_dev(dist, torch.int64, n, "dist") if n else None, n, q, len(quantiles), qo,
+                                 ct.byref(mean), ct.byref(cold), cap, len(capacities), ge, _stream(stream)),
+           "lms_reuse_stats")
+    return dict(quantiles=[qo[i] for i in range(len(quantiles))], mean=mean.value, n_cold=cold.value,
+                n_ge=[ge[i] for i in range(len(capacities))], n=n)
