@@ -56,7 +56,14 @@ typedef enum {
     LMS_ORDER_ORIGINAL = 0, /* identity: the generator / Triangle order */
     LMS_ORDER_RANDOM = 1,   /* random storage order: argsort of H(seed, 4, i) */
     LMS_ORDER_BFS = 2,      /* breadth-first order, Strout-Hovland */
-    LMS_ORDER_RDR = 3       /* Reuse-Distance-Reducing order, Alg. 2 */
+    LMS_ORDER_RDR = 3,      /* Reuse-Distance-Reducing order, Alg. 2 */
+    /* more orderings for the study */
+    LMS_ORDER_RBFS = 4,     /* reverse BFS: the BFS order reversed; `seed` = BFS seed */
+    LMS_ORDER_RCM = 5,      /* reverse Cuthill-McKee: queue BFS from the vertex of smallest (degree, label),
+                               children by (degree, label), restarts likewise; reversed (reading Z26) */
+    LMS_ORDER_DFS = 6       /* depth-first preorder (Fig. 2a): smallest unvisited neighbour
+                               first, restart at the smallest unvisited label (reading Z25); one warp,
+                               sequential; `seed` = start vertex */
 } lms_order_kind;
 
 typedef enum {

@@ -172,6 +172,11 @@ CONFIGS = {
                desc="3D Kuhn tetrahedral mesh 128^3"),
     "C4": dict(kind="grid2d", args=dict(nx=4096, ny=4096, jitter=0.3), sweeps=50,
                orderings=["original", "bfs", "rdr", "random"], desc="2D jittered-grid triangle mesh 4096x4096"),
+    # paper scale (Table II: 0.30-0.39 M vertices, ~2 triangles per vertex): not in BASELINE.json,
+    # the ordering / reuse studies' stand-in for the paper's meshes
+    "CP": dict(kind="grid2d", args=dict(nx=610, ny=610, jitter=0.3), sweeps=8,
+               orderings=["original", "random", "bfs", "rbfs", "rcm", "dfs", "rdr"],
+               desc="paper-scale 2D jittered-grid triangle mesh 610x610"),
     "C5": dict(kind="grid2d", args=dict(nx=16384, ny=8192, jitter=0.3, warp_x2=True), sweeps=20,
                orderings=["original", "bfs"], desc="2D graded (x<-x^2) jittered-grid triangle mesh 16384x8192"),
 }

@@ -73,6 +73,8 @@ def lib():
         L.o_trace.argtypes = [i64, P, P, P, P]
         L.o_trace.restype = i64
         L.o_reuse_distance.argtypes = [i64, P, i64, P]
+        L.o_order_dfs.argtypes = [i64, P, P, i64, P]
+        L.o_order_rcm.argtypes = [i64, P, P, P]
         L.o_free.argtypes = [P]
         _lib = L
     return _lib
@@ -283,6 +285,32 @@ def prepare(mesh: dict) -> dict:
     return out
 
 
+def order_rbfs(row_ptr, col, seed_vertex: int = 0) -> np.ndarray:
+    """N4 reverse BFS ("a breadth-first search of the vertices,
+    followed by a reversing of the order in which the vertices were visited")."""
+    return order_bfs(row_ptr, col, seed_vertex)[::-1].copy()
+
+
+def order_dfs(row_ptr, col, seed_vertex: int = 0) -> np.ndarray:
+    """N4 DFS preorder (Fig. 2a; reading Z25)."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    V = row_ptr.shape[0] - 1
+    perm = np.zeros(V, dtype=np.int32)
+    _chk(lib().o_order_dfs(V, _p(row_ptr), _p(col), seed_vertex, _p(perm)), "o_order_dfs")
+    return perm
+
+
+def order_rcm(row_ptr, col) -> np.ndarray:
+    """N4 reverse Cuthill-McKee (reading Z26)."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    V = row_ptr.shape[0] - 1
+    perm = np.zeros(V, dtype=np.int32)
+    _chk(lib().o_order_rcm(V, _p(row_ptr), _p(col), _p(perm)), "o_order_rcm")
+    return perm
+
+
 def order(mesh: dict, kind: str, seed: int = 0) -> np.ndarray:
     """Dispatch to the four orderings of PAPER.md Fig. 1 / Alg. 2 on a prepared mesh."""
     V = mesh["coords"][0].shape[0]
@@ -297,6 +325,12 @@ def order(mesh: dict, kind: str, seed: int = 0) -> np.ndarray:
         if q is None:
             q = quality(mesh["coords"], mesh["elems"])
         return order_rdr(mesh["row_ptr"], mesh["col"], mesh["fixed"], q)
+    if kind == "rbfs":
+        return order_rbfs(mesh["row_ptr"], mesh["col"], seed)
+    if kind == "dfs":
+        return order_dfs(mesh["row_ptr"], mesh["col"], seed)
+    if kind == "rcm":
+        return order_rcm(mesh["row_ptr"], mesh["col"])
     raise ValueError(kind)
 
 

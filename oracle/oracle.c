@@ -37,6 +37,8 @@
  *   o_smooth_seq         N3: Alg. 1 literally, storage-order in-place GS
  *   o_trace              N2: canonical access trace of one sequential sweep
  *   o_reuse_distance     N2: reuse distance of every access, Fenwick
+ *   o_order_dfs          N4: DFS preorder (Fig. 2a; reading Z25)
+ *   o_order_rcm          N4: reverse Cuthill-McKee (reading Z26)
  *
  * Parity pins for every function live in tests/test_oracle_*.py.
  *
@@ -652,5 +654,80 @@ int o_reuse_distance(int64_t n, const int32_t* trace, int64_t n_ids, int64_t* di
         last[x] = t;
     }
     free(last); free(bit);
+    return O_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* N4 orderings.
+ * o_order_dfs: depth-first preorder (the DFS ordering of Fig. 2a, P:310-313;
+ * reading Z25): from `seed`, always descend to the SMALLEST unvisited
+ * neighbour of the deepest vertex that still has one (recursive DFS with rows
+ * in ascending order), restart at the smallest unvisited label.           */
+int o_order_dfs(int64_t V, const int64_t* row_ptr, const int32_t* col, int64_t seed, int32_t* perm) {
+    if (V == 0) return O_OK;
+    if (seed < 0 || seed >= V) return O_E_ARG;
+    uint8_t* vis = (uint8_t*)calloc((size_t)V, 1);
+    int32_t* stk = (int32_t*)malloc((size_t)V * sizeof(int32_t));
+    int64_t* cur = (int64_t*)malloc((size_t)V * sizeof(int64_t));   /* next row entry to try */
+    if (!vis || !stk || !cur) { free(vis); free(stk); free(cur); return O_E_NOMEM; }
+    int64_t n = 0, top = 0, next_unvisited = 0, start = seed;
+    while (n < V) {
+        if (vis[start]) {
+            while (next_unvisited < V && vis[next_unvisited]) ++next_unvisited;
+            start = next_unvisited;
+        }
+        vis[start] = 1; perm[n++] = (int32_t)start;
+        stk[top++] = (int32_t)start; cur[start] = row_ptr[start];
+        while (top > 0) {
+            int32_t v = stk[top - 1];
+            while (cur[v] < row_ptr[v + 1] && vis[col[cur[v]]]) ++cur[v];
+            if (cur[v] == row_ptr[v + 1]) { --top; continue; }
+            int32_t u = col[cur[v]++];
+            vis[u] = 1; perm[n++] = u;
+            stk[top++] = u; cur[u] = row_ptr[u];
+        }
+    }
+    free(vis); free(stk); free(cur);
+    return O_OK;
+}
+
+/* o_order_rcm: reverse Cuthill-McKee (reading Z26): queue BFS that starts at
+ * the unvisited vertex of smallest (degree, label), enqueues each vertex's
+ * unvisited neighbours in ascending (degree, label), restarts the same way on
+ * a new component; the visit order reversed.                               */
+typedef struct { int64_t d; int32_t v; } dv;
+static int cmp_dv(const void* a, const void* b) {
+    const dv* p = (const dv*)a; const dv* q = (const dv*)b;
+    if (p->d != q->d) return (p->d > q->d) - (p->d < q->d);
+    return (p->v > q->v) - (p->v < q->v);
+}
+int o_order_rcm(int64_t V, const int64_t* row_ptr, const int32_t* col, int32_t* perm) {
+    if (V == 0) return O_OK;
+    uint8_t* vis = (uint8_t*)calloc((size_t)V, 1);
+    int32_t* q = (int32_t*)malloc((size_t)V * sizeof(int32_t));
+    dv* byd = (dv*)malloc((size_t)V * sizeof(dv));
+    int64_t maxdeg = 0;
+    for (int64_t v = 0; v < V; ++v) if (row_ptr[v + 1] - row_ptr[v] > maxdeg) maxdeg = row_ptr[v + 1] - row_ptr[v];
+    dv* l = (dv*)malloc((size_t)(maxdeg > 0 ? maxdeg : 1) * sizeof(dv));
+    if (!vis || !q || !byd || !l) { free(vis); free(q); free(byd); free(l); return O_E_NOMEM; }
+    for (int64_t v = 0; v < V; ++v) { byd[v].d = row_ptr[v + 1] - row_ptr[v]; byd[v].v = (int32_t)v; }
+    qsort(byd, (size_t)V, sizeof(dv), cmp_dv);
+    int64_t head = 0, tail = 0, nxt = 0;
+    while (tail < V) {
+        if (head == tail) {
+            while (vis[byd[nxt].v]) ++nxt;
+            vis[byd[nxt].v] = 1; q[tail++] = byd[nxt].v;
+        }
+        int32_t v = q[head++];
+        int64_t nl = 0;
+        for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
+            int32_t u = col[e];
+            if (!vis[u]) { l[nl].d = row_ptr[u + 1] - row_ptr[u]; l[nl].v = u; ++nl; }
+        }
+        qsort(l, (size_t)nl, sizeof(dv), cmp_dv);
+        for (int64_t j = 0; j < nl; ++j) { vis[l[j].v] = 1; q[tail++] = l[j].v; }
+    }
+    for (int64_t k = 0; k < V; ++k) perm[k] = q[V - 1 - k];
+    free(vis); free(q); free(byd); free(l);
     return O_OK;
 }

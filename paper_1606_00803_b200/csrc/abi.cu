@@ -348,6 +348,17 @@ lms_status lms_order(lms_mesh_t m, lms_order_kind kind, uint64_t seed, int32_t* 
       if ((int64_t)seed >= m->V || (int64_t)seed < 0) fail(LMS_E_ARG, "BFS seed vertex out of range");
       order_bfs(m, (int64_t)seed, d_perm, s);
       break;
+    case LMS_ORDER_RBFS:
+      if ((int64_t)seed >= m->V || (int64_t)seed < 0) fail(LMS_E_ARG, "BFS seed vertex out of range");
+      order_rbfs(m, (int64_t)seed, false, d_perm, s);
+      break;
+    case LMS_ORDER_RCM:
+      order_rbfs(m, 0, true, d_perm, s);
+      break;
+    case LMS_ORDER_DFS:
+      if ((int64_t)seed >= m->V || (int64_t)seed < 0) fail(LMS_E_ARG, "DFS seed vertex out of range");
+      order_dfs(m, (int64_t)seed, d_perm, s);
+      break;
     case LMS_ORDER_RDR:
       order_rdr(m, d_perm, s);
       break;

@@ -89,12 +89,38 @@ __global__ void k_bfs_expand(const int32_t* __restrict__ rp, const int32_t* __re
   }
 }
 
+// key (discoverer rank, [degree,] label): BFS queue order; with the degree
+// (db > 0 bits) the Cuthill-McKee queue order (children by (degree, label))
 __global__ void k_bfs_keys(const int32_t* __restrict__ cand, int n, const int32_t* __restrict__ minpar, int b,
-                           unsigned long long* keys) {
+                           const int32_t* __restrict__ rp, int db, unsigned long long* keys) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     int32_t u = cand[i];
-    keys[i] = ((unsigned long long)minpar[u] << b) | (unsigned long long)u;
+    const unsigned long long deg = db ? (unsigned long long)(rp[u + 1] - rp[u]) : 0ull;
+    keys[i] = ((((unsigned long long)minpar[u] << db) | deg) << b) | (unsigned long long)u;
   }
+}
+
+// the unvisited vertex of smallest (degree, label) (Cuthill-McKee start)
+__global__ void k_min_deg_unvisited(const int32_t* __restrict__ rank, const int32_t* __restrict__ rp, int64_t V,
+                                    unsigned long long* out) {
+  unsigned long long best = ~0ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
+    if (rank[i] < 0) {
+      const unsigned long long k = ((unsigned long long)(rp[i + 1] - rp[i]) << 32) | (unsigned long long)i;
+      best = k < best ? k : best;
+    }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long x = __shfl_down_sync(0xffffffffu, best, o);
+    best = x < best ? x : best;
+  }
+  if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(out, best);
+}
+
+__global__ void k_low32(const unsigned long long* in, int* out) { *out = (int)(*in & 0xffffffffull); }
+
+__global__ void k_reverse(const int32_t* __restrict__ in, int64_t V, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[V - 1 - i];
 }
 
 __global__ void k_bfs_place(const unsigned long long* __restrict__ keys, int n, int b, int64_t tail, int32_t* perm,
@@ -115,15 +141,42 @@ __global__ void k_min_unvisited(const int32_t* __restrict__ rank, int64_t V, int
   if ((threadIdx.x & 31) == 0 && best != 0x7fffffff) atomicMin(out, best);
 }
 
+__global__ void k_max_degree(const int32_t* __restrict__ rp, int64_t V, int* out) {
+  int mx = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < V; i += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, rp[i + 1] - rp[i]);
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
 static int bits_for2(int64_t n) {
   int b = 1;
   while (((int64_t)1 << b) < n) ++b;
   return b;
 }
 
-void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s) {
+// Queue BFS (rcm = false) or Cuthill-McKee (rcm = true: start and restarts at
+// the unvisited vertex of smallest (degree, label), children by (degree,
+// label)), level-synchronous: a level's new vertices sorted by (first
+// discoverer's rank, [degree,] label) is exactly the queue order.
+static void bfs_levels(lms_mesh_s* m, int64_t seed, bool rcm, int32_t* d_perm, cudaStream_t s) {
   const int64_t V = m->V;
   const int b = bits_for2(V + 1);
+  int db = 0;
+  if (rcm) {
+    int32_t maxdeg = 0;
+    {
+      DBuf<int> md(1, s);
+      LMS_TRY_CUDA(cudaMemsetAsync(md.p, 0, sizeof(int), s));
+      // degrees are < 2^31; the key needs their bit width
+      k_max_degree<<<grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256), 256, 0, s>>>(m->row_ptr.p, V, md.p);
+      LMS_CHECK_LAUNCH();
+      LMS_TRY_CUDA(cudaMemcpyAsync(&maxdeg, md.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    }
+    db = bits_for2((int64_t)maxdeg + 1);
+    if (2 * b + db > 64) fail(LMS_E_ARG, "RCM: mesh too large for the 64-bit level keys");
+  }
   DBuf<int32_t> rank(V, s), minpar(V, s), cand(V, s);
   DBuf<unsigned long long> keys(V, s), keys2(V, s);
   DBuf<int> dint(2, s);  // [0] = ncand, [1] = vertex scratch
@@ -131,19 +184,35 @@ void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s) {
   k_bfs_init<<<Gv, 256, 0, s>>>(V, rank.p, minpar.p);
   LMS_CHECK_LAUNCH();
   size_t tb_max = 0;
-  LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb_max, keys.p, keys2.p, (int)V, 0, 2 * b, s));
+  LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb_max, keys.p, keys2.p, (int)V, 0, 2 * b + db, s));
   DBuf<char> tmp(tb_max, s);
-  int hseed = (int)seed;
-  LMS_TRY_CUDA(cudaMemcpyAsync(dint.p + 1, &hseed, sizeof(int), cudaMemcpyHostToDevice, s));
+  DBuf<unsigned long long> best(1, s);
+  auto min_deg_start = [&]() {  // Cuthill-McKee (re)start vertex into dint[1]
+    LMS_TRY_CUDA(cudaMemsetAsync(best.p, 0xff, sizeof(unsigned long long), s));
+    k_min_deg_unvisited<<<Gv, 256, 0, s>>>(rank.p, m->row_ptr.p, V, best.p);
+    LMS_CHECK_LAUNCH();
+    k_low32<<<1, 1, 0, s>>>(best.p, dint.p + 1);
+    LMS_CHECK_LAUNCH();
+  };
+  if (rcm) {
+    min_deg_start();
+  } else {
+    int hseed = (int)seed;
+    LMS_TRY_CUDA(cudaMemcpyAsync(dint.p + 1, &hseed, sizeof(int), cudaMemcpyHostToDevice, s));
+  }
   k_bfs_set<<<1, 1, 0, s>>>(d_perm, rank.p, 0, dint.p + 1);
   LMS_CHECK_LAUNCH();
   int64_t head = 0, tail = 1;
   while (tail < V) {
-    if (head == tail) {  // component exhausted: restart at the smallest unvisited label
-      int big = 0x7fffffff;
-      LMS_TRY_CUDA(cudaMemcpyAsync(dint.p + 1, &big, sizeof(int), cudaMemcpyHostToDevice, s));
-      k_min_unvisited<<<Gv, 256, 0, s>>>(rank.p, V, dint.p + 1);
-      LMS_CHECK_LAUNCH();
+    if (head == tail) {  // component exhausted: restart at the smallest unvisited label (RCM: (degree, label))
+      if (rcm) {
+        min_deg_start();
+      } else {
+        int big = 0x7fffffff;
+        LMS_TRY_CUDA(cudaMemcpyAsync(dint.p + 1, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+        k_min_unvisited<<<Gv, 256, 0, s>>>(rank.p, V, dint.p + 1);
+        LMS_CHECK_LAUNCH();
+      }
       k_bfs_set<<<1, 1, 0, s>>>(d_perm, rank.p, tail, dint.p + 1);
       LMS_CHECK_LAUNCH();
       ++tail;
@@ -161,14 +230,92 @@ void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s) {
     head = tail;
     if (n == 0) continue;
     unsigned Gn = grid_for(n, 256) > 4096 ? 4096 : grid_for(n, 256);
-    k_bfs_keys<<<Gn, 256, 0, s>>>(cand.p, n, minpar.p, b, keys.p);
+    k_bfs_keys<<<Gn, 256, 0, s>>>(cand.p, n, minpar.p, b, m->row_ptr.p, db, keys.p);
     LMS_CHECK_LAUNCH();
     size_t tb = tb_max;
-    LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, keys2.p, n, 0, 2 * b, s));
+    LMS_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys.p, keys2.p, n, 0, 2 * b + db, s));
     k_bfs_place<<<Gn, 256, 0, s>>>(keys2.p, n, b, tail, d_perm, rank.p);
     LMS_CHECK_LAUNCH();
     tail += n;
   }
+}
+
+void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s) { bfs_levels(m, seed, false, d_perm, s); }
+
+// reverse BFS and reverse Cuthill-McKee (reading Z26): the visit
+// order reversed
+void order_rbfs(lms_mesh_s* m, int64_t seed, bool rcm, int32_t* d_perm, cudaStream_t s) {
+  DBuf<int32_t> fwd(m->V, s);
+  bfs_levels(m, seed, rcm, fwd.p, s);
+  k_reverse<<<grid_for(m->V, 256) > 8192 ? 8192 : grid_for(m->V, 256), 256, 0, s>>>(fwd.p, m->V, d_perm);
+  LMS_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------------------ DFS
+// Depth-first preorder (Fig. 2a; reading Z25): descend to the
+// smallest unvisited neighbour of the deepest vertex that has one; restart
+// at the smallest unvisited label.  Inherently sequential: one warp, the
+// stack in global memory, a vertex's row checked in one warp load per step.
+__global__ void k_dfs_walk(const int32_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t V,
+                           int32_t seed, uint8_t* vis, int32_t* stk, int32_t* perm) {
+  const int lane = threadIdx.x;
+  const unsigned FULL = 0xffffffffu;
+  int64_t n = 0, nu = 0;
+  int32_t start = seed;
+  while (n < V) {
+    if (vis[start]) {  // restart: smallest unvisited label, 32 labels per probe
+      for (;;) {
+        const int64_t i = nu + lane;
+        const unsigned bal = __ballot_sync(FULL, i < V && !vis[i]);
+        if (bal) {
+          nu += __ffs(bal) - 1;
+          break;
+        }
+        nu += 32;
+      }
+      start = (int32_t)nu;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      vis[start] = 1;
+      perm[n] = start;
+      stk[0] = start;
+    }
+    ++n;
+    int64_t top = 1;
+    __syncwarp();
+    while (top > 0) {
+      const int32_t v = stk[top - 1];
+      int32_t u = -1;
+      for (int32_t base = __ldg(rp + v), e = __ldg(rp + v + 1); base < e && u < 0; base += 32) {
+        const int32_t j = base + lane;
+        const int32_t c = j < e ? __ldg(col + j) : -1;
+        const unsigned bal = __ballot_sync(FULL, c >= 0 && !vis[c]);
+        if (bal) u = __shfl_sync(FULL, c, __ffs(bal) - 1);
+      }
+      if (u < 0) {
+        --top;
+        continue;
+      }
+      if (lane == 0) {
+        vis[u] = 1;
+        perm[n] = u;
+        stk[top] = u;
+      }
+      ++n;
+      ++top;
+      __syncwarp();
+    }
+  }
+}
+
+void order_dfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s) {
+  const int64_t V = m->V;
+  DBuf<uint8_t> vis(V, s);
+  DBuf<int32_t> stk(V, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(vis.p, 0, V, s));
+  k_dfs_walk<<<1, 32, 0, s>>>(m->row_ptr.p, m->col.p, V, (int32_t)seed, vis.p, stk.p, d_perm);
+  LMS_CHECK_LAUNCH();
 }
 
 // ------------------------------------------------------------------------ RDR
