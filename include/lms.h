@@ -69,6 +69,9 @@ typedef enum {
 typedef enum {
     LMS_SCHED_AUTO = 0,     /* pick per mesh: GZ for 2D meshes with <= 8 colours, else S1 */
     LMS_SCHED_S1 = 1,       /* one launch per colour (CUDA-graph captured sweep) */
+    LMS_SCHED_S2 = 2,       /* 3D only: one launch per colour over interleaved (x, y, z, 0) coordinates --
+                               one 32-byte sector per neighbour (256-bit loads) -- and the coalesced
+                               column-major CSR slab; LMS_E_ARG on a 2D mesh */
     LMS_SCHED_S3 = 3,       /* persistent colour-pipelined sweep with per-tile progress flags */
     LMS_SCHED_GZ = 4,       /* ghost-zone tiled sweep: one launch per P sweeps; each CTA stages a
                                spatial tile plus every vertex within C*P hops in shared memory,

@@ -399,10 +399,11 @@ lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, 
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");
   DevGuard dg(m);
-  if (kind != LMS_SCHED_AUTO && kind != LMS_SCHED_S1 && kind != LMS_SCHED_S3 && kind != LMS_SCHED_GZ &&
-      kind != LMS_SCHED_JACOBI)
+  if (kind != LMS_SCHED_AUTO && kind != LMS_SCHED_S1 && kind != LMS_SCHED_S2 && kind != LMS_SCHED_S3 &&
+      kind != LMS_SCHED_GZ && kind != LMS_SCHED_JACOBI)
     fail(LMS_E_ARG, "unknown schedule");
   if (kind == LMS_SCHED_GZ && lag > 8) fail(LMS_E_ARG, "GZ: at most 8 sweeps per pass");
+  if (kind == LMS_SCHED_S2 && m->dim != 3) fail(LMS_E_ARG, "S2 is the 3D kernel (2D meshes: GZ)");
   if (tile < 0 || lag < 0) fail(LMS_E_ARG, "tile/lag < 0");
   if (tile != 0 && (tile < 32 || tile > (1 << 20))) fail(LMS_E_ARG, "tile must be in [32, 2^20]");
   m->sched_req = kind;

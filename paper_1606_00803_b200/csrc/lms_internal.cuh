@@ -137,6 +137,10 @@ struct Schedule {
   DBuf<int32_t> slab;       // S3 slab: per chunk 32 vertex ids + W x 32 neighbour ids
   DBuf<int32_t> irec;       // [K*C*32] S3 128-byte item records (see smooth.cu)
   DBuf<unsigned long long> ticket;  // [1] S3 work counter
+  // S2 (s2.cu): the chunks of every colour, colour-major (slab offset, row width)
+  DBuf<long long> s2_choff;
+  DBuf<int32_t> s2_chw;
+  std::vector<int64_t> s2_cstart;  // [C + 1] first chunk of each colour
   // GZ (ghost-zone tiled sweep, gz.cu): per tile a region = owned free vertices
   // plus every vertex within C*P hops; a persistent kernel stages regions in
   // shared memory and runs P whole sweeps there, reading X and writing the
@@ -248,6 +252,7 @@ int64_t spatial_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s);
 bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s);  // gz.cu
 void run_gz(lms_mesh_s* m, int sweeps, cudaStream_t s);                     // gz.cu
 void run_jacobi(lms_mesh_s* m, int sweeps, cudaStream_t s);                 // jacobi.cu
+void run_s2(lms_mesh_s* m, int sweeps, cudaStream_t s);                     // s2.cu
 void halo_pack(lms_mesh_s* m, const int32_t* idx, int64_t n, double* out, cudaStream_t s);        // halo.cu
 void halo_unpack(lms_mesh_s* m, const int32_t* idx, int64_t n, const double* in, cudaStream_t s);  // halo.cu
 void sync_soa(lms_mesh_s* m, cudaStream_t s);   // make x[] current (gz.cu)

@@ -472,9 +472,9 @@ static void build_base(lms_mesh_s* m, cudaStream_t s, bool gz_base) {
   if (gz_base) return;
   // resolve the kernel: S3 pays off when the tile graph is banded (small reach)
   int kind = m->sched_req;
-  // AUTO beyond GZ: S1 (measured faster than S3 on the 3D Kuhn C3 under every
-  // ordering, profiles/round1_ordering_study.md)
-  if (kind == LMS_SCHED_AUTO) kind = LMS_SCHED_S1;
+  // AUTO beyond GZ: S2 for 3D (C3: BFS 192 vs 195 us, RDR 196 vs 262 us per
+  // sweep against S1; S3 slower under every ordering), else S1
+  if (kind == LMS_SCHED_AUTO) kind = m->dim == 3 ? LMS_SCHED_S2 : LMS_SCHED_S1;
   S.kind = kind;
   if (kind == LMS_SCHED_S3) {
     const int ctas = s3_ctas(m->device);
@@ -493,6 +493,8 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   Schedule& S = m->sched;
   S.valid = false;
   S.base_valid = false;
+  S.s2_choff.release();  // S2 chunk lists belong to the previous schedule
+  S.s2_chw.release();
   if (m->sched_req == LMS_SCHED_JACOBI) {  // N3 variant (jacobi.cu): no schedule tables
     S.kind = LMS_SCHED_JACOBI;
     S.valid = true;
@@ -1417,6 +1419,10 @@ void run_sweeps(lms_mesh_s* m, int sweeps, cudaStream_t s) {
   }
   if (S.kind == LMS_SCHED_JACOBI) {
     run_jacobi(m, sweeps, s);
+    return;
+  }
+  if (S.kind == LMS_SCHED_S2) {
+    run_s2(m, sweeps, s);
     return;
   }
   sync_soa(m, s);
