@@ -1512,14 +1512,8 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
       while (alive && rbat[slot] != bat) alive = guard.ok_spin();
       alive = alive && mbar_wait_g(rfull + slot, (uint32_t)(bat >> L.RR_log2) & 1u, guard);
       if (STATS) w_rec += clock64() - c0;
-      if (alive && !tile_ready) {  // the region of the item's tile
-        guard.start();
-        while (alive && buf_tile[tb & 0xffff] != i) alive = guard.ok();
-        alive = alive && mbar_wait_g(full + (tb & 0xffff), (uint32_t)(tb >> 16), guard);
-      }
     }
     if (!__shfl_sync(FULL, alive, 0)) return;
-    tile_ready = true;
     GzRec<RMAX> r[UPL];
     const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rbase + 2 * U * R);
     const uint4 desc = *reinterpret_cast<const uint4*>(rbase + 2 * U * R + 8 * U);
@@ -1569,6 +1563,18 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     reinterpret_cast<volatile uint32_t*>(rcp + GZ_RCP_MAX + 1)[warp] = fold;
     __syncwarp();
     if (early && lane == 0) mbar_arrive(rempty + slot);
+    // the region of the item's tile -- waited for only after the record slot
+    // is back in the ring, so a worker held at a tile boundary does not also
+    // hold a record slot the loader needs for the claims behind it
+    if (!tile_ready) {
+      if (lane == 0) {
+        guard.start();
+        while (alive && buf_tile[tb & 0xffff] != i) alive = guard.ok();
+        alive = alive && mbar_wait_g(full + (tb & 0xffff), (uint32_t)(tb >> 16), guard);
+      }
+      if (!__shfl_sync(FULL, alive, 0)) return;
+      tile_ready = true;
+    }
     if (desc.y == 0) {
 #pragma unroll
       for (int u = 0; u < UPL; ++u) {
