@@ -144,14 +144,21 @@ class ClockSampler:
 
 
 def load_traffic(config, ordering, kernel):
-    """ncu dram bytes per launch of the sweep kernel from the committed summary (or None)."""
+    """ncu DRAM bytes per launch of the sweep kernel from the committed capture
+    (profiles/ncu_summary.json), or None.  The capture records the sha256 of
+    the kernel's source file; a capture of another version of the kernel is
+    stale and not reported."""
+    import hashlib
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    src = os.path.join(ROOT, "paper_1606_00803_b200", "csrc", "gz.cu")
     try:
         with open(path) as f:
             d = json.load(f)
+        with open(src, "rb") as f:
+            sha = hashlib.sha256(f.read()).hexdigest()
         for rec in d.get("kernels", []):
             if rec.get("config") == config and rec.get("ordering") == ordering and rec.get("kernel") == kernel:
-                return rec
+                return rec if rec.get("gz_cu_sha256") == sha else None
     except Exception:
         pass
     return None
