@@ -1043,6 +1043,13 @@ __device__ __forceinline__ double2 gz_div2(double sx, double sy, int d, const do
   }
   return make_double2(__ddiv_rn(d ? sx : 0.0, dd), __ddiv_rn(d ? sy : 0.0, dd));
 }
+// the same with RN(1/d) loaded beforehand (rr = rcp[d] for 1 <= d <= GZ_RCP_MAX)
+__device__ __forceinline__ double2 gz_div2r(double sx, double sy, int d, double rr) {
+  const double dd = (double)d;
+  if (d >= 1 && d <= GZ_RCP_MAX && gz_div_ok(sx) && gz_div_ok(sy))
+    return make_double2(gz_div(sx, dd, rr), gz_div(sy, dd, rr));
+  return make_double2(__ddiv_rn(d ? sx : 0.0, dd), __ddiv_rn(d ? sy : 0.0, dd));
+}
 
 // Eq. 1 for this lane's update: neighbours (CSR order) from shared memory,
 // ordered IEEE adds, correctly rounded division, result back to shared
@@ -1147,6 +1154,8 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, int d
                                            uint32_t padv, double2& oa, double2& ob) {
   double2* s2 = reinterpret_cast<double2*>(sc);
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(sc);
+  // RN(1/d) from the table before the gathers: off the critical path
+  double rra = rcp[da <= GZ_RCP_MAX ? da : 0], rrb = rcp[db <= GZ_RCP_MAX ? db : 0];
   uint16_t ua[RMAX], ub[RMAX];
 #pragma unroll
   for (int p = 0; p < RMAX / 8; ++p) {
@@ -1206,15 +1215,21 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, int d
         }
       }
     }
-    if (da == 0) da = ca;
-    if (db == 0) db = cb;
+    if (da == 0) {
+      da = ca;
+      rra = rcp[da <= GZ_RCP_MAX ? da : 0];
+    }
+    if (db == 0) {
+      db = cb;
+      rrb = rcp[db <= GZ_RCP_MAX ? db : 0];
+    }
   }
   if (va) {
-    oa = gz_div2(ax, ay, da, rcp);
+    oa = gz_div2r(ax, ay, da, rra);
     s2[ra.pb & 0x7fffu] = oa;
   }
   if (vb) {
-    ob = gz_div2(bx, by, db, rcp);
+    ob = gz_div2r(bx, by, db, rrb);
     s2[rb.pb & 0x7fffu] = ob;
   }
 }
@@ -2242,6 +2257,16 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&cap, cudaDevAttrMaxSharedMemoryPerBlockOptin, m->device));
   cap -= 16;  // the kernel's static shared memory (abort flag)
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  // CTAs per SM (LMS_GZ_CTAS): 2 halves the shared memory and the warps of a
+  // CTA (one region buffer each) and lets one CTA's tile staging overlap the
+  // other's compute
+  const int cps = env_int("LMS_GZ_CTAS", 1, 1, 2);
+  if (cps == 2) {
+    int per_sm = 0;
+    LMS_TRY_CUDA(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, m->device));
+    cap = std::min(cap, per_sm / 2 - 1024 - 16);  // 1 KB reserved per CTA
+  }
+  nsm *= cps;  // persistent CTAs
   // updates per lane: 2D default 2 (64-update items halve the per-item claim /
   // record / dependency / completion work: C4 ~300 -> ~280 us per sweep), 3D 1.
   // (Its rare failures in back-to-back runs were the record ring's parity
@@ -2253,14 +2278,14 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   // or 12 (3D, 152)
   // (one warp below the register file's quotient: 21 x 96 registers fails
   // to launch with "too many resources")
-  const int cap_warps = m->dim == 2 ? (upl == 2 ? 65536 / (GZ_REGS2 * 32) - 1 : 24) : 12;
+  const int cap_warps = (m->dim == 2 ? (upl == 2 ? 65536 / (GZ_REGS2 * 32) - 1 : 24) : 12) / cps;
   const int maxw = cap_warps;  // producers + loader + workers
   // workers measured best on C4: 18 with 2 updates per lane, 22 with 1 (more
   // warps only lengthen every item: the shared-memory pipe is the shared
   // resource); + region producer + record loader
   const int nw_env = env_int("LMS_GZ_WORKERS", 0, 0, maxw - 2);
   const int nw = nw_env ? nw_env : std::min(maxw - 2, m->dim == 2 ? (upl == 2 ? 18 : 22) : 10);
-  const int want_nb = env_int("LMS_GZ_BUFFERS", 0, 0, 8);
+  const int want_nb = env_int("LMS_GZ_BUFFERS", cps == 2 ? 1 : 0, 0, 8);
   const int dim = m->dim, C = m->C;
   GzNeeds nd;
   Schedule& S = m->sched;
@@ -2305,6 +2330,7 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
       if (S.gz_L.NPW == 1 && S.gz_L.NW != nw) total = plan_layout(nd, dim, C, P, upl, cap, want_nb, nw, tiles_cap, &S.gz_L, 1);
       if (total > cap || (want_nb == 0 && S.gz_L.NB < min_nb)) continue;
       S.gz_smem = (int)total;
+      S.gz_cps = cps;
       S.gz_threads = 32 * (S.gz_L.NPW + 1 + S.gz_L.NW);
       if (getenv("LMS_GZ_VERBOSE"))
         fprintf(stderr, "[gz] %s T=%d P=%d tiles=%lld items=%lld NB=%d RR=%d NW=%d smem=%d buf=%d slots<=%lld "
@@ -2329,6 +2355,7 @@ static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
   LMS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S.gz_smem));
   int nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  nsm *= S.gz_cps;
   const int grid = (int)(S.gz_ntiles < nsm ? S.gz_ntiles : nsm);
   if (grid <= 0) return;
   static unsigned long long* stats = nullptr;

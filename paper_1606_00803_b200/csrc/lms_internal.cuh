@@ -151,6 +151,7 @@ struct Schedule {
   int gz_T = 0;             // target owned vertices per tile
   int gz_smem = 0;          // dynamic shared memory per CTA (bytes)
   int gz_threads = 0;       // threads per CTA
+  int gz_cps = 1;           // persistent CTAs per SM
   GzLayout gz_L;            // shared-memory plan of the kernel
   int64_t gz_nreg = 0;      // sum of region sizes
   int64_t gz_nupd = 0;      // sum over tiles of first-sweep updates
