@@ -1504,10 +1504,19 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
   bool tile_ready = false;
   constexpr int U = 32 * UPL;  // updates per item; lane l handles positions l, l + 32
   const int bs_log2 = L.BS_log2;
+  // The next claim is taken while the current item computes (its atomic's
+  // latency -- 18 warps contend on one counter -- is hidden).  Holding a
+  // claim while computing cannot deadlock: the current item waits only for
+  // earlier claims, and the held one is started right after it.
+  int kc_next = -1;
   for (;;) {
     int kc = 0;
-    if (lane == 0) kc = atomicAdd(ctl, 1);
-    kc = __shfl_sync(FULL, kc, 0);
+    if (kc_next >= 0) {
+      kc = kc_next;
+    } else {
+      if (lane == 0) kc = atomicAdd(ctl, 1);
+      kc = __shfl_sync(FULL, kc, 0);
+    }
     if (kc >= total) break;
     if (kc >= pre_hi) {
       enter_tile(kc);
@@ -1615,6 +1624,8 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     }
     if (!__all_sync(FULL, alive)) return;
     fence_cta();
+    int kn = 0;
+    if (L.prefetch_claim && lane == 0) kn = atomicAdd(ctl, 1);
     const long long c2 = STATS ? clock64() : 0;
     double* sc = reinterpret_cast<double*>(buf + L.coord_off);
     const bool last = j == P - 1;
@@ -1656,6 +1667,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
       if (desc.z) atomicAdd(cnt + sg, 1);  // stage counters: only tiles with whole-stage waits read them
       if (atomicAdd(ndone + (tb & 0xffff), 1) == pre_hi - pre_lo - 1) mbar_arrive(empty + (tb & 0xffff));
     }
+    kc_next = L.prefetch_claim ? __shfl_sync(FULL, kn, 0) : -1;
     if (STATS) {
       const long long c3 = clock64();
       w_wait += c1 - c0;
@@ -2223,6 +2235,7 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   L->padbase = (int)((nd.max_slots + 7) & ~(int64_t)7);  // 2D pad slots padbase .. padbase + 7
   L->sleep0 = env_int("LMS_GZ_SLEEP0", 20, 0, 1000);
   L->hint_rec = env_int("LMS_GZ_HINT", 0, 0, 1);
+  L->prefetch_claim = env_int("LMS_GZ_PREFETCH_CLAIM", 1, 0, 1);
   L->sleep1 = env_int("LMS_GZ_SLEEP1", 128, 0, 10000);
   const int64_t coords = dim == 2 ? 16 * ((int64_t)L->padbase + 8) : 24 * r4(nd.max_slots);
   L->buf_bytes = (int)((L->coord_off + coords + 127) & ~(int64_t)127);

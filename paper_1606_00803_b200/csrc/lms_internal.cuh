@@ -106,6 +106,7 @@ struct GzLayout {
   int padbase = 0;              // 2D: first of the 8 pad slots of every region buffer
   int sleep0 = 20, sleep1 = 128;  // dependency-poll back-off (ns), first 64 polls / later
   int hint_rec = 0;             // records TMA'd with an L2 evict_first policy
+  int prefetch_claim = 1;       // take the next claim while the current item computes
 };
 
 // ----------------------------------------------------------------- schedule
