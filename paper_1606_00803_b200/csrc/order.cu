@@ -20,9 +20,15 @@
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 
+#include <algorithm>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
+
 #include "lms_internal.cuh"
 
 namespace lms {
+namespace cg = cooperative_groups;
 
 __device__ __forceinline__ unsigned long long sm64(unsigned long long z) {
   z += 0x9E3779B97F4A7C15ull;
@@ -155,11 +161,223 @@ static int bits_for2(int64_t n) {
   return b;
 }
 
+// ------------------------------------------------------------------------ BFS / CM, one launch
+// The level loop in ONE cooperative kernel (no host round trip per level).
+// Per level [head, tail) of the queue:
+//   1. every unvisited neighbour u of a level vertex gets minpar[u] = the
+//      smallest level index that discovers it (atomicMin);
+//   2. every level vertex counts its children (neighbours u with
+//      minpar[u] == its index, still unvisited);
+//   3. one block scans the counts (exclusive, chunks of 1024 with a carry);
+//   4. every level vertex writes its children at its offset -- ascending label
+//      (its CSR row is ascending) for BFS, ascending (degree, label) for CM --
+//      which is exactly the queue order (children of earlier queue entries
+//      first, each entry's children in enqueue order).
+// A component restart takes the unvisited vertex of smallest label (BFS) or
+// (degree, label) (CM) by a grid-wide atomicMin.  grid.sync() between phases.
+struct BfsCtl {
+  long long head, tail, total;
+  unsigned long long best;
+};
+
+__global__ void __launch_bounds__(256) k_bfs_coop(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                  int64_t V, int32_t seed, int rcm, int32_t* __restrict__ perm,
+                                                  int32_t* __restrict__ rank, int32_t* __restrict__ minpar,
+                                                  int32_t* __restrict__ cnt, BfsCtl* ctl) {
+  // minpar[u] = the smallest QUEUE POSITION of a vertex that discovers u (not a
+  // level index: positions grow level by level, so discovering the next level
+  // while this one is being written can never undercut a parent of this level)
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = tid; v < V; v += nth) {
+    rank[v] = -1;
+    minpar[v] = 0x7fffffff;
+  }
+  if (tid == 0) ctl->best = ~0ull;
+  grid.sync();
+  __shared__ long long s_carry;
+  __shared__ int s_warp[32];
+  long long head = 0, tail = 0;
+  // discover the unvisited neighbours of queue entries [a, b) (warp per entry)
+  auto discover = [&](long long a, long long b) {
+    for (long long q = a + (tid >> 5); q < b; q += nth >> 5) {
+      const int32_t p = perm[q];
+      for (int32_t j = rp[p] + lane; j < rp[p + 1]; j += 32) {
+        const int32_t u = col[j];
+        if (rank[u] < 0) atomicMin(&minpar[u], (int32_t)q);
+      }
+    }
+  };
+  if (!rcm) {
+    if (tid == 0) {
+      perm[0] = seed;
+      rank[seed] = 0;
+    }
+    tail = 1;
+    grid.sync();
+    discover(0, 1);
+    grid.sync();
+  }
+  while (tail < V) {
+    if (head == tail) {  // restart: smallest unvisited label (BFS) or (degree, label) (CM)
+      unsigned long long best = ~0ull;
+      for (int64_t v = tid; v < V; v += nth)
+        if (rank[v] < 0) {
+          const unsigned long long k =
+              rcm ? ((unsigned long long)(rp[v + 1] - rp[v]) << 32) | (unsigned long long)v : (unsigned long long)v;
+          best = k < best ? k : best;
+        }
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long x = __shfl_down_sync(0xffffffffu, best, o);
+        best = x < best ? x : best;
+      }
+      if (lane == 0 && best != ~0ull) atomicMin(&ctl->best, best);
+      grid.sync();
+      const int32_t v = (int32_t)(ctl->best & 0xffffffffull);
+      if (tid == 0) {
+        perm[tail] = v;
+        rank[v] = (int32_t)tail;
+      }
+      grid.sync();
+      if (tid == 0) ctl->best = ~0ull;
+      discover(tail, tail + 1);
+      ++tail;
+      grid.sync();
+      continue;
+    }
+    const int64_t n = tail - head;
+    // children per queue entry of the level
+    for (int64_t i = tid; i < n; i += nth) {
+      const int32_t p = perm[head + i];
+      const int32_t me = (int32_t)(head + i);
+      int c = 0;
+      for (int32_t j = rp[p]; j < rp[p + 1]; ++j) {
+        const int32_t u = col[j];
+        c += (rank[u] < 0 && minpar[u] == me) ? 1 : 0;
+      }
+      cnt[i] = c;
+    }
+    grid.sync();
+    // exclusive scan of cnt[0, n) in block 0 (chunks of blockDim with a carry)
+    if (blockIdx.x == 0) {
+      if (threadIdx.x == 0) s_carry = 0;
+      __syncthreads();
+      const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const int x = i < n ? cnt[i] : 0;
+        int incl = x;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_warp[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+          int t = lane < nw ? s_warp[lane] : 0;
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+          }
+          if (lane < nw) s_warp[lane] = t;  // inclusive warp prefix
+        }
+        __syncthreads();
+        const long long off = s_carry + (w ? s_warp[w - 1] : 0) + incl - x;
+        if (i < n) cnt[i] = (int32_t)off;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += s_warp[nw - 1];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) ctl->total = s_carry;
+    }
+    grid.sync();
+    const long long total = ctl->total;
+    // children at their offsets in enqueue order (BFS: ascending label, the
+    // row's order; CM: ascending (degree, label)), ranked at once, and -- in
+    // the same phase -- each new entry's own discoveries for the next level
+    // (a sibling not ranked yet may see its minpar lowered to a position of
+    // this new level: never below its parent's, so nothing changes)
+    auto put = [&](int32_t u, long long o) {
+      perm[o] = u;
+      rank[u] = (int32_t)o;  // only this thread writes u (its unique discoverer)
+      for (int32_t j = rp[u]; j < rp[u + 1]; ++j) {
+        const int32_t x = col[j];
+        if (rank[x] < 0) atomicMin(&minpar[x], (int32_t)o);
+      }
+    };
+    for (int64_t i = tid; i < n; i += nth) {
+      const int32_t p = perm[head + i];
+      const int32_t me = (int32_t)(head + i);
+      long long o = tail + cnt[i];
+      if (!rcm) {
+        for (int32_t j = rp[p]; j < rp[p + 1]; ++j) {
+          const int32_t u = col[j];
+          if (rank[u] < 0 && minpar[u] == me) put(u, o++);
+        }
+      } else {  // ascending (degree, label): repeated minimum over the row
+        for (;;) {
+          unsigned long long bestk = ~0ull;
+          for (int32_t j = rp[p]; j < rp[p + 1]; ++j) {
+            const int32_t u = col[j];
+            if (minpar[u] == me && rank[u] < 0) {
+              const unsigned long long k = ((unsigned long long)(rp[u + 1] - rp[u]) << 32) | (unsigned long long)u;
+              if (k < bestk) bestk = k;
+            }
+          }
+          if (bestk == ~0ull) break;
+          put((int32_t)(bestk & 0xffffffffull), o++);
+        }
+      }
+    }
+    head = tail;
+    tail += total;
+    grid.sync();
+  }
+}
+
+static int env_int_o(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? std::max(1, atoi(e)) : dflt;
+}
+
+static bool bfs_coop(lms_mesh_s* m, int64_t seed, bool rcm, int32_t* d_perm, cudaStream_t s) {
+  if (getenv("LMS_BFS_HOST")) return false;
+  int dev = 0, coop = 0, nsm = 0, per_sm = 0;
+  LMS_TRY_CUDA(cudaGetDevice(&dev));
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) return false;
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  LMS_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bfs_coop, 256, 0));
+  if (per_sm < 1) return false;
+  const int64_t V = m->V;
+  DBuf<int32_t> rank(V, s), minpar(V, s), cnt(V, s);
+  DBuf<BfsCtl> ctl(1, s);
+  const int32_t* rp = m->row_ptr.p;
+  const int32_t* col = m->col.p;
+  int32_t sd = (int32_t)seed;
+  int r = rcm ? 1 : 0;
+  int32_t* pp = d_perm;
+  int32_t* rk = rank.p;
+  int32_t* mp = minpar.p;
+  int32_t* cn = cnt.p;
+  BfsCtl* cp = ctl.p;
+  void* args[] = {(void*)&rp, (void*)&col, (void*)&V, (void*)&sd, (void*)&r, (void*)&pp, (void*)&rk, (void*)&mp,
+                  (void*)&cn, (void*)&cp};
+  const int blocks = nsm * std::min(per_sm, env_int_o("LMS_BFS_BPS", 1));
+  LMS_TRY_CUDA(cudaLaunchCooperativeKernel((void*)k_bfs_coop, dim3(blocks), dim3(256), args, 0, s));
+  note_launch();
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));  // the buffers above are released on return
+  return true;
+}
+
 // Queue BFS (rcm = false) or Cuthill-McKee (rcm = true: start and restarts at
 // the unvisited vertex of smallest (degree, label), children by (degree,
 // label)), level-synchronous: a level's new vertices sorted by (first
 // discoverer's rank, [degree,] label) is exactly the queue order.
 static void bfs_levels(lms_mesh_s* m, int64_t seed, bool rcm, int32_t* d_perm, cudaStream_t s) {
+  if (bfs_coop(m, seed, rcm, d_perm, s)) return;  // one cooperative launch; below: host-driven levels
   const int64_t V = m->V;
   const int b = bits_for2(V + 1);
   int db = 0;
