@@ -1349,9 +1349,6 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     for (int i = warp; i < n_my; i += NPW) {
       const int b = i % NB;
       const uint32_t ph = (uint32_t)(i / NB) & 1u;
-      const long long q0 = STATS ? clock64() : 0;
-      if (i >= NB && !mbar_wait_g(empty + b, ph ^ 1u, guard)) return;
-      if (STATS) pw += clock64() - q0;
       const int k = tiles[blockIdx.x + (long long)i * gridDim.x];
       const GzTile t = tab[k];
       const uint32_t bytes = t.meta16 * 16u;
@@ -1364,6 +1361,11 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
           bulk_g2s(stgp + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, sb);
       }
       if (!mbar_wait_g(sb, (uint32_t)(i / NPW) & 1u, guard)) return;
+      // the tile's meta block is staged BEFORE its buffer frees up (the
+      // staging area is separate), so the refill starts right at the release
+      const long long q0 = STATS ? clock64() : 0;
+      if (i >= NB && !mbar_wait_g(empty + b, ph ^ 1u, guard)) return;
+      if (STATS) pw += clock64() - q0;
       unsigned char* buf = sm + L.off_ring + (size_t)b * L.buf_bytes;
       const uint32_t* hsrc = reinterpret_cast<const uint32_t*>(stgp);
       uint32_t* hdst = reinterpret_cast<uint32_t*>(buf);
@@ -2215,12 +2217,14 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   // A worker waits for the record batch of its claim; that batch's slot could
   // only be two phases behind if every claim of the RR batches before it were
   // outstanding too, i.e. RR * BS < NW; RR * BS >= NW + BS keeps each
-  // wait unambiguous.  The ring is also the record prefetch depth: about 45
-  // records are consumed per TMA latency on C4, so at least 8 batches (64
-  // records; 4 batches measured 1.7x slower).  RR is a power of two.
-  L->BS_log2 = env_int("LMS_GZ_BS_LOG2", upl == 2 ? 2 : 3, 0, 4);  // records per batch (about 3-6 KB per batch)
+  // wait unambiguous.  The ring is also the record prefetch depth (RR * BS
+  // records); RR is a power of two.  Records per batch (one TMA bulk copy per
+  // batch and tile): 8.  C4 (64-update records of 1,680 B, 32 in the ring):
+  // 4 x 8 = 263.5 us per sweep, 8 x 4 = 266.7, 16 x 2 = 470 (32-update
+  // records: 8 x 8, fewer batches measured 1.7x slower)
+  L->BS_log2 = env_int("LMS_GZ_BS_LOG2", 3, 0, 4);
   L->BS = 1 << L->BS_log2;
-  L->RR = env_int("LMS_GZ_RR", 8, 4, 64);
+  L->RR = env_int("LMS_GZ_RR", upl == 2 ? 4 : 8, 2, 64);
   while (L->RR & (L->RR - 1)) ++L->RR;
   while (L->RR * L->BS < nw + L->BS) L->RR *= 2;
   L->RR_log2 = 0;
