@@ -970,6 +970,12 @@ __device__ __forceinline__ uint32_t ld_stream4(const uint32_t* p, uint64_t pol) 
 // CTA-scope acquire/release ordering (lighter than __threadfence_block's
 // sequentially consistent fence)
 __device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
+// acquire load of a shared-memory flag (pairs with the writer's fence + store)
+__device__ __forceinline__ int ld_acquire_smem(const volatile int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32((const void*)p)) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ void unpack8(const uint4 q, uint16_t* u) {
   u[0] = (uint16_t)(q.x & 0xffff); u[1] = (uint16_t)(q.x >> 16);
@@ -1343,7 +1349,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
 
   if (warp < NPW) {  // -------------------------------------------- region producers
     const long long p0 = STATS ? clock64() : 0;
-    long long pw = 0;
+    long long pw = 0, pm = 0, pi = 0;
     unsigned char* stgp = stg + (size_t)warp * L.stage_bytes;
     uint64_t* sb = sbar + warp;
     for (int i = warp; i < n_my; i += NPW) {
@@ -1360,12 +1366,15 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
         for (uint32_t o = 0; o < bytes; o += PIECE)
           bulk_g2s(stgp + o, src + o, bytes - o < PIECE ? bytes - o : PIECE, sb);
       }
+      const long long qm = STATS ? clock64() : 0;
       if (!mbar_wait_g(sb, (uint32_t)(i / NPW) & 1u, guard)) return;
+      if (STATS) pm += clock64() - qm;
       // the tile's meta block is staged BEFORE its buffer frees up (the
       // staging area is separate), so the refill starts right at the release
       const long long q0 = STATS ? clock64() : 0;
       if (i >= NB && !mbar_wait_g(empty + b, ph ^ 1u, guard)) return;
       if (STATS) pw += clock64() - q0;
+      const long long qi = STATS ? clock64() : 0;
       unsigned char* buf = sm + L.off_ring + (size_t)b * L.buf_bytes;
       const uint32_t* hsrc = reinterpret_cast<const uint32_t*>(stgp);
       uint32_t* hdst = reinterpret_cast<uint32_t*>(buf);
@@ -1379,9 +1388,9 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
       if (DIM == 2 && nruns > 0) {
         // contiguous id runs: TMA bulk copies of the interleaved coordinates
         const uint32_t* runs = hsrc + HW;
-        if (lane == 0) mbar_expect_tx_only(full + b, (uint32_t)nr * 16u);
+        if (lane == 0 && !(L.dbg & 4)) mbar_expect_tx_only(full + b, (uint32_t)nr * 16u);
         __syncwarp();
-        for (int r = lane; r < nruns; r += 32) {
+        for (int r = lane; r < nruns && !(L.dbg & 4); r += 32) {
           const uint32_t g = runs[2 * r], s0 = runs[2 * r + 1];
           const uint32_t s1 = r + 1 < nruns ? runs[2 * r + 3] : (uint32_t)nr;
           bulk_g2s(sc + 2 * s0, a0 + g, (s1 - s0) * 16u, full + b);
@@ -1408,10 +1417,13 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
         buf_tile[b] = i;
       }
       __syncwarp();
+      if (STATS) pi += clock64() - qi;
     }
     if (STATS && lane == 0) {
       atomicAdd(stats + 4, (unsigned long long)pw);
       atomicAdd(stats + 5, (unsigned long long)(clock64() - p0));
+      atomicAdd(stats + 9, (unsigned long long)pm);
+      atomicAdd(stats + 10, (unsigned long long)pi);
     }
     return;
   }
@@ -1601,18 +1613,19 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
       if (!__shfl_sync(FULL, alive, 0)) return;
       tile_ready = true;
     }
-    if (desc.y == 0) {
+    if (L.dbg & 1) {
+    } else if (desc.y == 0) {
 #pragma unroll
       for (int u = 0; u < UPL; ++u) {
         const int dep = (int)(r[u].pb >> 16);
         if (dep != 0xffff && dep >= item0) {
           guard.start();
-          while (alive && flags[dep] != i + 1) alive = guard.ok();
+          while (alive && ld_acquire_smem(flags + dep) != i + 1) alive = guard.ok();
         }
         const int d2 = d2v[u] & 0xFFF;
         if (d2 != GZ_DNONE && d2 >= item0) {
           guard.start();
-          while (alive && flags[d2] != i + 1) alive = guard.ok();
+          while (alive && ld_acquire_smem(flags + d2) != i + 1) alive = guard.ok();
         }
       }
     } else if (lane == 0) {
@@ -1624,24 +1637,28 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
         while (alive && *(volatile int*)(cnt + s2) != need) alive = guard.ok();
       }
     }
+    // the dependency flags were read with acquire loads, and __all_sync orders
+    // the other lanes' gathers after them; whole-stage waits take a fence
     if (!__all_sync(FULL, alive)) return;
-    fence_cta();
+    if (desc.y != 0 && !(L.dbg & 2)) fence_cta();
     int kn = 0;
     if (L.prefetch_claim && lane == 0) kn = atomicAdd(ctl, 1);
     const long long c2 = STATS ? clock64() : 0;
     double* sc = reinterpret_cast<double*>(buf + L.coord_off);
     const bool last = j == P - 1;
     const uint32_t padv = DIM == 2 ? (uint32_t)L.padbase : (uint32_t)GZ_PAD;  // the first pad slot
+    // 2D, two updates per lane: the owned results of the pass's last sweep go
+    // to global memory only after the item's release below, so the release
+    // fence does not wait for these stores
+    double2 oa = make_double2(0.0, 0.0), ob = oa;
+    bool wa = false, wb = false;
     if (UPL == 2 && DIM == 2) {
       const bool va = (r[0].pb & 0x7fffu) != 0x7fffu, vb = (r[UPL - 1].pb & 0x7fffu) != 0x7fffu;
-      double2 oa, ob;
       gz_update2<RMAX>(r[0], va, d2v[0] >> 12, r[UPL - 1], vb, d2v[UPL - 1] >> 12, R,
                        reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3),
                        reinterpret_cast<const uint4*>(rbase) + (lane + 32) * (R >> 3), sc, rcp, padv, oa, ob);
-      if (last) {  // owned vertices, final values of the pass
-        if (va && (r[0].pb & 0x8000u)) a1[r[0].gid] = oa;
-        if (vb && (r[UPL - 1].pb & 0x8000u)) a1[r[UPL - 1].gid] = ob;
-      }
+      wa = last && va && (r[0].pb & 0x8000u);  // owned vertices, final values of the pass
+      wb = last && vb && (r[UPL - 1].pb & 0x8000u);
     } else {
 #pragma unroll
       for (int u = 0; u < UPL; ++u)
@@ -1669,6 +1686,8 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
       if (desc.z) atomicAdd(cnt + sg, 1);  // stage counters: only tiles with whole-stage waits read them
       if (atomicAdd(ndone + (tb & 0xffff), 1) == pre_hi - pre_lo - 1) mbar_arrive(empty + (tb & 0xffff));
     }
+    if (wa) a1[r[0].gid] = oa;
+    if (wb) a1[r[UPL - 1].gid] = ob;
     kc_next = L.prefetch_claim ? __shfl_sync(FULL, kn, 0) : -1;
     if (STATS) {
       const long long c3 = clock64();
@@ -2240,6 +2259,7 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   L->sleep0 = env_int("LMS_GZ_SLEEP0", 20, 0, 1000);
   L->hint_rec = env_int("LMS_GZ_HINT", 0, 0, 1);
   L->prefetch_claim = env_int("LMS_GZ_PREFETCH_CLAIM", 1, 0, 1);
+  L->dbg = env_int("LMS_GZ_DBG", 0, 0, 255);
   L->sleep1 = env_int("LMS_GZ_SLEEP1", 128, 0, 10000);
   const int64_t coords = dim == 2 ? 16 * ((int64_t)L->padbase + 8) : 24 * r4(nd.max_slots);
   L->buf_bytes = (int)((L->coord_off + coords + 127) & ~(int64_t)127);
@@ -2378,8 +2398,8 @@ static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
   static unsigned long long* stats = nullptr;
   const bool want_stats = getenv("LMS_GZ_STATS") != nullptr;
   if (want_stats) {
-    if (!stats) LMS_TRY_CUDA(cudaMalloc(&stats, 9 * sizeof(unsigned long long)));
-    LMS_TRY_CUDA(cudaMemsetAsync(stats, 0, 9 * sizeof(unsigned long long), s));
+    if (!stats) LMS_TRY_CUDA(cudaMalloc(&stats, 12 * sizeof(unsigned long long)));
+    LMS_TRY_CUDA(cudaMemsetAsync(stats, 0, 12 * sizeof(unsigned long long), s));
   }
   const double2* a0 = DIM == 2 ? reinterpret_cast<const double2*>(m->xy[m->xy_cur].p) : nullptr;
   double2* a1 = DIM == 2 ? reinterpret_cast<double2*>(m->xy[1 - m->xy_cur].p) : nullptr;
@@ -2390,14 +2410,14 @@ static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
       want_stats ? stats : nullptr, m->err.p);
   LMS_CHECK_LAUNCH();
   if (want_stats) {
-    unsigned long long h[9];
+    unsigned long long h[12];
     LMS_TRY_CUDA(cudaMemcpyAsync(h, stats, sizeof(h), cudaMemcpyDeviceToHost, s));
     LMS_TRY_CUDA(cudaStreamSynchronize(s));
     const double it = h[3] ? (double)h[3] : 1.0;
     fprintf(stderr, "[gz stats] per item cycles: wait_tile=%.0f (record %.0f) wait_deps=%.0f compute=%.0f (items=%.0f)\n",
             h[0] / it, h[8] / it, h[1] / it, h[2] / it, it);
-    fprintf(stderr, "[gz stats] per CTA kcycles: producer wait_empty=%.1f of %.1f, record loader wait_empty=%.1f of %.1f\n",
-            h[4] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid, h[7] / 1e3 / grid);
+    fprintf(stderr, "[gz stats] per CTA kcycles: producer wait_empty=%.1f wait_meta=%.1f issue=%.1f of %.1f, record loader wait_empty=%.1f of %.1f\n",
+            h[4] / 1e3 / grid, h[9] / 1e3 / grid, h[10] / 1e3 / grid, h[5] / 1e3 / grid, h[6] / 1e3 / grid, h[7] / 1e3 / grid);
   }
 }
 

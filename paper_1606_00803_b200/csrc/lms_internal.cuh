@@ -107,6 +107,7 @@ struct GzLayout {
   int sleep0 = 20, sleep1 = 128;  // dependency-poll back-off (ns), first 64 polls / later
   int hint_rec = 0;             // records TMA'd with an L2 evict_first policy
   int prefetch_claim = 1;       // take the next claim while the current item computes
+  int dbg = 0;                  // timing experiments (LMS_GZ_DBG bits; wrong results): 1 no dependency waits, 2 no fence, 4 no region loads
 };
 
 // ----------------------------------------------------------------- schedule
