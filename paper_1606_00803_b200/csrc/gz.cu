@@ -384,18 +384,12 @@ __global__ void k_gzd_region(const uint64_t* __restrict__ reg, int64_t n, int C,
 __constant__ uint8_t kGapMasks[256] = {0, 1, 2, 4, 8, 16, 32, 64, 128, 3, 5, 6, 9, 10, 12, 17, 18, 20, 24, 33, 34, 36, 40, 48, 65, 66, 68, 72, 80, 96, 129, 130, 132, 136, 144, 160, 192, 7, 11, 13, 14, 19, 21, 22, 25, 26, 28, 35, 37, 38, 41, 42, 44, 49, 50, 52, 56, 67, 69, 70, 73, 74, 76, 81, 82, 84, 88, 97, 98, 100, 104, 112, 131, 133, 134, 137, 138, 140, 145, 146, 148, 152, 161, 162, 164, 168, 176, 193, 194, 196, 200, 208, 224, 15, 23, 27, 29, 30, 39, 43, 45, 46, 51, 53, 54, 57, 58, 60, 71, 75, 77, 78, 83, 85, 86, 89, 90, 92, 99, 101, 102, 105, 106, 108, 113, 114, 116, 120, 135, 139, 141, 142, 147, 149, 150, 153, 154, 156, 163, 165, 166, 169, 170, 172, 177, 178, 180, 184, 195, 197, 198, 201, 202, 204, 209, 210, 212, 216, 225, 226, 228, 232, 240, 31, 47, 55, 59, 61, 62, 79, 87, 91, 93, 94, 103, 107, 109, 110, 115, 117, 118, 121, 122, 124, 143, 151, 155, 157, 158, 167, 171, 173, 174, 179, 181, 182, 185, 186, 188, 199, 203, 205, 206, 211, 213, 214, 217, 218, 220, 227, 229, 230, 233, 234, 236, 241, 242, 244, 248, 63, 95, 111, 119, 123, 125, 126, 159, 175, 183, 187, 189, 190, 207, 215, 219, 221, 222, 231, 235, 237, 238, 243, 245, 246, 249, 250, 252, 127, 191, 223, 239, 247, 251, 253, 254, 255};
 __constant__ uint16_t kGapOff[10] = {0, 1, 9, 37, 93, 163, 219, 247, 255, 256};
 
-// slot of vertex g in a tile's region (ids sorted ascending, in shared memory)
-__device__ __forceinline__ int region_slot(const uint32_t* __restrict__ rid, int nr, uint32_t g) {
-  int lo = 0, n = nr;
-  while (n > 0) {
-    const int h = n >> 1;
-    if (rid[lo + h] < g) {
-      lo += h + 1;
-      n -= h + 1;
-    } else {
-      n = h;
-    }
-  }
+// slot of vertex g in a tile's region (ids sorted ascending, in shared memory,
+// padded with 0xFFFFFFFF up to p2 = the power of two >= the slot count):
+// branchless lower bound, one probe per halving of p2
+__device__ __forceinline__ int region_slot(const uint32_t* __restrict__ rid, int p2, uint32_t g) {
+  int lo = 0;
+  for (int step = p2; step > 0; step >>= 1) lo += (rid[lo + step - 1] < g) ? step : 0;
   return lo;
 }
 
@@ -460,7 +454,9 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
     const int64_t ra = reg_off[k], rb = reg_off[k + 1];
     const int nr = (int)(rb - ra);
     __syncthreads();  // the previous tile's searches are done
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) gz_rid[i] = (uint32_t)(reg[ra + i] & 0xffffffffull);
+    int p2 = 1;
+    while (p2 < nr) p2 <<= 1;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x) gz_rid[i] = i < nr ? (uint32_t)(reg[ra + i] & 0xffffffffull) : ~0u;
     __syncthreads();
     const GzTile t = tab[k];
     const int R = (int)t.R;
@@ -495,7 +491,7 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
             cnt = 1;
             const int32_t b = rp[v], d = rp[v + 1] - b;
             for (int w = 0; w < d && w < 8; ++w) {
-              const int sl = region_slot(gz_rid, nr, (uint32_t)col[b + w]);
+              const int sl = region_slot(gz_rid, p2, (uint32_t)col[b + w]);
               sl8[e * 8 + w] = (uint16_t)sl;
               const uint32_t bank = (uint32_t)sl & 7u;
               if (w < 7) {
@@ -614,7 +610,7 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
             uint16_t li = padv;
             const bool use = R == 8 ? (((gm >> w) & 1) && kk < d) : w < d;
             if (use) {
-              const int sl = R == 8 ? sl8[e * 8 + kk] : region_slot(gz_rid, nr, (uint32_t)col[b + kk]);
+              const int sl = R == 8 ? sl8[e * 8 + kk] : region_slot(gz_rid, p2, (uint32_t)col[b + kk]);
               ++kk;
               li = (uint16_t)sl;
               lo = min(lo, sl);
@@ -2111,7 +2107,9 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   }
   if (NI > 0) {
     DBuf<int32_t> it_lo(NI, s), it_hi(NI, s);
-    const int rid_bytes = (int)(4 * std::max<int64_t>(out->max_slots, 1));
+    int64_t p2max = 1;
+    while (p2max < out->max_slots) p2max <<= 1;
+    const int rid_bytes = (int)(4 * p2max);  // ids padded to a power of two (region_slot)
     LMS_TRY_CUDA(cudaFuncSetAttribute(k_gzd_records, cudaFuncAttributeMaxDynamicSharedMemorySize, rid_bytes));
     k_gzd_records<<<(unsigned)std::min<int64_t>(K, 1 << 20), 256, rid_bytes, s>>>(
         K, it_ks.p, it_q.p, C, P, upl, kc_off.p, cntj.p, ck2.p, cv2.p, tab.p, sfirst.p, m->row_ptr.p, m->col.p,
