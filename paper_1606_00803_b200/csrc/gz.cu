@@ -47,16 +47,16 @@
 //   rounded up to 8):
 //       u16 rows[32][R]   lane l's neighbour slots in CSR order (0xFFFF pad)
 //       u32 pb[32]        slot of lane l's vertex (0x7FFF: empty lane) | owned << 15
-//                         | dep_l << 16.  The item's updates are placed on lanes
-//                         by a greedy bank-aware assignment to quarter-warps
-//                         (2D), which cuts shared-memory bank conflicts
-//                         (dep_l: l-th item this one waits for, 0xFFFF none)
+//                         | dep_l << 16 | degree << 28.  The item's updates are
+//                         placed on lanes by a greedy bank-aware assignment to
+//                         quarter-warps (2D), which cuts shared-memory bank
+//                         conflicts (dep_l: l-th item this one waits for, 0xFFF
+//                         none; degree 0: > 15, counted)
 //       i32 gid[32]       global id of lane l's vertex
 //       u32 desc[4]       {n | sweep << 8 | stage << 16, mode, tile counts
 //                         stages, number of dependencies}; mode 1 = wait for
-//                         whole stages (more than 2U deps); then every item of
+//                         whole stages (more than U deps); then every item of
 //                         that tile increments the per-stage completion counters
-//       u16 dep2[32]      the dependencies beyond the first U
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_scan.cuh>
@@ -77,12 +77,13 @@ namespace lms {
 constexpr int GZ_MAX_C = 15;    // colours: 4 bits of the update sort key
 constexpr int GZ_MAX_P = 8;     // sweeps per pass: 3 bits of the update sort key
 constexpr uint16_t GZ_PAD = 0xFFFF;  // 3D row padding (predicated gathers)
-// 2D rows pad with the region's PAD SLOT (slot n_slots, staged as (-0.0, -0.0):
-// the identity of IEEE addition), so every gather is unpredicated.  The
-// update's degree then comes from the record: the second dependency word of
-// each position is (d << 12) | dependency, d = 0 when d > 15 (count instead),
-// dependency 0xFFF = none (a tile with 4095+ items waits for whole stages).
-constexpr uint16_t GZ_DNONE = 0xFFF;
+// 2D rows pad with the region's PAD SLOTS (after the largest region, staged as
+// (-0.0, -0.0): the identity of IEEE addition), so every gather is
+// unpredicated.  The update's degree then comes from the record: each
+// position's word is slot (15 bits) | owned (bit 15) | dependency (12 bits,
+// 0xFFF = none) | degree (4 bits, 0 when > 15: count instead).  An item lists
+// at most U dependencies (more, or a tile with 4095+ items: whole stages).
+constexpr uint32_t GZ_DNONE = 0xFFF;
 #ifndef LMS_GZ_REGS
 #define LMS_GZ_REGS 96
 #endif
@@ -94,10 +95,9 @@ constexpr int GZ_MAX_REGION = 32767;  // slots are 15 bits (bit 15 = owned flag)
 
 __host__ __device__ inline int64_t r4(int64_t n) { return (n + 3) & ~(int64_t)3; }
 __host__ __device__ inline int gz_hdr_words(int C, int P) { return (int)r4(4 + P * C + 1); }
-// record bytes for rows of R and U positions: rows, pb, gid, descriptor,
-// second dependency slot per position (u16)
-__host__ __device__ inline int gz_rec16(int R, int U) { return (2 * U * R + 8 * U + 16 + 2 * U) / 16; }
-__host__ __device__ inline int gz_dep2_off(int R, int U) { return 2 * U * R + 8 * U + 16; }
+// record bytes for rows of R and U positions: rows (u16), pb (u32: slot,
+// owned, dependency, degree), vertex ids (u32), descriptor (16 B)
+__host__ __device__ inline int gz_rec16(int R, int U) { return (2 * U * R + 8 * U + 16) / 16; }
 
 
 // ---------------------------------------------------------------- build kernels
@@ -476,7 +476,6 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
       uint32_t* pb = reinterpret_cast<uint32_t*>(base + 2 * U * R);
       int32_t* gid = reinterpret_cast<int32_t*>(base + 2 * U * R + 4 * U);
       uint32_t* desc = reinterpret_cast<uint32_t*>(base + 2 * U * R + 8 * U);
-      uint16_t* dep2 = reinterpret_cast<uint16_t*>(base + gz_dep2_off(R, U));
       // bank groups of each update (position-independent), then the placement
       if (R == 8) {
         for (int u0 = 0; u0 < U; u0 += 32) {
@@ -592,19 +591,18 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
       for (int u0 = 0; u0 < U; u0 += 32) {
         const int e = u0 + lane;
         const int pos = ps[e];
-        uint32_t p = 0xffff0000u | 0x7fffu;  // slot 0x7fff = empty position
+        uint32_t p = (GZ_DNONE << 16) | 0x7fffu;  // slot 0x7fff = empty position (degree 0)
         int32_t g = -1;
-        uint16_t dg = GZ_DNONE;  // degree bits (0 for an empty position)
         if (e < n) {
           const int64_t uu = kc_off[kc] + (int64_t)U * q + e;
           const int32_t v = cv[uu];
           const int lv = (int)(ck[uu] & 0xffffull);
           g = v;
-          p = 0xffff0000u | (uint32_t)lv | (tile_of[v] == (int32_t)k ? 0x8000u : 0u);
+          const int32_t b = rp[v], d = rp[v + 1] - b;
+          p = (GZ_DNONE << 16) | ((uint32_t)(d <= 15 ? d : 0) << 28) | (uint32_t)lv |
+              (tile_of[v] == (int32_t)k ? 0x8000u : 0u);
           lo = min(lo, lv);
           hi = max(hi, lv);
-          const int32_t b = rp[v], d = rp[v + 1] - b;
-          dg = (uint16_t)(((d <= 15 ? d : 0) << 12) | GZ_DNONE);
           const int gm = R == 8 ? gp[e] : 0;
           for (int w = 0, kk = 0; w < R; ++w) {
             uint16_t li = padv;
@@ -623,7 +621,6 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
         }
         pb[pos] = p;
         gid[pos] = g;
-        dep2[pos] = dg;
       }
       __syncwarp();
       if (dim == 2 && R == 8) {
@@ -683,17 +680,15 @@ __global__ void k_gzd_deps(const int32_t* __restrict__ it_ks, int64_t NI, int C,
     uint32_t* desc = reinterpret_cast<uint32_t*>(base + 2 * U * t.R + 8 * U);
     const int lo = it_lo[it], hi = it_hi[it];
     const int64_t a = sfirst[k * PC + (sg - C > 0 ? sg - C : 0)], b = sfirst[k * PC + sg];
-    uint16_t* dep2 = reinterpret_cast<uint16_t*>(base + gz_dep2_off(t.R, U));
-    for (int e = 0; e < U; ++e) dep2[e] = (uint16_t)((dep2[e] & 0xF000u) | GZ_DNONE);  // keep the degree bits
+    for (int e = 0; e < U; ++e) pb[e] = (pb[e] & 0xF000FFFFu) | (GZ_DNONE << 16);  // keep slot, owned, degree
     int nd = 0;
     for (int64_t o = a; o < b; ++o)
       if (it_lo[o] <= hi && it_hi[o] >= lo) {
-        if (nd < U) pb[nd] = (pb[nd] & 0xffffu) | ((uint32_t)(o - f0) << 16);
-        else if (nd < 2 * U) dep2[nd - U] = (uint16_t)((dep2[nd - U] & 0xF000u) | ((uint32_t)(o - f0) & 0xFFFu));
+        if (nd < U) pb[nd] = (pb[nd] & 0xF000FFFFu) | (((uint32_t)(o - f0) & GZ_DNONE) << 16);
         ++nd;
       }
     // dependencies are 12-bit item indices: a tile with 4095+ items waits for whole stages
-    const bool whole = nd > 2 * U || t.n_items >= GZ_DNONE;
+    const bool whole = nd > U || t.n_items >= GZ_DNONE;
     desc[1] = whole ? 1u : 0u;
     desc[3] = (uint32_t)nd;  // (informational: the number of overlapping earlier items)
     if (whole) atomicOr(&tneed[k], 1);
@@ -772,12 +767,9 @@ __global__ void k_gzd_permute(const int32_t* __restrict__ it_ks, const int32_t* 
     for (uint32_t q = lane; q < t.rec16; q += 32) dst[q] = src[q];
     __syncwarp();
     uint32_t* pb = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(dst) + 2 * U * t.R);
-    uint16_t* dep2 = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(dst) + gz_dep2_off(t.R, U));
     for (int e = lane; e < U; e += 32) {
-      const uint32_t d = pb[e] >> 16;
-      if (d != 0xffffu) pb[e] = (pb[e] & 0xffffu) | ((uint32_t)(newpos[f0 + d] - f0) << 16);
-      const uint32_t d2 = dep2[e] & 0xFFFu;
-      if (d2 != GZ_DNONE) dep2[e] = (uint16_t)((dep2[e] & 0xF000u) | ((uint32_t)(newpos[f0 + d2] - f0) & 0xFFFu));
+      const uint32_t d = (pb[e] >> 16) & GZ_DNONE;
+      if (d != GZ_DNONE) pb[e] = (pb[e] & 0xF000FFFFu) | (((uint32_t)(newpos[f0 + d] - f0) & GZ_DNONE) << 16);
     }
   }
 }
@@ -793,11 +785,9 @@ __global__ void k_gzd_check_order(const int32_t* __restrict__ it_ks, int64_t NI,
     const int64_t loc = it - sfirst[k * PC];
     const unsigned char* base = reinterpret_cast<const unsigned char*>(rec + t.rec_base + loc * t.rec16);
     const uint32_t* pb = reinterpret_cast<const uint32_t*>(base + 2 * U * t.R);
-    const uint16_t* dep2 = reinterpret_cast<const uint16_t*>(base + gz_dep2_off(t.R, U));
     for (int e = 0; e < U; ++e) {
-      const uint32_t d = pb[e] >> 16, d2 = dep2[e] & 0xFFFu;
-      if (d != 0xffffu && (int64_t)d >= loc) atomicAdd(bad, 1ull);
-      if (d2 != GZ_DNONE && (int64_t)d2 >= loc) atomicAdd(bad, 1ull);
+      const uint32_t d = (pb[e] >> 16) & GZ_DNONE;
+      if (d != GZ_DNONE && (int64_t)d >= loc) atomicAdd(bad, 1ull);
     }
   }
 }
@@ -1568,13 +1558,6 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     const int sg = (int)(desc.x >> 16);
     // this item's dependencies
     alive = 1;
-    // second dependency + degree bits of each of the lane's positions
-    int d2v[UPL];
-    {
-      const uint16_t* dep2 = reinterpret_cast<const uint16_t*>(rbase + gz_dep2_off(R, U));
-#pragma unroll
-      for (int u = 0; u < UPL; ++u) d2v[u] = dep2[lane + 32 * u];
-    }
     // the record is in registers now: hand its ring slot back before the
     // dependency waits and the compute, so the ring holds prefetched records
     // rather than items in progress (rows longer than RMAX read their tail
@@ -1590,7 +1573,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     uint32_t fold = desc.x ^ desc.y ^ desc.z ^ desc.w;
 #pragma unroll
     for (int u = 0; u < UPL; ++u) {
-      fold ^= r[u].pb ^ (uint32_t)r[u].gid ^ (uint32_t)d2v[u];
+      fold ^= r[u].pb ^ (uint32_t)r[u].gid;
 #pragma unroll
       for (int p = 0; p < RMAX / 8; ++p) fold ^= r[u].row[p].x ^ r[u].row[p].y ^ r[u].row[p].z ^ r[u].row[p].w;
     }
@@ -1613,15 +1596,10 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     } else if (desc.y == 0) {
 #pragma unroll
       for (int u = 0; u < UPL; ++u) {
-        const int dep = (int)(r[u].pb >> 16);
-        if (dep != 0xffff && dep >= item0) {
+        const int dep = (int)((r[u].pb >> 16) & GZ_DNONE);
+        if (dep != (int)GZ_DNONE && dep >= item0) {
           guard.start();
           while (alive && ld_acquire_smem(flags + dep) != i + 1) alive = guard.ok();
-        }
-        const int d2 = d2v[u] & 0xFFF;
-        if (d2 != GZ_DNONE && d2 >= item0) {
-          guard.start();
-          while (alive && ld_acquire_smem(flags + d2) != i + 1) alive = guard.ok();
         }
       }
     } else if (lane == 0) {
@@ -1650,7 +1628,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     bool wa = false, wb = false;
     if (UPL == 2 && DIM == 2) {
       const bool va = (r[0].pb & 0x7fffu) != 0x7fffu, vb = (r[UPL - 1].pb & 0x7fffu) != 0x7fffu;
-      gz_update2<RMAX>(r[0], va, d2v[0] >> 12, r[UPL - 1], vb, d2v[UPL - 1] >> 12, R,
+      gz_update2<RMAX>(r[0], va, (int)(r[0].pb >> 28), r[UPL - 1], vb, (int)(r[UPL - 1].pb >> 28), R,
                        reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3),
                        reinterpret_cast<const uint4*>(rbase) + (lane + 32) * (R >> 3), sc, rcp, padv, oa, ob);
       wa = last && va && (r[0].pb & 0x8000u);  // owned vertices, final values of the pass
@@ -1662,7 +1640,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
           const int nr4 = DIM == 3 ? (int)r4(reinterpret_cast<const uint32_t*>(buf)[1]) : 0;
           double ox, oy, oz;
           gz_update<DIM, RMAX>(r[u], R, reinterpret_cast<const uint4*>(rbase) + (lane + 32 * u) * (R >> 3), sc,
-                               rcp, nr4, padv, DIM == 2 ? (d2v[u] >> 12) : 0, ox, oy, oz);
+                               rcp, nr4, padv, DIM == 2 ? (int)(r[u].pb >> 28) : 0, ox, oy, oz);
           if (last && (r[u].pb & 0x8000u)) {
             if (DIM == 2) {
               a1[r[u].gid] = make_double2(ox, oy);
