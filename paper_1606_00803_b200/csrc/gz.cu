@@ -1503,7 +1503,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
   unsigned long long w_wait = 0, w_dep = 0, w_comp = 0, w_items = 0, w_rec = 0;
   bool tile_ready = false;
   constexpr int U = 32 * UPL;  // updates per item; lane l handles positions l, l + 32
-  const int bs_log2 = L.BS_log2;
+  const unsigned long long bs_magic = L.bs_magic;  // claim / BS = (claim * magic) >> 40
   // The next claim is taken while the current item computes (its atomic's
   // latency -- 18 warps contend on one counter -- is hidden).  Holding a
   // claim while computing cannot deadlock: the current item waits only for
@@ -1526,10 +1526,10 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     const int t = item0 + (kc - pre_lo);
     const long long c0 = STATS ? clock64() : 0;
     // the item's record, from the record ring
-    const int bat = kc >> bs_log2;
+    const int bat = (int)(((unsigned long long)kc * bs_magic) >> 40);
     const int slot = bat & (RR - 1);
     const unsigned char* rbase =
-        rring + ((size_t)slot * L.BS + (kc & (L.BS - 1))) * L.rec_bytes;
+        rring + ((size_t)slot * L.BS + (kc - bat * L.BS)) * L.rec_bytes;
     int alive = 1;
     if (lane == 0) {
       guard.start();
@@ -2217,8 +2217,13 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   // batch and tile): 8.  C4 (64-update records of 1,680 B, 32 in the ring):
   // 4 x 8 = 263.5 us per sweep, 8 x 4 = 266.7, 16 x 2 = 470 (32-update
   // records: 8 x 8, fewer batches measured 1.7x slower)
+  // The shared memory left over after the buffers deepens the ring: BS grows
+  // (any size: a claim's batch is a magic multiply) while RR * BS records fit,
+  // up to 16; C4 (1,552 B records): 4 x 9 = 255.4 us, 4 x 8 = 258.0, 4 x 7 =
+  // 263.6.  LMS_GZ_BS fixes it.
   L->BS_log2 = env_int("LMS_GZ_BS_LOG2", 3, 0, 4);
-  L->BS = 1 << L->BS_log2;
+  const bool bs_fixed = getenv("LMS_GZ_BS") != nullptr;
+  L->BS = env_int("LMS_GZ_BS", 1 << L->BS_log2, 1, 64);
   L->RR = env_int("LMS_GZ_RR", upl == 2 ? 4 : 8, 2, 64);
   while (L->RR & (L->RR - 1)) ++L->RR;
   while (L->RR * L->BS < nw + L->BS) L->RR *= 2;
@@ -2253,9 +2258,19 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
     L->off_stage = L->off_tab + tab_bytes;
     L->off_rec = L->off_stage + L->NPW * L->stage_bytes;
     L->off_ring = (L->off_rec + L->RR * L->BS * L->rec_bytes + 127) & ~127;
-    const int64_t total = (int64_t)L->off_ring + (int64_t)nb * L->buf_bytes;
-    if (total <= cap) return total;
-    if (want_nb > 0) return total;
+    int64_t total = (int64_t)L->off_ring + (int64_t)nb * L->buf_bytes;
+    if (total <= cap || want_nb > 0) {
+      while (total <= cap && !bs_fixed && L->BS < 16) {  // deepen the ring into the leftover
+        const int off2 = (L->off_rec + L->RR * (L->BS + 1) * L->rec_bytes + 127) & ~127;
+        const int64_t t2 = (int64_t)off2 + (int64_t)nb * L->buf_bytes;
+        if (t2 > cap) break;
+        ++L->BS;
+        L->off_ring = off2;
+        total = t2;
+      }
+      L->bs_magic = ((1ull << 40) + (unsigned long long)L->BS - 1) / (unsigned long long)L->BS;
+      return total;
+    }
   }
   return (int64_t)cap + 1;
 }
@@ -2346,9 +2361,9 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
       S.gz_cps = cps;
       S.gz_threads = 32 * (S.gz_L.NPW + 1 + S.gz_L.NW);
       if (getenv("LMS_GZ_VERBOSE"))
-        fprintf(stderr, "[gz] %s T=%d P=%d tiles=%lld items=%lld NB=%d RR=%d NW=%d smem=%d buf=%d slots<=%lld "
+        fprintf(stderr, "[gz] %s T=%d P=%d tiles=%lld items=%lld NB=%d RR=%d BS=%d NW=%d smem=%d buf=%d slots<=%lld "
                 "items/tile<=%lld regions=%lld updates=%lld blob=%lld B meta16/tile=%lld NPW=%d\n", kd ? "kd" : "bins", t, P, (long long)S.gz_ntiles,
-                (long long)S.gz_items, S.gz_L.NB, S.gz_L.RR, S.gz_L.NW, S.gz_smem, S.gz_L.buf_bytes,
+                (long long)S.gz_items, S.gz_L.NB, S.gz_L.RR, S.gz_L.BS, S.gz_L.NW, S.gz_smem, S.gz_L.buf_bytes,
                 (long long)nd.max_slots, (long long)nd.max_items, (long long)S.gz_nreg, (long long)S.gz_nupd,
                 (long long)S.gz_bytes, (long long)nd.mean_meta16, S.gz_L.NPW);
       return true;

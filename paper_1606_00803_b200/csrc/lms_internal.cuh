@@ -96,6 +96,7 @@ struct GzLayout {
   int NB = 0, NPW = 0, NW = 0;  // region buffers, producer warps, worker warps
   int RR = 0, RR_log2 = 0, rec_bytes = 0, off_rec = 0;  // record ring: batches (power of 2), bytes per record
   int BS = 8, BS_log2 = 3;      // records per batch
+  unsigned long long bs_magic = 0;  // ceil(2^40 / BS): claim / BS for claims < 2^24
   int U = 32;                   // updates per item (32 * updates per lane)
   int hdr_bytes = 0;            // per buffer header copy
   int flag_off = 0, cnt_off = 0, coord_off = 0, buf_bytes = 0;  // inside a buffer
