@@ -1817,6 +1817,20 @@ __global__ void k_kd_tile(const int32_t* __restrict__ sorted_ids, int64_t V, int
   }
 }
 
+// balanced: Kt tiles in nbx strips, `extra` strips with base + 1 tiles and the
+// rest with base; a strip's vertices split evenly over its tiles
+__global__ void k_kd_tile_bal(const int32_t* __restrict__ sorted_ids, int64_t V, int64_t per_strip, int64_t base,
+                              int64_t extra, int32_t* tile_of) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < V; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t strip = p / per_strip;
+    const int64_t r = p - strip * per_strip;
+    const int64_t len = min(per_strip, V - strip * per_strip);
+    const int64_t nt = base + (strip < extra ? 1 : 0);
+    const int64_t t0 = strip * base + min(strip, extra);
+    tile_of[sorted_ids[p]] = (int32_t)(t0 + r * nt / len);
+  }
+}
+
 static int64_t kd_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) {
   sync_soa(m, s);
   const int64_t V = m->V;
@@ -1854,6 +1868,13 @@ static int64_t kd_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) 
       tps = bt;
     }
   }
+  // many tiles per SM: round the tile count up to a multiple of the SM count
+  // (tiles go to the persistent CTAs round-robin, so 4096 tiles on 148 SMs
+  // leave a third of the CTAs idle for the last tile), spread over the same
+  // strips with base or base + 1 tiles each (tiles stay near square)
+  int64_t kbal = 0;
+  if (nsm > 0 && K0 >= 4 * (int64_t)nsm && K0 % nsm && env_int("LMS_GZ_BALANCE", 1, 0, 1))
+    kbal = (K0 + nsm - 1) / nsm * nsm;
   const int64_t per_strip = (V + nbx - 1) / nbx;
   T = (int)((per_strip + tps - 1) / tps);
   DBuf<uint32_t> k1(V, s), k2(V, s);
@@ -1868,6 +1889,11 @@ static int64_t kd_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) 
   k_kd_ykey<<<gsz(V), 256, 0, s>>>(i2.p, m->x[1].p, V, per_strip, sb, k1.p, i1.p);
   LMS_CHECK_LAUNCH();
   LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k1.p, k2.p, i1.p, i2.p, V, 0, 32, s));
+  if (kbal > 0) {
+    k_kd_tile_bal<<<gsz(V), 256, 0, s>>>(i2.p, V, per_strip, kbal / nbx, kbal % nbx, tile_of);
+    LMS_CHECK_LAUNCH();
+    return kbal;
+  }
   k_kd_tile<<<gsz(V), 256, 0, s>>>(i2.p, V, per_strip, T, tps, tile_of);
   LMS_CHECK_LAUNCH();
   return nbx * tps;
