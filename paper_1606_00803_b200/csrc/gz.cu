@@ -85,7 +85,7 @@ constexpr uint16_t GZ_PAD = 0xFFFF;  // 3D row padding (predicated gathers)
 // at most U dependencies (more, or a tile with 4095+ items: whole stages).
 constexpr uint32_t GZ_DNONE = 0xFFF;
 #ifndef LMS_GZ_REGS
-#define LMS_GZ_REGS 96
+#define LMS_GZ_REGS 80
 #endif
 constexpr int GZ_REGS2 = LMS_GZ_REGS;  // register budget of the 2D two-updates-per-lane sweep
 constexpr int GZ_MAX_REGION = 32767;  // slots are 15 bits (bit 15 = owned flag)
@@ -1233,8 +1233,8 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, int d
 // records into the record ring (one TMA bulk copy per record, in claim
 // order), warps 2.. are workers (one claimed item at a time).
 template <int DIM, int RMAX, int UPL, bool STATS>
-// register budget per thread for the CTA's threads (2D 64-update items: 21
-// warps x 96; 32-update items: 25 x 80; 3D: 13 x 152)
+// register budget per thread for the CTA's threads (2D 64-update items: 24
+// warps x 80; 32-update items: 24 x 80; 3D: 12 x 152)
 __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
                                                                       const GzTile* __restrict__ tab,
                                                                       const int32_t* __restrict__ item_sweep,
@@ -2327,18 +2327,17 @@ bool build_gz(lms_mesh_s* m, int T, int P, bool required, cudaStream_t s) {
   // ambiguity under out-of-order TMA completion, fixed by rbat.)
   const int upl = env_int("LMS_GZ_UPL", m->dim == 2 ? 2 : 1, 1, m->dim == 2 ? 2 : 1);
   // warps per CTA: the register file is 16 K registers per scheduler and the
-  // CTA's warps are spread over 4 schedulers, so at the kernel's register
-  // budget (__maxnreg__) at most 20 warps (96 regs, 64-update items), 24 (80)
-  // or 12 (3D, 152)
-  // (one warp below the register file's quotient: 21 x 96 registers fails
-  // to launch with "too many resources")
-  const int cap_warps = (m->dim == 2 ? (upl == 2 ? 65536 / (GZ_REGS2 * 32) - 1 : 24) : 12) / cps;
+  // CTA's warps are spread over the 4 schedulers, so at the kernel's register
+  // budget (__maxnreg__) at most 4 x floor(16384 / (32 x regs)) warps: 24 at
+  // 80 registers (64-update items), 20 at 96, 12 in 3D (152)
+  const int cap_warps = (m->dim == 2 ? (upl == 2 ? 4 * (16384 / (GZ_REGS2 * 32)) : 24) : 12) / cps;
   const int maxw = cap_warps;  // producers + loader + workers
-  // workers measured best on C4: 18 with 2 updates per lane, 22 with 1 (more
-  // warps only lengthen every item: the shared-memory pipe is the shared
-  // resource); + region producer + record loader
+  // workers measured best on C4: 21 at 80 registers with 2 updates per lane
+  // (250.3 us; 96 registers / 18 workers 254.0, 88 / 18 252.2, 80 / 20
+  // 250.8, 80 / 22 250.9, 72 / 21-24 251.4-253.8), 22 with 1; + region
+  // producer + record loader
   const int nw_env = env_int("LMS_GZ_WORKERS", 0, 0, maxw - 2);
-  const int nw = nw_env ? nw_env : std::min(maxw - 2, m->dim == 2 ? (upl == 2 ? 18 : 22) : 10);
+  const int nw = nw_env ? nw_env : std::min(maxw - 2, m->dim == 2 ? (upl == 2 ? 21 : 22) : 10);
   const int want_nb = env_int("LMS_GZ_BUFFERS", cps == 2 ? 1 : 0, 0, 8);
   const int dim = m->dim, C = m->C;
   GzNeeds nd;
