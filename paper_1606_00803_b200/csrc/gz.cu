@@ -553,8 +553,11 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
         // class and the group takes the arg-min (lowest mask on ties)
         for (int e = lane; e < U; e += 32) od[ps[e]] = (uint8_t)e;  // od := position -> update
         __syncwarp();
-        for (int a0 = 0; a0 < ng; a0 += 4) {
-          const int a = a0 + (lane >> 3), sub = lane & 7;
+        // SUB lanes per group: all 8 groups of a 64-update item in one round
+        // (4 lanes each), the 4 of a 32-update item with 8 lanes each
+        const int SUB = ng >= 8 ? 4 : 8;
+        for (int a0 = 0; a0 < ng; a0 += 32 / SUB) {
+          const int a = a0 + lane / SUB, sub = lane % SUB;
           uint64_t occ = 0;  // bit 8 * bank + w: bank already read at position w
           for (int j = 0; j < 8; ++j) {
             const int e = a < ng ? od[8 * a + j] : 0;
@@ -569,10 +572,10 @@ __global__ void __launch_bounds__(256) k_gzd_records(int64_t K, const int32_t* _
                 hit |= ((occ >> (8 * ((nb >> (3 * kk)) & 7u))) & 0xffull) << (8 * kk);
               // collisions of a mask = popc(hit & selection); the table index
               // orders masks of one popcount ascending, so it breaks ties
-              for (int t = gz_goff[dn] + sub; t < gz_goff[dn + 1]; t += 8)
+              for (int t = gz_goff[dn] + sub; t < gz_goff[dn + 1]; t += SUB)
                 key = min(key, (__popcll(hit & gz_gsel[t]) << 8) | t);
             }
-            for (int o = 1; o < 8; o <<= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+            for (int o = 1; o < SUB; o <<= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
             const int best = dn >= 8 ? 0xff : (dn > 0 ? (int)gz_gmsk[key & 0xff] : 0);
             if (a < ng && sub == 0) gp[e] = (uint8_t)best;
             // neighbour k's position (byte k of the selection) into its bank's byte
