@@ -144,6 +144,11 @@ struct Schedule {
   DBuf<long long> s2_choff;
   DBuf<int32_t> s2_chw;
   std::vector<int64_t> s2_cstart;  // [C + 1] first chunk of each colour
+  DBuf<int32_t> s2_crange;        // [C * (G + 1)] persistent S2: chunk range of each (colour, CTA)
+  int s2_G = 0;                    // persistent S2 CTAs (one per SM, at most K)
+  int s2_wmax = 16;                // widest item row count (S2 ring slot size)
+  DBuf<int32_t> s2_nbptr, s2_nb;  // persistent S2: CTA neighbour lists (CSR over CTAs)
+  DBuf<unsigned> s2_prog;          // [G] persistent S2: passes published per CTA
   // GZ (ghost-zone tiled sweep, gz.cu): per tile a region = owned free vertices
   // plus every vertex within C*P hops; a persistent kernel stages regions in
   // shared memory and runs P whole sweeps there, reading X and writing the

@@ -309,9 +309,19 @@ static void build_base(lms_mesh_s* m, cudaStream_t s, bool gz_base) {
   const bool want_s3 = !gz_base && m->sched_req == LMS_SCHED_S3;
   // tiling: S3 defaults to spatial cells of ~4096 vertices; S1 to storage tiles
   // of ~256*C vertices (one vertex per thread of a 256-thread CTA per item)
+  // S2 (3D): spatial boxes, ~4 per SM (the persistent S2 kernel gives each
+  // CTA consecutive boxes, so its chunks' neighbourhoods overlap in L1)
+  const bool want_s2 = !gz_base && (m->sched_req == LMS_SCHED_S2 || (m->sched_req == LMS_SCHED_AUTO && m->dim == 3));
   int tiling = m->tiling_req;
-  if (tiling == LMS_TILING_AUTO) tiling = want_s3 ? LMS_TILING_SPATIAL : LMS_TILING_STORAGE;
+  if (tiling == LMS_TILING_AUTO) tiling = (want_s3 || want_s2) ? LMS_TILING_SPATIAL : LMS_TILING_STORAGE;
   int T = m->tile_req;
+  if (T == 0 && want_s2) {
+    int nsm = 148;
+    LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+    int per = 8;  // tiles per SM (LMS_S2_TILES_PER_SM tunes)
+    if (const char* e = getenv("LMS_S2_TILES_PER_SM")) per = std::max(1, atoi(e));
+    T = (int)std::max<int64_t>(256, std::min<int64_t>(1 << 20, V / (per * (int64_t)nsm)));
+  }
   if (T == 0) T = want_s3 ? 4096 : 256 * C;
   if (T > V) T = (int)((V + 31) / 32 * 32);
   if (T < 32) T = 32;
@@ -495,6 +505,10 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   S.base_valid = false;
   S.s2_choff.release();  // S2 chunk lists belong to the previous schedule
   S.s2_chw.release();
+  S.s2_crange.release();
+  S.s2_nbptr.release();
+  S.s2_nb.release();
+  S.s2_prog.release();
   if (m->sched_req == LMS_SCHED_JACOBI) {  // N3 variant (jacobi.cu): no schedule tables
     S.kind = LMS_SCHED_JACOBI;
     S.valid = true;

@@ -307,6 +307,28 @@ def test_C3_full_bfs_rdr():
         gm.close()
 
 
+@pytest.mark.parametrize("persistent", ["1", "0"])
+def test_s2_persistent_and_pass_launches(persistent, monkeypatch):
+    """The 3D S2 sweep in both launch forms: one cooperative launch for every
+    pass (spatial boxes over ~148 CTAs, ragged chunk ranges per CTA, grid
+    barriers between colours) and one launch per colour; bit-exact against
+    the oracle's colour-GS schedule under three orderings (Eq. 1)."""
+    monkeypatch.setenv("LMS_S2_PERSISTENT", persistent)
+    m = meshgen.kuhn3d(45, 0.25, seed=21)
+    om = oracle.prepare(m)
+    for kind in ["original", "bfs", "random"]:
+        seed = 803 if kind == "random" else 0
+        perm = oracle.order(om, kind, seed)
+        pm = oracle.permute_mesh(om, perm)
+        want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 6)
+        with gpu_mesh(m) as gm:
+            gm.permute(cuda(perm))
+            gm.set_schedule("s2")
+            gm.smooth(1)
+            gm.smooth(5)
+            assert bits_equal(gpu_coords(gm), want), (kind, persistent, gm.schedule_info())
+
+
 def test_C4_full_bench_config():
     """BASELINE.json configs[3] (the bench workload), original ordering, the
     launch configuration bench.py times (AUTO -> GZ), 3 sweeps bit-exact."""
