@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include <cooperative_groups.h>
 
@@ -630,6 +631,94 @@ __global__ void k_rdr_walk(const int32_t* __restrict__ rp, const int32_t* __rest
   if (lane == 0) { stats[0] = next; stats[1] = walks; }
 }
 
+// The walk over an ELL copy of the presorted rows (row v at v * WM, -1
+// padded; WM = the maximum degree rounded up to 8 or 16): a step loads, per
+// lane, its neighbour u's state AND u's whole row (WM / 4 16-byte loads) in
+// ONE round of independent loads, so when l0 = l[0] is chosen its row is
+// already in lane src's registers and moves to the lanes by shuffles.  A
+// step is one dependent memory round instead of two (row, then states), and
+// the row-bound loads are gone.  Same order as k_rdr_walk (Alg. 2).
+template <int WM>
+__global__ void k_rdr_walk_ell(const int32_t* __restrict__ ell, const int32_t* __restrict__ outer, int64_t n_outer,
+                               uint8_t* st, int32_t* perm, long long* stats /* [next, walks] */) {
+  const int lane = threadIdx.x;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  long long next = 0, walks = 0;
+  int64_t oi = 0;
+  while (oi < n_outer) {
+    const int64_t idx = oi + lane;
+    const int32_t i_l = idx < n_outer ? __ldg(outer + idx) : -1;
+    const int p_l = i_l >= 0 ? st[i_l] : 2;
+    const unsigned bal = __ballot_sync(FULL, p_l < 2);
+    if (bal == 0) { oi += 32; continue; }
+    const int first = __ffs(bal) - 1;
+    const int32_t i = __shfl_sync(FULL, i_l, first);
+    const int si = __shfl_sync(FULL, p_l, first);
+    oi += first + 1;
+    if (lane == 0) {
+      if (si == 0) perm[next] = i;
+      st[i] = 2;
+    }
+    next += si == 0 ? 1 : 0;
+    ++walks;
+    // lane j < WM holds l[j]: the j-th neighbour of cur in (quality, label) order
+    int32_t u = lane < WM ? __ldg(ell + (int64_t)i * WM + lane) : -1;
+    __syncwarp();
+    for (;;) {
+      int su = 2;
+      int32_t row[WM];
+      if (u >= 0) {  // one round: u's state and u's row
+        su = st[u];
+        const int4* rp4 = reinterpret_cast<const int4*>(ell + (int64_t)u * WM);
+#pragma unroll
+        for (int q = 0; q < WM / 4; ++q) {
+          const int4 t = __ldg(rp4 + q);
+          row[4 * q] = t.x;
+          row[4 * q + 1] = t.y;
+          row[4 * q + 2] = t.z;
+          row[4 * q + 3] = t.w;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < WM; ++q) row[q] = -1;
+      }
+      const unsigned unp = __ballot_sync(FULL, su < 2);
+      const unsigned app = __ballot_sync(FULL, su == 0);
+      if (su == 0) {
+        perm[next + __popc(app & lt)] = u;
+        st[u] = 1;
+      }
+      next += __popc(app);
+      if (unp == 0) break;
+      const int src = __ffs(unp) - 1;
+      const int32_t l0 = __shfl_sync(FULL, u, src);
+      int32_t un = -1;
+#pragma unroll
+      for (int q = 0; q < WM; ++q) {
+        const int32_t t = __shfl_sync(FULL, row[q], src);
+        if (lane == q) un = t;
+      }
+      __syncwarp();
+      if (lane == 0) st[l0] = 2;
+      __syncwarp();
+      u = un;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) { stats[0] = next; stats[1] = walks; }
+}
+
+__global__ void k_fill_ell(const int32_t* __restrict__ rp, const int32_t* __restrict__ scol, int64_t V, int WM,
+                           int32_t* __restrict__ ell) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < V * WM; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / WM;
+    const int j = (int)(t - v * WM);
+    const int32_t b = rp[v], e = rp[v + 1];
+    ell[t] = j < e - b ? scol[b + j] : -1;
+  }
+}
+
 __global__ void k_state_unsorted(const uint8_t* __restrict__ st, int64_t V, uint8_t* flags, int32_t* ids) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     flags[v] = st[v] == 0 ? 1 : 0;
@@ -677,8 +766,36 @@ void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s) {
   DBuf<uint8_t> state(V, s);
   LMS_TRY_CUDA(cudaMemsetAsync(state.p, 0, V, s));
   DBuf<long long> stats(2, s);
-  k_rdr_walk<<<1, 32, 0, s>>>(m->row_ptr.p, scol.p, outer.p, n_outer, state.p, d_perm, stats.p);
-  LMS_CHECK_LAUNCH();
+  // the ELL walk for maximum degree <= 16 (LMS_RDR_ELL=0: the CSR walk)
+  int md = 0;
+  {
+    DBuf<int> dmd(1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(dmd.p, 0, sizeof(int), s));
+    k_max_degree<<<Gv, 256, 0, s>>>(m->row_ptr.p, V, dmd.p);
+    LMS_CHECK_LAUNCH();
+    LMS_TRY_CUDA(cudaMemcpyAsync(&md, dmd.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  }
+  const char* ee = getenv("LMS_RDR_ELL");
+  const int WM = md <= 8 ? 8 : md <= 16 ? 16 : 0;
+  if (WM > 0 && !(ee && !strcmp(ee, "0"))) {
+    DBuf<int32_t> ell(V * WM, s);
+    const unsigned Ge = grid_for(V * WM, 256) > 8192 ? 8192 : grid_for(V * WM, 256);
+    k_fill_ell<<<Ge, 256, 0, s>>>(m->row_ptr.p, scol.p, V, WM, ell.p);
+    LMS_CHECK_LAUNCH();
+    scol.release();
+    // (a two-hop L1 prefetch of the candidates' rows and states measured
+    // slower: C4 8.5 -> 9.5 s)
+    if (WM == 8)
+      k_rdr_walk_ell<8><<<1, 32, 0, s>>>(ell.p, outer.p, n_outer, state.p, d_perm, stats.p);
+    else
+      k_rdr_walk_ell<16><<<1, 32, 0, s>>>(ell.p, outer.p, n_outer, state.p, d_perm, stats.p);
+    LMS_CHECK_LAUNCH();
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));  // ell is released on return
+  } else {
+    k_rdr_walk<<<1, 32, 0, s>>>(m->row_ptr.p, scol.p, outer.p, n_outer, state.p, d_perm, stats.p);
+    LMS_CHECK_LAUNCH();
+  }
   long long hs[2] = {0, 0};
   LMS_TRY_CUDA(cudaMemcpyAsync(hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
   LMS_TRY_CUDA(cudaStreamSynchronize(s));

@@ -148,3 +148,20 @@ def test_fan_mesh_orderings():
         assert np.array_equal(np_(gm.order("bfs", 0)), oracle.order_bfs(om["row_ptr"], om["col"], 0))
         q = oracle.quality(m["coords"], m["elems"])
         assert np.array_equal(np_(gm.order("rdr")), oracle.order_rdr(om["row_ptr"], om["col"], om["fixed"], q))
+
+
+@pytest.mark.parametrize("ell", ["1", "0"])
+def test_rdr_walk_forms(ell, monkeypatch):
+    """Alg. 2 on the GPU in both walk forms: the ELL walk (one
+    load round per step, max degree <= 16: the 2D grids' 8 and the Kuhn
+    meshes' 14) and the CSR walk (LMS_RDR_ELL=0; also every mesh of higher
+    degree, e.g. the fan's 90-spoke hub), bit-exact against the oracle on a
+    disconnected 2D mesh and a 3D Kuhn mesh."""
+    monkeypatch.setenv("LMS_RDR_ELL", ell)
+    for m in (DISCONNECTED[1][1](), meshgen.kuhn3d(17, 0.25, seed=61)):
+        om = oracle.prepare(m)
+        om["fixed"] = oracle.boundary(m.V, m["elems"]) if m["dim"] == 2 else om["fixed"]
+        q = oracle.quality(m["coords"], m["elems"])
+        with gpu_mesh(m) as gm:
+            assert np.array_equal(np_(gm.order("rdr")),
+                                  oracle.order_rdr(om["row_ptr"], om["col"], om["fixed"], q)), (ell, m.V)
