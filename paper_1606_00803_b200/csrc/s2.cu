@@ -291,9 +291,14 @@ __device__ __forceinline__ double4 s2_gather(const double4* p, uint64_t pl) {
   return HINT ? s2_ld4(p, pl) : s2_ld4_plain(p);
 }
 
-// one staged chunk: ids from the slot, gathers in NB batches, CSR-order sums
-template <int WMAX, int NB, bool HINT>
-__device__ __forceinline__ void s2r_chunk(const int32_t (&u)[WMAX], int32_t v, double4* X, uint64_t pl, int dbg) {
+// one staged chunk: ids from the slot, gathers in NB batches, CSR-order sums.
+// The row positions q < W (W uniform over the chunk) are gathered without
+// per-lane predication: a -1 entry (a row shorter than W) reads the pad
+// vertex X[padv] = (-0, -0, -0), the identity of IEEE addition, and is not
+// counted in the degree.
+template <int WMAX, int NB>
+__device__ __forceinline__ void s2r_chunk(const int32_t (&u)[WMAX], int W, int32_t v, double4* X, int32_t padv,
+                                          uint64_t pl) {
   constexpr int H = WMAX / NB;
   double sx = 0.0, sy = 0.0, sz = 0.0;
   int d = 0;
@@ -302,12 +307,15 @@ __device__ __forceinline__ void s2r_chunk(const int32_t (&u)[WMAX], int32_t v, d
     double4 g[H];
 #pragma unroll
     for (int q = 0; q < H; ++q)
-      if (u[h * H + q] >= 0)
-        g[q] = (dbg & 8) ? make_double4((double)u[h * H + q], 1.0, 2.0, 0.0) : s2_gather<WMAX, HINT>(X + u[h * H + q], pl);
+      if (h * H + q < W) {
+        const int32_t x = u[h * H + q];
+        g[q] = s2_ld4(X + (x >= 0 ? x : padv), pl);
+        d += x >= 0 ? 1 : 0;
+      }
 #pragma unroll
     for (int q = 0; q < H; ++q)
-      if (u[h * H + q] >= 0) {
-        if (d == 0) {
+      if (h * H + q < W) {
+        if (h * H + q == 0) {
           sx = g[q].x;
           sy = g[q].y;
           sz = g[q].z;
@@ -316,7 +324,6 @@ __device__ __forceinline__ void s2r_chunk(const int32_t (&u)[WMAX], int32_t v, d
           sy = __dadd_rn(sy, g[q].y);
           sz = __dadd_rn(sz, g[q].z);
         }
-        ++d;
       }
   }
   if (v >= 0) {
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__((NCONS + 1) * 32, 1)
     k_sweep_s2p(const long long* __restrict__ choff, const int32_t* __restrict__ chw,
                 const int32_t* __restrict__ crange, int G, int C, long long npass, const int32_t* __restrict__ slab,
                 double4* X, int opts, unsigned long long* stats, const int32_t* __restrict__ nb_ptr,
-                const int32_t* __restrict__ nb, unsigned* prog, int* err, int R, int slot_ints) {
+                const int32_t* __restrict__ nb, unsigned* prog, int* err, int R, int slot_ints, int32_t padv) {
   extern __shared__ __align__(128) unsigned char s2_sm[];
   int32_t* ring = reinterpret_cast<int32_t*>(s2_sm);
   uint64_t* full = reinterpret_cast<uint64_t*>(s2_sm + (size_t)R * slot_ints * 4);
@@ -339,6 +346,7 @@ __global__ void __launch_bounds__((NCONS + 1) * 32, 1)
   int32_t* s_w = reinterpret_cast<int32_t*>(s_off + R);
   __shared__ int s_abort;
   __shared__ int s_fold[NCONS];
+  __shared__ int s_claim;
   const uint64_t pf = s2_policy_first(), pl = s2_policy_last();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x;
@@ -420,10 +428,15 @@ __global__ void __launch_bounds__((NCONS + 1) * 32, 1)
       __syncwarp();
       if (lane == 0) __threadfence();  // L1 invalidate (CCTL.IVALL) after the acquires
     }
+    if (threadIdx.x == 0) s_claim = 0;
     s2_cons_sync(NCONS);
     if (*sab) return;
     if (stats && threadIdx.x == 0) t0 = s2_gtimer();
-    for (int k = warp; k < n; k += NCONS) {
+    for (;;) {  // chunks claimed in order (a warp done early takes the next)
+      int k = 0;
+      if (lane == 0) k = atomicAdd(&s_claim, 1);
+      k = __shfl_sync(0xffffffffu, k, 0);
+      if (k >= n) break;
       const long long seq = base + k;
       const int slot = (int)(seq % R);
       if (!s2_mbar_wait(full + slot, (uint32_t)((seq / R) & 1), sab)) {
@@ -454,7 +467,7 @@ __global__ void __launch_bounds__((NCONS + 1) * 32, 1)
         if (lane == 0) s_fold[warp] = f;
         __syncwarp();
         if (lane == 0) s2_mbar_arrive(empty + slot);
-        s2r_chunk<WMAX, NB, true>(u, v, X, pl, opts);
+        s2r_chunk<WMAX, NB>(u, W, v, X, padv, pl);
       } else {
         const long long off = s_off[slot];
         __syncwarp();
@@ -503,8 +516,8 @@ __global__ void k_s2_fill(const int32_t* __restrict__ item_ptr, const long long*
 
 __global__ void k_soa_to_aos4(const double* __restrict__ x, const double* __restrict__ y,
                               const double* __restrict__ z, int64_t V, double4* __restrict__ a) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
-    a[v] = make_double4(x[v], y[v], z[v], 0.0);
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= V; v += (int64_t)gridDim.x * blockDim.x)
+    a[v] = v < V ? make_double4(x[v], y[v], z[v], 0.0) : make_double4(-0.0, -0.0, -0.0, 0.0);
 }
 __global__ void k_aos4_to_soa(const double4* __restrict__ a, int64_t V, double* __restrict__ x, double* __restrict__ y,
                               double* __restrict__ z) {
@@ -516,12 +529,12 @@ __global__ void k_aos4_to_soa(const double4* __restrict__ a, int64_t V, double* 
   }
 }
 
-// dev knob LMS_S2P_OPTS (bit 0: L2 prefetch of the next pass's slab, 1: no L2
-// hints on the gathers, 2: grid barrier instead of neighbour waits, 3: timing
-// only -- no coordinate gathers (wrong results))
+// dev knob LMS_S2P_OPTS, timing experiments only (wrong results): bit 4 the
+// consumers only cycle the ring (no gathers, no stores), bit 5 no neighbour
+// waits
 static int s2p_opts() {
   const char* e = getenv("LMS_S2P_OPTS");
-  return e ? atoi(e) : 1;
+  return e ? atoi(e) : 0;
 }
 
 static int s2_blocks(lms_mesh_s* m) {
@@ -629,7 +642,7 @@ void run_s2(lms_mesh_s* m, int sweeps, cudaStream_t s) {
   }
   sync_soa(m, s);
   soa_changed(m);
-  DBuf<double> buf(4 * V, s);
+  DBuf<double> buf(4 * (V + 1), s);  // + the pad vertex X[V] = (-0, -0, -0, 0)
   double4* X = reinterpret_cast<double4*>(buf.p);
   const unsigned G = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
   k_soa_to_aos4<<<G, 256, 0, s>>>(m->x[0].p, m->x[1].p, m->x[2].p, V, X);
@@ -716,7 +729,7 @@ void run_s2(lms_mesh_s* m, int sweeps, cudaStream_t s) {
                                     (const int32_t*)S.s2_crange.p, G, C, npass, (const int32_t*)S.slab.p, X,
                                     s2p_opts(), st ? stats.p : (unsigned long long*)nullptr,
                                     (const int32_t*)S.s2_nbptr.p, (const int32_t*)S.s2_nb.p, S.s2_prog.p, m->err.p, R,
-                                    slot_ints));
+                                    slot_ints, (int32_t)V));
     note_launch(1);
     if (st) {
       std::vector<unsigned long long> h(4 * G);
