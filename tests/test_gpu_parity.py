@@ -329,6 +329,47 @@ def test_s2_persistent_and_pass_launches(persistent, monkeypatch):
             assert bits_equal(gpu_coords(gm), want), (kind, persistent, gm.schedule_info())
 
 
+def _kuhn_with_hub(n=12, seed=23):
+    """A Kuhn cube plus one free hub vertex below its z = 0 face, joined by a
+    tetrahedron to every triangle of that face (the face stays fixed): the
+    hub's row has n^2 entries, past the 16-wide staged rows of S2."""
+    k = meshgen.kuhn3d(n, 0.25, seed=seed)
+    el = np.asarray(k["elems"], dtype=np.int64)
+    tri = set()
+    for a, b, c in ((0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3)):
+        f = np.sort(el[:, [a, b, c]], axis=1)
+        for t in f[(f < n * n).all(axis=1)]:
+            tri.add(tuple(t))
+    tri = np.array(sorted(tri), dtype=np.int64)
+    hub = k.V
+    hub_el = np.concatenate([np.full((len(tri), 1), hub), tri], axis=1)
+    coords = [np.append(c, v) for c, v in zip(k["coords"], (0.5, 0.5, -0.3))]
+    fixed = np.append(np.asarray(k["fixed"], dtype=np.uint8), np.uint8(0))
+    return meshgen.Mesh(dim=3, coords=coords, elems=np.concatenate([el, hub_el]).astype(np.int32), fixed=fixed,
+                        name="kuhn_hub")
+
+
+@pytest.mark.parametrize("persistent", ["1", "0"])
+def test_s2_long_row(persistent, monkeypatch):
+    """S2 rows wider than the staged 16 (the hub's n^2 neighbours) take the
+    ordered one-neighbour-at-a-time path, in both launch forms; bit-exact
+    (Eq. 1, P:244-251)."""
+    monkeypatch.setenv("LMS_S2_PERSISTENT", persistent)
+    m = _kuhn_with_hub()
+    om = oracle.prepare(m)
+    assert int(np.diff(om["row_ptr"]).max()) > 16
+    for kind in ["original", "bfs"]:
+        perm = oracle.order(om, kind, 0)
+        pm = oracle.permute_mesh(om, perm)
+        want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 5)
+        with gpu_mesh(m, use_fixed=True) as gm:
+            gm.permute(cuda(perm))
+            gm.set_schedule("s2")
+            gm.smooth(2)
+            gm.smooth(3)
+            assert bits_equal(gpu_coords(gm), want), (kind, persistent)
+
+
 def test_C4_full_bench_config():
     """BASELINE.json configs[3] (the bench workload), original ordering, the
     launch configuration bench.py times (AUTO -> GZ), 3 sweeps bit-exact."""
