@@ -517,7 +517,15 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   // GZ (gz.cu): the default for 2D meshes with few colours, where the
   // C-hop ghost zone of a tile is a small fraction of it
   if (m->sched_req == LMS_SCHED_GZ || (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->C <= 8)) {
-    const int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 4096 : 512);
+    int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 4096 : 512);
+    // few tiles per SM (under 2 at T = 4096): larger tiles, up to one per SM
+    // (C2 1024^2: 26.3 -> 24.6 us per sweep; the builder still shrinks T
+    // until two region buffers fit)
+    if (m->tile_req == 0 && m->dim == 2) {
+      int nsm = 148;
+      LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+      if (m->V / 4096 < 2 * (int64_t)nsm) Tg = (int)std::max<int64_t>(4096, std::min<int64_t>(8192, m->V / nsm));
+    }
     const int P = (m->sched_req == LMS_SCHED_GZ && m->lag_req > 0) ? m->lag_req : 1;
     if (build_gz(m, Tg, P, m->sched_req == LMS_SCHED_GZ, s)) {
       S.kind = LMS_SCHED_GZ;
