@@ -199,6 +199,39 @@ def order_rdr(row_ptr, col, fixed, q, stats: bool = False):
     return perm
 
 
+def order_rdr_windowed(row_ptr, col, fixed, q, L: int):
+    """windowed RDR, a parallel approximation of Alg. 2
+     -- NOT the paper's ordering unless L >= V.  The current
+    labels are cut into windows [w L, (w + 1) L); Alg. 2 (order_rdr, readings
+    Z9-Z12) runs on each window's induced subgraph (edges leaving the window
+    dropped, rows keep CSR order), and window w's order fills output positions
+    [w L, ...) in window order.  Definition of this repo (DESIGN.md reading
+    Z28); pinned by: L >= V equals order_rdr, L = 1 is the identity, each
+    window's block holds exactly its own labels, and per window the result is
+    order_rdr of the explicitly built induced submesh."""
+    row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    fixed = np.ascontiguousarray(fixed, dtype=np.uint8)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    V = row_ptr.shape[0] - 1
+    L = int(L)
+    if L < 1:
+        raise ValueError("window length must be >= 1")
+    perm = np.empty(V, dtype=np.int32)
+    for w0 in range(0, V, L):
+        w1 = min(V, w0 + L)
+        seg = col[row_ptr[w0]:row_ptr[w1]]
+        keep = (seg >= w0) & (seg < w1)
+        lens = np.diff(row_ptr[w0:w1 + 1])
+        row_of = np.repeat(np.arange(w1 - w0), lens)
+        cnt = np.bincount(row_of[keep], minlength=w1 - w0)
+        sub_rp = np.zeros(w1 - w0 + 1, dtype=np.int64)
+        np.cumsum(cnt, out=sub_rp[1:])
+        sub_col = (seg[keep] - w0).astype(np.int32)
+        perm[w0:w1] = order_rdr(sub_rp, sub_col, fixed[w0:w1], q[w0:w1]) + w0
+    return perm
+
+
 # --------------------------------------------------------------------------- O6
 def inverse_perm(perm) -> np.ndarray:
     perm = np.ascontiguousarray(perm, dtype=np.int32)
@@ -325,6 +358,11 @@ def order(mesh: dict, kind: str, seed: int = 0) -> np.ndarray:
         if q is None:
             q = quality(mesh["coords"], mesh["elems"])
         return order_rdr(mesh["row_ptr"], mesh["col"], mesh["fixed"], q)
+    if kind == "rdrw":  # seed = window length (0: the library default, 65536)
+        q = mesh.get("q")
+        if q is None:
+            q = quality(mesh["coords"], mesh["elems"])
+        return order_rdr_windowed(mesh["row_ptr"], mesh["col"], mesh["fixed"], q, seed if seed > 0 else 65536)
     if kind == "rbfs":
         return order_rbfs(mesh["row_ptr"], mesh["col"], seed)
     if kind == "dfs":
