@@ -61,9 +61,14 @@ typedef enum {
     LMS_ORDER_RBFS = 4,     /* reverse BFS: the BFS order reversed; `seed` = BFS seed */
     LMS_ORDER_RCM = 5,      /* reverse Cuthill-McKee: queue BFS from the vertex of smallest (degree, label),
                                children by (degree, label), restarts likewise; reversed (reading Z26) */
-    LMS_ORDER_DFS = 6       /* depth-first preorder (Fig. 2a): smallest unvisited neighbour
+    LMS_ORDER_DFS = 6,      /* depth-first preorder (Fig. 2a): smallest unvisited neighbour
                                first, restart at the smallest unvisited label (reading Z25); one warp,
                                sequential; `seed` = start vertex */
+    LMS_ORDER_RDR_WINDOWED = 7 /* APPROXIMATION of RDR (reading Z28): the labels cut into
+                               windows [wL, (w+1)L), L = `seed` (0: 65536); Alg. 2 on each window's induced
+                               subgraph (edges leaving it dropped), window w's order in perm[wL, ...);
+                               the windows walk in parallel, one warp each.  L >= V is RDR itself.
+                               LMS_E_ARG if L > INT32_MAX or the maximum degree exceeds 32 */
 } lms_order_kind;
 
 typedef enum {

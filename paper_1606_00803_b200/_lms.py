@@ -14,7 +14,7 @@ from . import build_lib
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
-ORDERINGS = {"original": 0, "random": 1, "bfs": 2, "rdr": 3, "rbfs": 4, "rcm": 5, "dfs": 6}
+ORDERINGS = {"original": 0, "random": 1, "bfs": 2, "rdr": 3, "rbfs": 4, "rcm": 5, "dfs": 6, "rdrw": 7}
 SCHEDULES = {"auto": 0, "s1": 1, "s2": 2, "s3": 3, "gz": 4, "jacobi": 5}
 STOP_REASONS = {1: "goal", 2: "converged", 3: "max_sweeps"}
 SCHED_NAMES = {v: k for k, v in SCHEDULES.items()}

@@ -362,6 +362,10 @@ lms_status lms_order(lms_mesh_t m, lms_order_kind kind, uint64_t seed, int32_t* 
     case LMS_ORDER_RDR:
       order_rdr(m, d_perm, s);
       break;
+    case LMS_ORDER_RDR_WINDOWED:
+      if ((int64_t)seed < 0 || seed > (uint64_t)INT32_MAX) fail(LMS_E_ARG, "window length out of range");
+      order_rdr(m, d_perm, s, seed == 0 ? 65536 : (int64_t)seed);
+      break;
     default:
       fail(LMS_E_ARG, "unknown ordering kind");
   }

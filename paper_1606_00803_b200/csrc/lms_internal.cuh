@@ -254,7 +254,7 @@ void order_random(lms_mesh_s* m, uint64_t seed, int32_t* d_perm, cudaStream_t s)
 void order_bfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s);
 void order_rbfs(lms_mesh_s* m, int64_t seed, bool rcm, int32_t* d_perm, cudaStream_t s);
 void order_dfs(lms_mesh_s* m, int64_t seed, int32_t* d_perm, cudaStream_t s);
-void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s);
+void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s, int64_t L = 0);
 void permute_mesh(lms_mesh_s* m, const int32_t* d_perm, cudaStream_t s);
 void build_schedule(lms_mesh_s* m, cudaStream_t s);
 int64_t spatial_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s);

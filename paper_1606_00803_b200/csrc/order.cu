@@ -17,6 +17,7 @@
 //                   to l[0] (readings Z9-Z12).  Never-sorted vertices are
 //                   appended in ascending label.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 
@@ -709,6 +710,105 @@ __global__ void k_rdr_walk_ell(const int32_t* __restrict__ ell, const int32_t* _
   if (lane == 0) { stats[0] = next; stats[1] = walks; }
 }
 
+// Windowed RDR (DESIGN reading Z28): window w = labels
+// [w L, (w + 1) L) walks Alg. 2 on its induced subgraph -- every neighbour
+// outside the window is dropped from the rows -- and fills perm[w L, ...).
+// One warp per window, the walk of k_rdr_walk_ell; the windows run in
+// parallel (each only reads and writes its own vertices' states).  outer_w:
+// the free vertices by (window, quality, label); wofs: per window offsets.
+template <int WM>
+__global__ void k_rdr_walk_win(const int32_t* __restrict__ ell, const int32_t* __restrict__ outer_w,
+                               const int64_t* __restrict__ wofs, int64_t V, int64_t L, int64_t W, uint8_t* st,
+                               int32_t* perm, int* err) {
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < W;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t lo = w * L, hi = lo + L < V ? lo + L : V;
+    long long next = lo;
+    int64_t oi = wofs[w];
+    const int64_t oe = wofs[w + 1];
+    while (oi < oe) {
+      const int64_t idx = oi + lane;
+      const int32_t i_l = idx < oe ? __ldg(outer_w + idx) : -1;
+      const int p_l = i_l >= 0 ? st[i_l] : 2;
+      const unsigned bal = __ballot_sync(FULL, p_l < 2);
+      if (bal == 0) { oi += 32; continue; }
+      const int first = __ffs(bal) - 1;
+      const int32_t i = __shfl_sync(FULL, i_l, first);
+      const int si = __shfl_sync(FULL, p_l, first);
+      oi += first + 1;
+      if (lane == 0) {
+        if (si == 0) perm[next] = i;
+        st[i] = 2;
+      }
+      next += si == 0 ? 1 : 0;
+      int32_t u = lane < WM ? __ldg(ell + (int64_t)i * WM + lane) : -1;
+      if (u < lo || u >= hi) u = -1;
+      __syncwarp();
+      for (;;) {
+        int su = 2;
+        int32_t row[WM];
+        if (u >= 0) {
+          su = st[u];
+          const int4* rp4 = reinterpret_cast<const int4*>(ell + (int64_t)u * WM);
+#pragma unroll
+          for (int q = 0; q < WM / 4; ++q) {
+            const int4 t = __ldg(rp4 + q);
+            row[4 * q] = t.x;
+            row[4 * q + 1] = t.y;
+            row[4 * q + 2] = t.z;
+            row[4 * q + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < WM; ++q) row[q] = -1;
+        }
+        const unsigned unp = __ballot_sync(FULL, su < 2);
+        const unsigned app = __ballot_sync(FULL, su == 0);
+        if (su == 0) {
+          perm[next + __popc(app & lt)] = u;
+          st[u] = 1;
+        }
+        next += __popc(app);
+        if (unp == 0) break;
+        const int src = __ffs(unp) - 1;
+        const int32_t l0 = __shfl_sync(FULL, u, src);
+        int32_t un = -1;
+#pragma unroll
+        for (int q = 0; q < WM; ++q) {
+          const int32_t t = __shfl_sync(FULL, row[q], src);
+          if (lane == q) un = t;
+        }
+        if (un < lo || un >= hi) un = -1;  // the row restricted to the window
+        __syncwarp();
+        if (lane == 0) st[l0] = 2;
+        __syncwarp();
+        u = un;
+      }
+      __syncwarp();
+    }
+    // the window's never-sorted vertices, ascending label (reading Z12)
+    for (int64_t b = lo; b < hi; b += 32) {
+      const int64_t v = b + lane;
+      const bool f = v < hi && st[v] == 0;
+      const unsigned fb = __ballot_sync(FULL, f);
+      if (f) perm[next + __popc(fb & lt)] = (int32_t)v;
+      next += __popc(fb);
+    }
+    if (lane == 0 && next != hi) raise_err(err, LMS_E_PERM);
+  }
+}
+__global__ void k_window_keys(const int32_t* __restrict__ outer, int64_t n, int64_t L, uint32_t* key,
+                              unsigned long long* cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = (uint32_t)(outer[i] / L);
+    key[i] = w;
+    atomicAdd(cnt + w, 1ull);
+  }
+}
+
 __global__ void k_fill_ell(const int32_t* __restrict__ rp, const int32_t* __restrict__ scol, int64_t V, int WM,
                            int32_t* __restrict__ ell) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < V * WM; t += (int64_t)gridDim.x * blockDim.x) {
@@ -726,8 +826,9 @@ __global__ void k_state_unsorted(const uint8_t* __restrict__ st, int64_t V, uint
   }
 }
 
-void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s) {
+void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s, int64_t L) {
   const int64_t V = m->V, nnz = m->nnz;
+  if (L >= V) L = 0;  // one window: Alg. 2 itself
   const double* q = initial_quality(m, s);
   const unsigned Gv = grid_for(V, 256) > 8192 ? 8192 : grid_for(V, 256);
   // rows presorted by (q, label): stable segmented sort of (q bits, col) pairs
@@ -765,6 +866,61 @@ void order_rdr(lms_mesh_s* m, int32_t* d_perm, cudaStream_t s) {
   }
   DBuf<uint8_t> state(V, s);
   LMS_TRY_CUDA(cudaMemsetAsync(state.p, 0, V, s));
+  if (L > 0) {  // windowed (reading Z28): every window walks in parallel over an ELL copy
+    int md = 0;
+    {
+      DBuf<int> dmd(1, s);
+      LMS_TRY_CUDA(cudaMemsetAsync(dmd.p, 0, sizeof(int), s));
+      k_max_degree<<<Gv, 256, 0, s>>>(m->row_ptr.p, V, dmd.p);
+      LMS_CHECK_LAUNCH();
+      LMS_TRY_CUDA(cudaMemcpyAsync(&md, dmd.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    }
+    const int WM = md <= 8 ? 8 : md <= 16 ? 16 : md <= 32 ? 32 : 0;
+    if (WM == 0) fail(LMS_E_ARG, "windowed RDR: maximum degree above 32");
+    const int64_t W = (V + L - 1) / L;
+    DBuf<int32_t> ell(V * WM, s);
+    const unsigned Ge = grid_for(V * WM, 256) > 8192 ? 8192 : grid_for(V * WM, 256);
+    k_fill_ell<<<Ge, 256, 0, s>>>(m->row_ptr.p, scol.p, V, WM, ell.p);
+    LMS_CHECK_LAUNCH();
+    scol.release();
+    // outer list by (window, q, label): a stable sort of the (q, label)-sorted
+    // list on the window index, and per-window offsets
+    DBuf<uint32_t> wk(n_outer > 0 ? n_outer : 1, s), wk2(n_outer > 0 ? n_outer : 1, s);
+    DBuf<int32_t> outer_w(n_outer > 0 ? n_outer : 1, s);
+    DBuf<unsigned long long> cnt(W + 1, s);
+    DBuf<int64_t> wofs(W + 1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(cnt.p, 0, (W + 1) * sizeof(unsigned long long), s));
+    if (n_outer > 0) {
+      const unsigned Go = grid_for(n_outer, 256) > 8192 ? 8192 : grid_for(n_outer, 256);
+      k_window_keys<<<Go, 256, 0, s>>>(outer.p, n_outer, L, wk.p, cnt.p);
+      LMS_CHECK_LAUNCH();
+      int wb = 1;
+      while (((int64_t)1 << wb) < W) ++wb;
+      size_t tb = 0;
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, wk.p, wk2.p, outer.p, outer_w.p, n_outer, 0, wb, s));
+      DBuf<char> tmp(tb, s);
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, wk.p, wk2.p, outer.p, outer_w.p, n_outer, 0, wb, s));
+    }
+    {
+      size_t tb = 0;
+      LMS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, wofs.p, W + 1, s));
+      DBuf<char> tmp(tb, s);
+      LMS_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, wofs.p, W + 1, s));
+    }
+    DBuf<uint8_t> state(V, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(state.p, 0, V, s));
+    const unsigned Gw = (unsigned)std::min<int64_t>((W + 7) / 8, 148 * 16);
+    if (WM == 8)
+      k_rdr_walk_win<8><<<Gw, 256, 0, s>>>(ell.p, outer_w.p, wofs.p, V, L, W, state.p, d_perm, m->err.p);
+    else if (WM == 16)
+      k_rdr_walk_win<16><<<Gw, 256, 0, s>>>(ell.p, outer_w.p, wofs.p, V, L, W, state.p, d_perm, m->err.p);
+    else
+      k_rdr_walk_win<32><<<Gw, 256, 0, s>>>(ell.p, outer_w.p, wofs.p, V, L, W, state.p, d_perm, m->err.p);
+    LMS_CHECK_LAUNCH();
+    check_err_flag(m, s, "windowed RDR (a window did not order each of its vertices once)");  // synchronises s
+    return;
+  }
   DBuf<long long> stats(2, s);
   // the ELL walk for maximum degree <= 16 (LMS_RDR_ELL=0: the CSR walk)
   int md = 0;

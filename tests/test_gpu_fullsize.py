@@ -41,7 +41,7 @@ def c4():
     return m, oracle.prepare(m)
 
 
-@pytest.mark.parametrize("kind", ["bfs", "rdr", "random"])
+@pytest.mark.parametrize("kind", ["bfs", "rdr", "random", "rdrw"])
 def test_C4_full_orderings_bit_exact(c4, kind):
     m, om = c4
     seed = meshgen.RANDOM_ORDER_SEED if kind == "random" else 0
@@ -165,3 +165,21 @@ def test_rdr_walk_forms(ell, monkeypatch):
         with gpu_mesh(m) as gm:
             assert np.array_equal(np_(gm.order("rdr")),
                                   oracle.order_rdr(om["row_ptr"], om["col"], om["fixed"], q)), (ell, m.V)
+
+
+@pytest.mark.parametrize("L", [1, 7, 64, 1000, 0])
+def test_rdr_windowed(L):
+    """Windowed RDR (reading Z28): one warp per window of L
+    labels walking Alg. 2 on the window's induced subgraph; bit-exact against
+    the oracle on a 2D grid, a 3D Kuhn mesh and a disconnected mesh with
+    interleaved labels (L = 0: the default 65536 >= V, i.e. Alg. 2 itself)."""
+    for m in (meshgen.grid2d(61, 47, 0.3, seed=71), meshgen.kuhn3d(13, 0.25, seed=72), DISCONNECTED[1][1]()):
+        om = oracle.prepare(m)
+        om["fixed"] = oracle.boundary(m.V, m["elems"]) if m["dim"] == 2 else om["fixed"]
+        q = oracle.quality(m["coords"], m["elems"])
+        want = oracle.order_rdr_windowed(om["row_ptr"], om["col"], om["fixed"], q, L if L > 0 else 65536)
+        with gpu_mesh(m) as gm:
+            assert np.array_equal(np_(gm.order("rdrw", L)), want), (L, m.V)
+    if L == 0:
+        assert np.array_equal(want, oracle.order_rdr(om["row_ptr"], om["col"], om["fixed"], q))
+

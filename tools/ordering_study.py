@@ -20,7 +20,7 @@ import paper_1606_00803_b200 as lms  # noqa: E402
 
 p = argparse.ArgumentParser()
 p.add_argument("--config", default="C4")
-p.add_argument("--orderings", default="original,random,bfs,rbfs,rcm,rdr")
+p.add_argument("--orderings", default="original,random,bfs,rbfs,rcm,rdr,rdrw")
 p.add_argument("--sweeps", type=int, default=20)
 p.add_argument("--reps", type=int, default=3)
 a = p.parse_args()
