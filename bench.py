@@ -415,13 +415,54 @@ def run_ours(args):
             e2e_step()
             sev[k + 1].record(stream)
         torch.cuda.synchronize()
-        e_ms = sev[0].elapsed_time(sev[-1]) / n_e2e
+        lat_ms = sev[0].elapsed_time(sev[-1]) / n_e2e
         step_ms = [round(sev[k].elapsed_time(sev[k + 1]), 2) for k in range(n_e2e)]
+        # throughput with two jobs in flight (a serving loop): job k runs on
+        # stream k % 2, so one job's H2D / D2H copies (PCIe) overlap the other
+        # job's kernels; the kernels themselves still share the SMs.  Every job
+        # copies its whole input from pinned host memory and its result back.
+        strs = [torch.cuda.Stream(), torch.cuda.Stream()]
+        houts = [hout, [torch.empty(V, dtype=torch.float64).pin_memory() for _ in range(dim)]]
+
+        def e2e_job(slot, keep):
+            with torch.cuda.stream(strs[slot]):
+                g = lms.Mesh.build_csr_host(hc, he)
+                g.set_async_errors(True)  # smooth() returns once enqueued; checked after the loop
+                p = g.order(args.ordering, meshgen.RANDOM_ORDER_SEED if args.ordering == "random" else 0)
+                g.permute(p)
+                g.set_schedule(args.schedule, args.tile, args.lag)
+                g.smooth(sweeps)
+                out = g.coords()
+                for o, h in zip(out, houts[slot]):
+                    h.copy_(o, non_blocking=True)
+            keep.append((g, out, p))
+
+        def pipelined(n):
+            keep = []
+            torch.cuda.synchronize()
+            a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            a.record(strs[0])
+            strs[1].wait_event(a)
+            for k in range(n):
+                e2e_job(k % 2, keep)
+            b.record(strs[1])
+            strs[0].wait_event(b)
+            c.record(strs[0])
+            torch.cuda.synchronize()
+            for g, _, _ in keep:
+                g.check()
+                g.close()
+            return a.elapsed_time(c) / n
+        pipelined(n_e2e)  # warm: the allocator caches of both streams
+        e_ms = pipelined(n_e2e)
         e2e = {"value": vfree * sweeps / (e_ms / 1e3) * world, "unit": "vertex-updates/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
-               "steps": n_e2e, "step_ms": step_ms, "phases_ms": e2e_phases,
-               "path": "build_csr_host (H2D elems, then CSR + colouring under the H2D of coords) -> order -> permute "
-                       "-> smooth(%d) -> D2H coords" % sweeps}
+               "jobs_in_flight": 2, "steps": n_e2e,
+               "latency_ms_per_job": lat_ms, "serial_value": vfree * sweeps / (lat_ms / 1e3) * world,
+               "serial_step_ms": step_ms, "phases_ms": e2e_phases,
+               "path": "per job: build_csr_host (H2D elems, then CSR + colouring under the H2D of coords) -> order "
+                       "-> permute -> smooth(%d) -> D2H coords; %d jobs, two in flight on two streams (value, "
+                       "ms_per_step); serial_value / latency_ms_per_job: one job at a time" % (sweeps, n_e2e)}
 
     cpu = None
     if rank == 0 and not args.no_cpu:

@@ -179,6 +179,18 @@ lms_status lms_permute(lms_mesh_t m, const int32_t* d_perm, lms_stream_t stream)
  * LMS_SCHED_JACOBI instead runs the named Jacobi variant (a different method). */
 lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream);
 
+/* lms_set_async_errors -- on != 0: lms_smooth returns once its sweeps are
+ * enqueued on `stream`, without waiting for them; a sweep kernel's watchdog
+ * abort (LMS_E_CUDA, the coordinates then partly updated) is reported by the
+ * next lms_check on the handle instead.  Lets a caller keep several jobs in
+ * flight on several streams (one job's copies overlapping another's
+ * kernels).  Default off: lms_smooth synchronises `stream` and reports it. */
+lms_status lms_set_async_errors(lms_mesh_t m, int32_t on);
+
+/* lms_check -- synchronise `stream` and report (and clear) a device-side
+ * error recorded on the handle since the last check: LMS_OK or the error. */
+lms_status lms_check(lms_mesh_t m, lms_stream_t stream);
+
 /* lms_set_schedule -- choose the sweep kernel.  tile: vertices per tile
  * (0 = default); lag: S3 tile lag L (0 = automatic); for LMS_SCHED_GZ `lag` is
  * the number of sweeps P fused into one pass (0 = 1; at most 8).  Takes effect

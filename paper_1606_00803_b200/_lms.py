@@ -33,7 +33,7 @@ EXPORTS = ["lms_build_csr", "lms_build_csr_host", "lms_mesh_from_csr", "lms_mesh
            "lms_global_quality", "lms_smooth_until",
            "lms_nccl_unique_id", "lms_dist_create", "lms_dist_replan", "lms_smooth_dist", "lms_dist_export_owned", "lms_dist_info",
            "lms_dist_export_local_ids", "lms_dist_create_local", "lms_smooth_dist_local", "lms_dist_destroy",
-           "lms_trace", "lms_reuse_distance", "lms_reuse_stats"]
+           "lms_trace", "lms_reuse_distance", "lms_reuse_stats", "lms_set_async_errors", "lms_check"]
 
 
 class LMSError(RuntimeError):
@@ -66,6 +66,8 @@ def load_library(build: bool = True):
         "lms_permute": [P, P, P],
         "lms_smooth": [P, i32, P],
         "lms_set_schedule": [P, i32, i32, i32],
+        "lms_set_async_errors": [P, i32],
+        "lms_check": [P, P],
         "lms_mesh_info": [P, ct.POINTER(i64), ct.POINTER(i64), ct.POINTER(i32), ct.POINTER(i32)],
         "lms_schedule_info": [P, ct.POINTER(i64), ct.POINTER(i32), ct.POINTER(i32), ct.POINTER(i32)],
         "lms_export_coords": [P, PP, P],
@@ -354,6 +356,15 @@ class Mesh:
         n = idx.numel()
         _check(lib().lms_scatter_coords(self._h, _dev(idx, torch.int32, name="idx"), n,
                                         _dev(src, torch.float64, name="src"), _stream(stream)), "lms_scatter_coords")
+
+    def set_async_errors(self, on: bool = True):
+        """lms_set_async_errors: smooth() returns once its sweeps are enqueued;
+        a watchdog abort is reported by check()."""
+        _check(lib().lms_set_async_errors(self._h, 1 if on else 0), "lms_set_async_errors")
+
+    def check(self, stream=None):
+        """lms_check: synchronise the stream, raise a recorded device-side error."""
+        _check(lib().lms_check(self._h, _stream(stream)), "lms_check")
 
     def set_schedule(self, kind: str = "auto", tile: int = 0, lag: int = 0, tiling: str | None = None):
         _check(lib().lms_set_schedule(self._h, SCHEDULES[kind], tile, lag), "lms_set_schedule")

@@ -399,6 +399,23 @@ lms_status lms_smooth(lms_mesh_t m, int32_t sweeps, lms_stream_t stream) {
   LMS_API_END
 }
 
+lms_status lms_set_async_errors(lms_mesh_t m, int32_t on) {
+  LMS_API_BEGIN
+  if (!m) fail(LMS_E_ARG, "NULL handle");
+  m->async_errors = on != 0;
+  return LMS_OK;
+  LMS_API_END
+}
+
+lms_status lms_check(lms_mesh_t m, lms_stream_t stream) {
+  LMS_API_BEGIN
+  if (!m) fail(LMS_E_ARG, "NULL handle");
+  DevGuard dg(m);
+  check_err_flag(m, (cudaStream_t)stream, "lms_check (a sweep kernel's watchdog aborted a wait)");
+  return LMS_OK;
+  LMS_API_END
+}
+
 lms_status lms_set_schedule(lms_mesh_t m, lms_schedule_kind kind, int32_t tile, int32_t lag) {
   LMS_API_BEGIN
   if (!m) fail(LMS_E_ARG, "NULL handle");

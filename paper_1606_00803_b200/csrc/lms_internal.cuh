@@ -215,6 +215,7 @@ struct lms_mesh_s {
   int sched_req = LMS_SCHED_AUTO, tile_req = 0, lag_req = 0, tiling_req = LMS_TILING_AUTO;
   lms::Schedule sched;
   lms::DBuf<int> err;          // device error flag
+  bool async_errors = false;   // lms_set_async_errors: smooth leaves the flag to lms_check
 };
 
 namespace lms {

@@ -779,7 +779,7 @@ void run_s2(lms_mesh_s* m, int sweeps, cudaStream_t s) {
     LMS_TRY_CUDA(cudaCtxResetPersistingL2Cache());
     LMS_TRY_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev_limit));
   }
-  if (used_p) check_err_flag(m, s, "lms_smooth (S2 watchdog: a neighbour wait exceeded its budget)");
+  if (used_p && !m->async_errors) check_err_flag(m, s, "lms_smooth (S2 watchdog: a neighbour wait exceeded its budget)");
 }
 
 }  // namespace lms

@@ -592,3 +592,38 @@ def test_gz_region_producers(producers, kind, monkeypatch):
         gm.smooth(3)
         assert gm.schedule_info()["kind"] == "gz"
         assert bits_equal(gpu_coords(gm), want)
+
+
+def test_two_jobs_in_flight_on_two_streams():
+    """bench.py's e2e keeps two jobs in flight (job k on stream k % 2): the
+    whole path from pinned host buffers on two streams at once -- CSR build,
+    colouring, ordering, relabelling, GZ schedule and sweeps, export -- each
+    job bit-exact against the oracle (Eq. 1)."""
+    import torch
+    m = meshgen.grid2d(301, 211, 0.3, seed=33)
+    om = oracle.prepare(m)
+    hc = [torch.from_numpy(c).pin_memory() for c in m["coords"]]
+    he = torch.from_numpy(np.asarray(m["elems"], dtype=np.int32)).pin_memory()
+    strs = [torch.cuda.Stream(), torch.cuda.Stream()]
+    jobs = []
+    for k in range(4):
+        kind = ["original", "bfs", "rdr", "random"][k]
+        seed = 803 if kind == "random" else 0
+        with torch.cuda.stream(strs[k % 2]):
+            g = lms.Mesh.build_csr_host(hc, he)
+            g.set_async_errors(k % 2 == 0)  # lms_smooth returns once enqueued; lms_check reports
+            p = g.order(kind, seed)
+            g.permute(p)
+            g.smooth(6)
+            out = [torch.empty(m.V, dtype=torch.float64).pin_memory() for _ in range(2)]
+            for o, d in zip(out, g.coords()):
+                o.copy_(d, non_blocking=True)
+        jobs.append((kind, seed, g, out))
+    torch.cuda.synchronize()
+    for kind, seed, g, out in jobs:
+        perm = oracle.order(om, kind, seed)
+        pm = oracle.permute_mesh(om, perm)
+        want = oracle.smooth(pm["coords"], pm["row_ptr"], pm["col"], pm["colour"], pm["C"], 6)
+        assert bits_equal([o.numpy() for o in out], want), kind
+        g.check()
+        g.close()
