@@ -488,6 +488,11 @@ static void exchange_nccl(lms_dist_s* d, cudaStream_t s) {
   unpack_all(d, s);
 }
 
+// One pass on the rank's local mesh, without waiting for it: the sweep
+// kernels' watchdog flag is read once per lms_smooth_dist call (end_passes),
+// so the host enqueues the next exchange and pass while this one runs
+// instead of paying a stream synchronisation (and the NCCL / pack launch
+// latencies behind it) every pass.
 static void local_pass(lms_dist_s* d, int p, cudaStream_t s) {
   lms_mesh_s* m = d->local;
   if (!m || m->n_free == 0) return;
@@ -496,7 +501,20 @@ static void local_pass(lms_dist_s* d, int p, cudaStream_t s) {
     build_schedule(m, s);
   }
   m->coords_moved = true;
-  run_sweeps(m, p, s);
+  const bool was = m->async_errors;
+  m->async_errors = true;
+  try {
+    run_sweeps(m, p, s);
+  } catch (...) {
+    m->async_errors = was;
+    throw;
+  }
+  m->async_errors = was;
+}
+static void end_passes(lms_dist_s* d, cudaStream_t s) {
+  lms_mesh_s* m = d->local;
+  if (m && m->n_free > 0 && !m->async_errors)
+    check_err_flag(m, s, "lms_smooth_dist (sweep watchdog: a wait exceeded its budget)");
 }
 
 }  // namespace lms
@@ -621,6 +639,7 @@ lms_status lms_smooth_dist(lms_dist_t d, int32_t sweeps, lms_stream_t stream) {
       local_pass(d, p, s);
       left -= p;
     }
+    if (sweeps > 0) end_passes(d, s);
     return LMS_OK;
   } catch (const Err& e) {
     set_error(e.msg);
@@ -656,6 +675,8 @@ lms_status lms_smooth_dist_local(lms_dist_t* ds, int32_t nranks, int32_t sweeps,
       for (int r = 0; r < nranks; ++r) local_pass(ds[r], p, s);
       left -= p;
     }
+    if (sweeps > 0)
+      for (int r = 0; r < nranks; ++r) end_passes(ds[r], s);
     return LMS_OK;
   } catch (const Err& e) {
     set_error(e.msg);
