@@ -345,7 +345,7 @@ __global__ void __launch_bounds__((NCONS + 1) * 32, 1)
   long long* s_off = reinterpret_cast<long long*>(empty + R);
   int32_t* s_w = reinterpret_cast<int32_t*>(s_off + R);
   __shared__ int s_abort;
-  __shared__ int s_fold[NCONS];
+  __shared__ int s_fold[NCONS * 32];
   __shared__ int s_claim;
   const uint64_t pf = s2_policy_first(), pl = s2_policy_last();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -459,12 +459,13 @@ __global__ void __launch_bounds__((NCONS + 1) * 32, 1)
 #pragma unroll
         for (int q = 0; q < WMAX; ++q) u[q] = q < W ? sl[32 * (1 + q) + lane] : -1;
         // the slot's shared-memory reads must have returned before the
-        // release lets the producer's TMA overwrite it: fold them into one
-        // store (it cannot issue before the loads complete)
+        // release lets the producer's TMA (async proxy) overwrite it: every
+        // lane folds its reads into one store (it cannot issue before they
+        // complete), and __syncwarp orders the stores before lane 0's arrive
         int f = v;
 #pragma unroll
         for (int q = 0; q < WMAX; ++q) f ^= u[q];
-        if (lane == 0) s_fold[warp] = f;
+        reinterpret_cast<volatile int*>(s_fold)[warp * 32 + lane] = f;
         __syncwarp();
         if (lane == 0) s2_mbar_arrive(empty + slot);
         s2r_chunk<WMAX, NB>(u, W, v, X, padv, pl);
