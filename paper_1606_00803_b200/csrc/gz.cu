@@ -98,6 +98,14 @@ __host__ __device__ inline int gz_hdr_words(int C, int P) { return (int)r4(4 + P
 // record bytes for rows of R and U positions: rows (u16), pb (u32: slot,
 // owned, dependency, degree), vertex ids (u32), descriptor (16 B)
 __host__ __device__ inline int gz_rec16(int R, int U) { return (2 * U * R + 8 * U + 16) / 16; }
+// 8-bit rows (2D, 64-update items, every tile's rows of R = 8): the same
+// record with each neighbour slot as ONE byte, b < 248: slot = own + b - 124
+// (own = the position's vertex slot, pb & 0x7fff), b >= 248: pad slot
+// padbase + b - 248 -- used when every slot of every record fits (C4 under
+// the original ordering: the region's rows are ~80 slots apart), else the
+// 16-bit rows.  1,552 -> 1,040 bytes per record.
+constexpr int GZ_ROW8_PAD = 248, GZ_ROW8_BIAS = 124;
+__host__ __device__ inline int gz_rec16_row8(int U) { return (8 * U + 8 * U + 16) / 16; }
 
 
 // ---------------------------------------------------------------- build kernels
@@ -1142,7 +1150,15 @@ __device__ __forceinline__ void gz_update(const GzRec<RMAX>& r, int R, const uin
 // per warp, two independent FP64 add chains per axis).  Every gather is
 // unpredicated: padding reads the pad slot's (-0.0, -0.0), the exact identity
 // of IEEE addition; the degrees come from the record (da, db; 0 = count).
-template <int RMAX>
+// one record row of 8-bit codes -> slots (see gz_rec16_row8)
+__device__ __forceinline__ void unpack8_row8(const uint4 q, uint32_t own, uint32_t padv, uint16_t* u) {
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const uint32_t b = ((w < 4 ? q.x : q.y) >> (8 * (w & 3))) & 0xffu;
+    u[w] = (uint16_t)(b >= GZ_ROW8_PAD ? padv + (b - GZ_ROW8_PAD) : own + b - GZ_ROW8_BIAS);
+  }
+}
+template <int RMAX, bool ROW8 = false>
 __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, int da, const GzRec<RMAX>& rb, bool vb,
                                            int db, int R, const uint4* __restrict__ rowgA,
                                            const uint4* __restrict__ rowgB, double* sc, const double* rcp,
@@ -1152,10 +1168,15 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, int d
   // RN(1/d) from the table before the gathers: off the critical path
   double rra = rcp[da <= GZ_RCP_MAX ? da : 0], rrb = rcp[db <= GZ_RCP_MAX ? db : 0];
   uint16_t ua[RMAX], ub[RMAX];
+  if (ROW8) {
+    unpack8_row8(ra.row[0], ra.pb & 0x7fffu, padv, ua);
+    unpack8_row8(rb.row[0], rb.pb & 0x7fffu, padv, ub);
+  } else {
 #pragma unroll
-  for (int p = 0; p < RMAX / 8; ++p) {
-    unpack8(ra.row[p], ua + 8 * p);
-    unpack8(rb.row[p], ub + 8 * p);
+    for (int p = 0; p < RMAX / 8; ++p) {
+      unpack8(ra.row[p], ua + 8 * p);
+      unpack8(rb.row[p], ub + 8 * p);
+    }
   }
   double2 ga[RMAX], gb[RMAX];
 #pragma unroll
@@ -1235,7 +1256,7 @@ __device__ __forceinline__ void gz_update2(const GzRec<RMAX>& ra, bool va, int d
 // copies of id runs, or 16-byte cp.async gathers), warp 1 streams item
 // records into the record ring (one TMA bulk copy per record, in claim
 // order), warps 2.. are workers (one claimed item at a time).
-template <int DIM, int RMAX, int UPL, bool STATS>
+template <int DIM, int RMAX, int UPL, bool STATS, bool ROW8 = false>
 // register budget per thread for the CTA's threads (2D 64-update items: 24
 // warps x 80; 32-update items: 24 x 80; 3D: 12 x 152)
 __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep_gz(const int32_t* __restrict__ tiles, int ntiles,
@@ -1542,14 +1563,20 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     }
     if (!__shfl_sync(FULL, alive, 0)) return;
     GzRec<RMAX> r[UPL];
-    const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rbase + 2 * U * R);
-    const uint4 desc = *reinterpret_cast<const uint4*>(rbase + 2 * U * R + 8 * U);
+    const int rows_bytes = ROW8 ? 8 * U : 2 * U * R;  // 8-bit rows: R = 8 bytes per position
+    const uint32_t* pbs = reinterpret_cast<const uint32_t*>(rbase + rows_bytes);
+    const uint4 desc = *reinterpret_cast<const uint4*>(rbase + rows_bytes + 8 * U);
 #pragma unroll
     for (int u = 0; u < UPL; ++u) {
       const int pos = lane + 32 * u;
-      const uint4* rows = reinterpret_cast<const uint4*>(rbase) + pos * (R >> 3);
+      if (ROW8) {
+        const uint2 q = reinterpret_cast<const uint2*>(rbase)[pos];
+        r[u].row[0] = make_uint4(q.x, q.y, 0u, 0u);
+      } else {
+        const uint4* rows = reinterpret_cast<const uint4*>(rbase) + pos * (R >> 3);
 #pragma unroll
-      for (int p = 0; p < RMAX / 8; ++p) r[u].row[p] = (p * 8 < R) ? rows[p] : make_uint4(~0u, ~0u, ~0u, ~0u);
+        for (int p = 0; p < RMAX / 8; ++p) r[u].row[p] = (p * 8 < R) ? rows[p] : make_uint4(~0u, ~0u, ~0u, ~0u);
+      }
       r[u].pb = pbs[pos];
       r[u].gid = (int32_t)pbs[U + pos];
       r[u].desc = desc;
@@ -1631,7 +1658,7 @@ __global__ void __maxnreg__(DIM == 2 ? (UPL == 2 ? GZ_REGS2 : 80) : 152) k_sweep
     bool wa = false, wb = false;
     if (UPL == 2 && DIM == 2) {
       const bool va = (r[0].pb & 0x7fffu) != 0x7fffu, vb = (r[UPL - 1].pb & 0x7fffu) != 0x7fffu;
-      gz_update2<RMAX>(r[0], va, (int)(r[0].pb >> 28), r[UPL - 1], vb, (int)(r[UPL - 1].pb >> 28), R,
+      gz_update2<RMAX, ROW8>(r[0], va, (int)(r[0].pb >> 28), r[UPL - 1], vb, (int)(r[UPL - 1].pb >> 28), R,
                        reinterpret_cast<const uint4*>(rbase) + lane * (R >> 3),
                        reinterpret_cast<const uint4*>(rbase) + (lane + 32) * (R >> 3), sc, rcp, padv, oa, ob);
       wa = last && va && (r[0].pb & 0x8000u);  // owned vertices, final values of the pass
@@ -1903,9 +1930,69 @@ static int64_t kd_tiles(lms_mesh_s* m, int T, int32_t* tile_of, cudaStream_t s) 
 }
 
 struct GzNeeds {
+  bool row8 = false;  // the records were rewritten with 8-bit rows
   int64_t max_slots = 0, max_items = 0, max_meta16 = 0, max_row = 0;
   int64_t mean_meta16 = 0;  // region staging work per tile: meta 16-byte units (run pairs or ids)
 };
+
+// 8-bit rows: does every row entry of every record fit the one-byte code?
+__global__ void k_gzd_row8_check(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P, int U,
+                                 const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
+                                 const uint4* __restrict__ rec, uint32_t padv, int* bad) {
+  const int PC = P * C;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < NI * U; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t it = g / U;
+    const int pos = (int)(g - it * U);
+    const int64_t k = it_ks[it] / PC;
+    const GzTile t = tab[k];
+    if (t.R != 8) { atomicOr(bad, 1); continue; }
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(rec + t.rec_base + (it - sfirst[k * PC]) * t.rec16);
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(base) + pos * 8;
+    const int own = (int)(reinterpret_cast<const uint32_t*>(base + 2 * U * 8)[pos] & 0x7fffu);
+    bool ok = true;
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t x = row[w];
+      if (x >= padv) ok = ok && x < padv + 8;
+      else ok = ok && own != 0x7fff && (int)x - own >= -GZ_ROW8_BIAS && (int)x - own < GZ_ROW8_PAD - GZ_ROW8_BIAS;
+    }
+    if (!ok) atomicOr(bad, 1);
+  }
+}
+// rewrite every record with 8-bit rows (pb, gid and desc unchanged, moved up)
+__global__ void k_gzd_row8_convert(const int32_t* __restrict__ it_ks, int64_t NI, int C, int P, int U,
+                                   const GzTile* __restrict__ tab, const int64_t* __restrict__ sfirst,
+                                   const uint4* __restrict__ rec, uint32_t padv, uint4* __restrict__ rec8) {
+  const int PC = P * C;
+  const int r8 = gz_rec16_row8(U);
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < NI * U; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t it = g / U;
+    const int pos = (int)(g - it * U);
+    const int64_t k = it_ks[it] / PC;
+    const GzTile t = tab[k];
+    const unsigned char* base = reinterpret_cast<const unsigned char*>(rec + t.rec_base + (it - sfirst[k * PC]) * t.rec16);
+    unsigned char* dst = reinterpret_cast<unsigned char*>(rec8 + it * r8);
+    const uint16_t* row = reinterpret_cast<const uint16_t*>(base) + pos * 8;
+    const uint32_t* pb = reinterpret_cast<const uint32_t*>(base + 2 * U * 8);
+    const int own = (int)(pb[pos] & 0x7fffu);
+    uint32_t lo = 0, hi = 0;
+    for (int w = 0; w < 8; ++w) {
+      const uint32_t x = row[w];
+      const uint32_t b = x >= padv ? (uint32_t)GZ_ROW8_PAD + (x - padv) : (uint32_t)((int)x - own + GZ_ROW8_BIAS);
+      if (w < 4) lo |= b << (8 * w);
+      else hi |= b << (8 * (w - 4));
+    }
+    reinterpret_cast<uint2*>(dst)[pos] = make_uint2(lo, hi);
+    reinterpret_cast<uint32_t*>(dst + 8 * U)[pos] = pb[pos];                       // pb
+    reinterpret_cast<uint32_t*>(dst + 8 * U + 4 * U)[pos] = pb[U + pos];           // gid
+    if (pos < 4) reinterpret_cast<uint32_t*>(dst + 16 * U)[pos] = pb[2 * U + pos];  // desc
+  }
+}
+__global__ void k_gzd_row8_tab(GzTile* tab, int64_t K, int PC, const int64_t* __restrict__ sfirst, int U) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    tab[k].rec_base = sfirst[k * PC] * gz_rec16_row8(U);
+    tab[k].rec16 = (uint32_t)gz_rec16_row8(U);
+  }
+}
 
 // Build the GZ schedule for tiles of ~T owned vertices and P sweeps per pass.
 // Returns false (nothing kept) if the limits (region <= 32767 slots, items per
@@ -1927,6 +2014,7 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   const int64_t V = m->V;
   const int C = m->C;
   const int D = C * P;
+  out->row8 = false;
   DBuf<int32_t> tile_of(V, s);
   const int64_t K = kd ? kd_tiles(m, T, tile_of.p, s) : spatial_tiles(m, T, tile_of.p, s);
   const int kbits = bits_for(K + 1);
@@ -2189,6 +2277,30 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
     }
   }
   mark("records+deps");
+  // 8-bit rows when every record's slots fit (LMS_GZ_ROW8=0: keep 16-bit)
+  out->row8 = false;
+  if (m->dim == 2 && upl == 2 && NI > 0 && mx[3] <= 8 && env_int("LMS_GZ_ROW8", 1, 0, 1)) {
+    const uint32_t padv = (uint32_t)((mx[0] + 7) & ~7LL);
+    DBuf<int> bad(1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    k_gzd_row8_check<<<gsz(NI * 32 * upl), 256, 0, s>>>(it_ks.p, NI, C, P, 32 * upl, tab.p, sfirst.p, rec.p, padv,
+                                                          bad.p);
+    LMS_CHECK_LAUNCH();
+    int hb = 1;
+    LMS_TRY_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    if (hb == 0) {
+      DBuf<uint4> rec8(NI * gz_rec16_row8(32 * upl), s);
+      k_gzd_row8_convert<<<gsz(NI * 32 * upl), 256, 0, s>>>(it_ks.p, NI, C, P, 32 * upl, tab.p, sfirst.p, rec.p,
+                                                              padv, rec8.p);
+      LMS_CHECK_LAUNCH();
+      k_gzd_row8_tab<<<gsz(K), 256, 0, s>>>(tab.p, K, P * C, sfirst.p, 32 * upl);
+      LMS_CHECK_LAUNCH();
+      rec = std::move(rec8);
+      out->row8 = true;
+    }
+  }
+  mark("row8");
   // the non-empty tiles, in tile order
   DBuf<int32_t> tiles(K > 0 ? K : 1, s);
   int64_t nt = 0;
@@ -2217,7 +2329,8 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   S.gz_nreg = nreg_all;
   S.gz_nupd = nU;
   S.gz_items = NI;
-  S.gz_bytes = (rec16_all + meta16_all) * 16;
+  S.gz_bytes = ((out->row8 ? NI * gz_rec16_row8(32 * upl) : rec16_all) + meta16_all) * 16;
+  S.gz_row8 = out->row8;
   S.gz_max_reg = (int)mx[0];
   S.gz_K = K;
   S.gz_T = T;
@@ -2258,7 +2371,8 @@ static int64_t plan_layout(const GzNeeds& nd, int dim, int C, int P, int upl, in
   while (L->RR * L->BS < nw + L->BS) L->RR *= 2;
   L->RR_log2 = 0;
   while ((1 << L->RR_log2) < L->RR) ++L->RR_log2;
-  L->rec_bytes = gz_rec16(nd.max_row > 0 ? (int)((nd.max_row + 7) & ~7) : 8, 32 * upl) * 16;
+  L->rec_bytes = nd.row8 ? gz_rec16_row8(32 * upl) * 16
+                          : gz_rec16(nd.max_row > 0 ? (int)((nd.max_row + 7) & ~7) : 8, 32 * upl) * 16;
   L->U = 32 * upl;
   const int HW = gz_hdr_words(C, P);
   L->hdr_bytes = r16i(4 * (int64_t)HW);
@@ -2408,6 +2522,9 @@ static void launch_gz_t(lms_mesh_s* m, int j0, cudaStream_t s) {
   Schedule& S = m->sched;
   const bool want_stats_t = getenv("LMS_GZ_STATS") != nullptr;
   auto kern = want_stats_t ? k_sweep_gz<DIM, RMAX, UPL, true> : k_sweep_gz<DIM, RMAX, UPL, false>;
+  if (DIM == 2 && UPL == 2 && S.gz_row8)
+    kern = want_stats_t ? k_sweep_gz<DIM, RMAX, UPL, true, DIM == 2 && UPL == 2>
+                        : k_sweep_gz<DIM, RMAX, UPL, false, DIM == 2 && UPL == 2>;
   LMS_TRY_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S.gz_smem));
   int nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));

@@ -165,6 +165,7 @@ struct Schedule {
   int64_t gz_nupd = 0;      // sum over tiles of first-sweep updates
   int64_t gz_items = 0;     // work items (32 updates of one stage of one tile)
   int64_t gz_bytes = 0;     // schedule bytes (records + meta)
+  bool gz_row8 = false;     // records carry 8-bit row codes (relative to the vertex's slot; see gz.cu)
   int gz_max_reg = 0;       // largest region
   int64_t gz_ntiles = 0;    // non-empty tiles
   DBuf<int32_t> gz_tiles;   // [gz_ntiles] non-empty tile ids, ascending
