@@ -278,8 +278,11 @@ __device__ __forceinline__ void s2_bulk_g2s(void* dst, const void* src, uint32_t
       : "memory");
 }
 // rows longer than the staged width: the slab read directly, one neighbour
-// at a time (kept out of line: the common path's registers stay small)
-__device__ __noinline__ void s2_chunk_long(const int32_t* ch, int W, double4* X, int lane, uint64_t pf, uint64_t pl) {
+// at a time.  (Kept inline: compiled out of line (__noinline__) it gave wrong
+// results under the 24-warp / 72-register variant on the hub mesh of
+// tests/test_gpu_parity.py::test_s2_long_row; inline, both variants are
+// bit-exact and neither spills.)
+__device__ __forceinline__ void s2_chunk_long(const int32_t* ch, int W, double4* X, int lane, uint64_t pf, uint64_t pl) {
   s2_chunk<2, true>(ch, W, X, lane, pf, pl);
 }
 __device__ __forceinline__ void s2_cons_sync(int ncons) {
@@ -470,7 +473,10 @@ __global__ void __launch_bounds__((NCONS + 1) * 32, 1)
         if (lane == 0) s2_mbar_arrive(empty + slot);
         s2r_chunk<WMAX, NB>(u, W, v, X, padv, pl);
       } else {
+        // the descriptor read must have returned before the release lets the
+        // producer overwrite it: every lane stores the value it read first
         const long long off = s_off[slot];
+        reinterpret_cast<volatile int*>(s_fold)[warp * 32 + lane] = (int)off;
         __syncwarp();
         if (lane == 0) s2_mbar_arrive(empty + slot);
         s2_chunk_long(slab + off, W, X, lane, pf, pl);
