@@ -518,15 +518,25 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   // C-hop ghost zone of a tile is a small fraction of it
   if (m->sched_req == LMS_SCHED_GZ || (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->C <= 8)) {
     int Tg = m->tile_req > 0 ? m->tile_req : (m->dim == 2 ? 4096 : 512);
-    // few tiles per SM (under 2 at T = 4096): larger tiles, up to one per SM
-    // (C2 1024^2: 26.3 -> 24.6 us per sweep; the builder still shrinks T
-    // until two region buffers fit)
+    // few tiles per SM (under 2 at T = 4096): one tile per SM, T = V / SMs
+    // within [1024, 8192] (C2 1024^2: 26.3 -> 24.6 us per sweep; the
+    // paper-scale CP has 91 tiles at T = 4096, a third of the SMs idle; the
+    // builder still shrinks T until two region buffers fit)
     if (m->tile_req == 0 && m->dim == 2) {
       int nsm = 148;
       LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
-      if (m->V / 4096 < 2 * (int64_t)nsm) Tg = (int)std::max<int64_t>(4096, std::min<int64_t>(8192, m->V / nsm));
+      // ~nsm - 4 tiles: the kd balancer then finds a near-square count at
+      // or below the SM count (148 itself factors badly and doubles to 294)
+      if (m->V / 4096 < 2 * (int64_t)nsm)
+        Tg = (int)std::max<int64_t>(1024, std::min<int64_t>(8192, (m->V + nsm - 5) / (nsm - 4)));
     }
-    const int P = (m->sched_req == LMS_SCHED_GZ && m->lag_req > 0) ? m->lag_req : 1;
+    int P = (m->sched_req == LMS_SCHED_GZ && m->lag_req > 0) ? m->lag_req : 1;
+    // AUTO on small 2D meshes: several sweeps per pass, the per-pass region
+    // staging and stage ramp paid once for P sweeps (CP, the paper-scale
+    // 372 K-vertex mesh: 18.4 -> 12.3 us per sweep at P = 2; C1 (10 K):
+    // 14.3 -> 8.6 at P = 4; C2 (1 M): P = 1 stays best)
+    if (m->sched_req == LMS_SCHED_AUTO && m->dim == 2 && m->lag_req == 0 && !getenv("LMS_GZ_P1"))
+      P = m->V < (1 << 15) ? 4 : (m->V < (1 << 19) ? 2 : 1);
     if (build_gz(m, Tg, P, m->sched_req == LMS_SCHED_GZ, s)) {
       S.kind = LMS_SCHED_GZ;
       S.lag = 0;

@@ -20,6 +20,7 @@ p.add_argument("--config", default="C3")
 p.add_argument("--orderings", default="original,bfs,rdr")
 p.add_argument("--schedule", default="auto")
 p.add_argument("--tile", type=int, default=0)
+p.add_argument("--lag", type=int, default=0, help="GZ: sweeps per pass")
 p.add_argument("--n1", type=int, default=2)
 p.add_argument("--n2", type=int, default=42)
 p.add_argument("--reps", type=int, default=3)
@@ -46,7 +47,7 @@ for kind in a.orderings.split(","):
         V, nnz, dim = inf["V"], inf["nnz"], inf["dim"]
         if kind != "original":
             gm.permute(gm.order(kind, 803 if kind == "random" else 0))
-        gm.set_schedule(a.schedule, a.tile, 0)
+        gm.set_schedule(a.schedule, a.tile, a.lag)
         gm.smooth(1)
         vfree = gm.schedule_info()["n_free"]
         bsw = 4 * (V + 1) + 4 * nnz + 8 * dim * V + 8 * dim * vfree
