@@ -69,6 +69,7 @@
 #include <cmath>
 #include <cstring>
 #include <utility>
+#include <vector>
 
 #include "lms_internal.cuh"
 
@@ -219,6 +220,176 @@ __global__ void k_gz_collect_u(const uint64_t* __restrict__ keys, int64_t n, int
 __global__ void k_gz_tile_off(const uint64_t* __restrict__ keys, int64_t n, int64_t K, int64_t* off) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= K; k += (int64_t)gridDim.x * blockDim.x)
     off[k] = lower_bound_u64(keys, 0, n, (uint64_t)k << 32);
+}
+
+// ---------------------------------------------------------------- per-tile ghost-zone BFS
+// The fast path of the level, update-set and region phases when every tile's
+// ghost zone lies in a window of GZB_BITS consecutive ids (original / BFS-like
+// orderings of a grid: a 64 x 64 kd tile of C4 spans ~0.3 M ids): one CTA per
+// tile walks the rings in shared memory, a bit per id for "reached" (vis) and
+// "in the region" (rg), instead of the global expand / sort / unique / set
+// difference per ring.  It computes the same sets as the sort path (k_gz_cnt
+// .. k_gz_collect_u and the region expansion above):
+//   * BFS distance through free vertices from the tile's owned free vertices
+//     (fixed vertices are never expanded, so they never enter a ring);
+//   * U = { free u : dist(u) + colour(u) <= D - 1 }, with ud = dist(u);
+//   * region = U and all neighbours of U, ascending id (the sort path's
+//     (tile, id) order).
+// Two launches: COUNT gives the per-tile sizes (for the offsets and the
+// allocations), WRITE repeats the walk and stores.  Any id outside the
+// window or a ring longer than GZB_FCAP sets *bad and the caller takes the
+// sort path (nothing of this pass is used then).
+constexpr int GZB_THREADS = 1024;
+constexpr int GZB_WORDS = 16384;  // 512 K ids per window
+constexpr int64_t GZB_BITS = 32 * (int64_t)GZB_WORDS;
+constexpr int GZB_FCAP = 6144;    // ring capacity (ring 0 is read from lev0)
+constexpr int GZB_SMEM = 2 * GZB_WORDS * 4 + 2 * GZB_FCAP * 4;
+
+// set bit p of a shared bitmap, one atomic per distinct word among the active
+// lanes (level 0 marks consecutive ids: ~32 lanes share a word)
+__device__ __forceinline__ void gzb_or_agg(uint32_t* bm, int64_t p) {
+  const uint32_t w = (uint32_t)(p >> 5), bit = 1u << (p & 31);
+  const unsigned am = __activemask();
+  const unsigned g = __match_any_sync(am, w);
+  const uint32_t bits = __reduce_or_sync(g, bit);
+  if ((threadIdx.x & 31) == __ffs(g) - 1) atomicOr(bm + w, bits);
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(GZB_THREADS, 1)
+    k_gz_bfs_tile(const uint64_t* __restrict__ lev0, const int64_t* __restrict__ own_off, int64_t K, int D,
+                  const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const uint8_t* __restrict__ fixed,
+                  const int8_t* __restrict__ colour, int64_t* __restrict__ nUk, int64_t* __restrict__ nRk,
+                  const int64_t* __restrict__ u_off, const int64_t* __restrict__ r_off, uint64_t* __restrict__ ukey,
+                  uint8_t* __restrict__ ud, uint64_t* __restrict__ reg, int* bad) {
+  extern __shared__ __align__(16) unsigned char gzb_sm[];
+  uint32_t* vis = reinterpret_cast<uint32_t*>(gzb_sm);
+  uint32_t* rg = vis + GZB_WORDS;
+  int32_t* fr0 = reinterpret_cast<int32_t*>(rg + GZB_WORDS);
+  int32_t* fr1 = fr0 + GZB_FCAP;
+  __shared__ int s_n[2], s_u, s_bad;
+  __shared__ int s_wsum[GZB_THREADS / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
+    const int64_t a = own_off[k], b = own_off[k + 1];
+    for (int i = t; i < GZB_WORDS / 2; i += GZB_THREADS)  // vis and rg are contiguous
+      reinterpret_cast<uint4*>(vis)[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (t == 0) s_n[0] = 0, s_n[1] = 0, s_u = 0, s_bad = 0;
+    int64_t lo = 0;
+    if (b > a) {
+      const int64_t vmin = (int64_t)(lev0[a] & 0xffffffffull), vmax = (int64_t)(lev0[b - 1] & 0xffffffffull);
+      lo = vmin - (GZB_BITS - (vmax - vmin + 1)) / 2;
+      if (lo < 0) lo = 0;
+    }
+    __syncthreads();
+    auto inwin = [&](int64_t v) { return v >= lo && v < lo + GZB_BITS; };
+    for (int64_t i = a + t; i < b; i += GZB_THREADS) {  // ring 0 (every owned free vertex is in U)
+      const int64_t p = (int64_t)(lev0[i] & 0xffffffffull) - lo;
+      if (p < 0 || p >= GZB_BITS) {
+        s_bad = 1;
+      } else {
+        gzb_or_agg(vis, p);
+        gzb_or_agg(rg, p);
+      }
+    }
+    __syncthreads();
+    int cur = 0;
+    for (int L = 0; L < D; ++L) {  // no early exit: every thread must reach the barriers
+      const int64_t n = L == 0 ? b - a : min(s_n[cur], GZB_FCAP);
+      int32_t* fnext = cur ? fr0 : fr1;
+      const int32_t* fcur = cur ? fr1 : fr0;
+      for (int64_t i = t; i < n; i += GZB_THREADS) {
+        const int32_t u = L == 0 ? (int32_t)(lev0[a + i] & 0xffffffffull) : fcur[i];
+        if (!inwin(u)) {
+          s_bad = 1;
+          continue;
+        }
+        const bool isU = L + colour[u] <= D - 1;
+        if (isU) {
+          if (L > 0) {
+            const int64_t p = (int64_t)u - lo;
+            atomicOr(rg + (p >> 5), 1u << (p & 31));
+          }
+          const int j = atomicAdd(&s_u, 1);
+          if (WRITE) {
+            ukey[u_off[k] + j] = ((uint64_t)k << 32) | (uint32_t)u;
+            ud[u_off[k] + j] = (uint8_t)L;
+          }
+        }
+        const bool grow = L + 1 < D;
+        if (!isU && !grow) continue;
+        for (int32_t e = rp[u]; e < rp[u + 1]; ++e) {
+          const int32_t w = col[e];
+          if (!inwin(w)) {
+            s_bad = 1;
+            continue;
+          }
+          const int64_t p = (int64_t)w - lo;
+          const uint32_t bit = 1u << (p & 31);
+          // read before the atomic: most neighbours are already marked
+          if (isU && !(rg[p >> 5] & bit)) atomicOr(rg + (p >> 5), bit);
+          if (grow && !(vis[p >> 5] & bit) && !fixed[w] && !(atomicOr(vis + (p >> 5), bit) & bit)) {
+            const int j = atomicAdd(&s_n[cur ^ 1], 1);
+            if (j < GZB_FCAP) fnext[j] = w;
+            else s_bad = 1;
+          }
+        }
+      }
+      __syncthreads();
+      if (t == 0) s_n[cur] = 0;
+      cur ^= 1;
+      __syncthreads();
+    }
+    if (s_bad) {
+      if (t == 0) atomicOr(bad, 1);
+      __syncthreads();
+      continue;
+    }
+    // region size / ids: thread t owns words [t * WPT, (t + 1) * WPT)
+    constexpr int WPT = GZB_WORDS / GZB_THREADS;
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) c += __popc(rg[t * WPT + q]);
+    if (!WRITE) {
+      for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0) s_wsum[warp] = c;
+      __syncthreads();
+      if (t == 0) {
+        int64_t tot = 0;
+        for (int w = 0; w < GZB_THREADS / 32; ++w) tot += s_wsum[w];
+        nRk[k] = tot;
+        nUk[k] = s_u;
+      }
+    } else {
+      int x = c;  // inclusive warp scan, then the warp totals
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) s_wsum[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        int y = s_wsum[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+          const int z = __shfl_up_sync(0xffffffffu, y, o);
+          if (lane >= o) y += z;
+        }
+        s_wsum[lane] = y;
+      }
+      __syncthreads();
+      int64_t o = r_off[k] + (warp ? s_wsum[warp - 1] : 0) + x - c;
+      const uint64_t hi = (uint64_t)k << 32;
+      for (int q = 0; q < WPT; ++q) {
+        uint32_t wd = rg[t * WPT + q];
+        while (wd) {
+          const int bpos = __ffs(wd) - 1;
+          wd &= wd - 1;
+          reg[o++] = hi | (uint32_t)(lo + 32 * (int64_t)(t * WPT + q) + bpos);
+        }
+      }
+    }
+    __syncthreads();
+  }
 }
 
 __global__ void k_gz_low32(const uint64_t* __restrict__ keys, int64_t n, int32_t* out) {
@@ -1994,6 +2165,97 @@ __global__ void k_gzd_row8_tab(GzTile* tab, int64_t K, int PC, const int64_t* __
   }
 }
 
+// LMS_GZ_TILE_BFS_CHECK (tests): U as a set of (key, ud) and the region
+// (keys and per-tile offsets) compared on the host
+static bool gz_same_sets(const DBuf<uint64_t>& ua, const DBuf<uint8_t>& da, int64_t na, const DBuf<uint64_t>& ra,
+                         const DBuf<int64_t>& oa, int64_t nra, const DBuf<uint64_t>& ub, const DBuf<uint8_t>& db,
+                         int64_t nb, const DBuf<uint64_t>& rb, const DBuf<int64_t>& ob, int64_t nrb, int64_t K,
+                         cudaStream_t s) {
+  if (na != nb || nra != nrb) {
+    fprintf(stderr, "[gz check] |U| %lld vs %lld, |region| %lld vs %lld\n", (long long)na, (long long)nb,
+            (long long)nra, (long long)nrb);
+    return false;
+  }
+  auto h64 = [&](const uint64_t* d, int64_t n) {
+    std::vector<uint64_t> h(n);
+    if (n) LMS_TRY_CUDA(cudaMemcpyAsync(h.data(), d, n * 8, cudaMemcpyDeviceToHost, s));
+    return h;
+  };
+  auto h8 = [&](const uint8_t* d, int64_t n) {
+    std::vector<uint8_t> h(n);
+    if (n) LMS_TRY_CUDA(cudaMemcpyAsync(h.data(), d, n, cudaMemcpyDeviceToHost, s));
+    return h;
+  };
+  std::vector<uint64_t> hua = h64(ua.p, na), hub = h64(ub.p, nb), hra = h64(ra.p, nra), hrb = h64(rb.p, nrb);
+  std::vector<uint8_t> hda = h8(da.p, na), hdb = h8(db.p, nb);
+  std::vector<int64_t> hoa(K + 1), hob(K + 1);
+  LMS_TRY_CUDA(cudaMemcpyAsync(hoa.data(), oa.p, (K + 1) * 8, cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaMemcpyAsync(hob.data(), ob.p, (K + 1) * 8, cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  if (hra != hrb || hoa != hob) {
+    for (int64_t i = 0; i < nra; ++i)
+      if (hra[i] != hrb[i]) {
+        fprintf(stderr, "[gz check] region[%lld]: tile %llu id %llu vs tile %llu id %llu\n", (long long)i,
+                (unsigned long long)(hra[i] >> 32), (unsigned long long)(hra[i] & 0xffffffffull),
+                (unsigned long long)(hrb[i] >> 32), (unsigned long long)(hrb[i] & 0xffffffffull));
+        break;
+      }
+    return false;
+  }
+  std::vector<std::pair<uint64_t, uint8_t>> pa(na), pb(nb);
+  for (int64_t i = 0; i < na; ++i) pa[i] = {hua[i], hda[i]}, pb[i] = {hub[i], hdb[i]};
+  std::sort(pa.begin(), pa.end());
+  std::sort(pb.begin(), pb.end());
+  for (int64_t i = 0; i < na; ++i)
+    if (pa[i] != pb[i]) {
+      fprintf(stderr, "[gz check] U[%lld]: (%llx, %d) vs (%llx, %d)\n", (long long)i, (unsigned long long)pa[i].first,
+              pa[i].second, (unsigned long long)pb[i].first, pb[i].second);
+      return false;
+    }
+  return true;
+}
+
+// The per-tile shared-memory walk (k_gz_bfs_tile): fills U (ukey, ud, nU) and
+// the region (reg, reg_off, nreg_all) exactly as the sort path would, or
+// returns false (outputs untouched) when a ghost zone leaves its id window or
+// LMS_GZ_TILE_BFS=0.
+static bool gz_tile_bfs(lms_mesh_s* m, int64_t K, int D, const DBuf<uint64_t>& lev0, const DBuf<int64_t>& own_off,
+                        DBuf<uint64_t>& ukey, DBuf<uint8_t>& ud, int64_t& nU, DBuf<uint64_t>& reg,
+                        DBuf<int64_t>& reg_off, int64_t& nreg_all, cudaStream_t s) {
+  if (const char* e = getenv("LMS_GZ_TILE_BFS"))
+    if (atoi(e) == 0) return false;
+  if (K <= 0 || D > 255) return false;
+  int nsm = 0;
+  LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
+  const int grid = (int)std::min<int64_t>(K, nsm > 0 ? nsm : 1);
+  LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GZB_SMEM));
+  LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GZB_SMEM));
+  DBuf<int64_t> nUk(K, s), nRk(K, s), u_off(K + 1, s);
+  DBuf<int> bad(1, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+  k_gz_bfs_tile<false><<<grid, GZB_THREADS, GZB_SMEM, s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p, m->col.p,
+                                                            m->fixed.p, m->colour.p, nUk.p, nRk.p, nullptr, nullptr,
+                                                            nullptr, nullptr, nullptr, bad.p);
+  LMS_CHECK_LAUNCH();
+  int hbad = 0;
+  LMS_TRY_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  if (getenv("LMS_GZ_VERBOSE")) fprintf(stderr, "[gz] rings: %s\n", hbad ? "sort path (a ghost zone leaves its id window)" : "per-tile walk");
+  if (hbad) return false;
+  const int64_t tu = scan_i64(nUk.p, K, u_off.p, s);
+  const int64_t tr = scan_i64(nRk.p, K, reg_off.p, s);
+  ukey.alloc(tu > 0 ? tu : 1, s);
+  ud.alloc(tu > 0 ? tu : 1, s);
+  reg.alloc(tr > 0 ? tr : 1, s);
+  k_gz_bfs_tile<true><<<grid, GZB_THREADS, GZB_SMEM, s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p, m->col.p,
+                                                           m->fixed.p, m->colour.p, nullptr, nullptr, u_off.p,
+                                                           reg_off.p, ukey.p, ud.p, reg.p, bad.p);
+  LMS_CHECK_LAUNCH();
+  nU = tu;
+  nreg_all = tr;
+  return true;
+}
+
 // Build the GZ schedule for tiles of ~T owned vertices and P sweeps per pass.
 // Returns false (nothing kept) if the limits (region <= 32767 slots, items per
 // tile, `fits`: the shared-memory plan) are not met.
@@ -2044,59 +2306,79 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   }
   nlev[0] = m->n_free;
   mark("level0");
-  // levels 1..D-1: breadth-first rings through free vertices, per tile
-  for (int L = 1; L < D; ++L) {
-    DBuf<uint64_t> cand;
-    int64_t nc = expand(lev[L - 1], nlev[L - 1], m, 0, cand, s, L == 1 ? tile_of.p : nullptr);
-    sort_keys(cand, nc, kbits, idb, s);
-    nc = unique_keys(cand, nc, s);
-    DBuf<uint8_t> keep(nc > 0 ? nc : 1, s);
-    if (nc > 0) {
-      k_gz_not_in<<<gsz(nc), 256, 0, s>>>(cand.p, nc, lev[L - 1].p, nlev[L - 1], L >= 2 ? lev[L - 2].p : nullptr,
-                                          L >= 2 ? nlev[L - 2] : 0, keep.p);
-      LMS_CHECK_LAUNCH();
-    }
-    lev[L].alloc(nc > 0 ? nc : 1, s);
-    DBuf<int> nsel(1, s);
-    LMS_TRY_CUDA(cudaMemsetAsync(nsel.p, 0, sizeof(int), s));
-    if (nc > 0) {
-      size_t tb = 0;
-      LMS_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, cand.p, keep.p, lev[L].p, nsel.p, nc, s));
-      DBuf<char> tmp(tb, s);
-      LMS_TRY_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, cand.p, keep.p, lev[L].p, nsel.p, nc, s));
-    }
-    nlev[L] = read_i64(nsel.p, false, s);
-  }
-  mark("levels");
-  // update set U: free entries with L + colour <= D - 1
-  int64_t ntot = 0;
-  for (int L = 0; L < D; ++L) ntot += nlev[L];
-  DBuf<uint64_t> ukey(ntot > 0 ? ntot : 1, s);
-  DBuf<uint8_t> ud(ntot > 0 ? ntot : 1, s);
-  DBuf<unsigned long long> nu(1, s);
-  LMS_TRY_CUDA(cudaMemsetAsync(nu.p, 0, sizeof(unsigned long long), s));
-  for (int L = 0; L < D; ++L)
-    if (nlev[L] > 0) {
-      k_gz_collect_u<<<gsz(nlev[L]), 256, 0, s>>>(lev[L].p, nlev[L], L, D, m->fixed.p, m->colour.p, ukey.p, ud.p,
-                                                   nu.p);
-      LMS_CHECK_LAUNCH();
-    }
-  const int64_t nU = read_i64(nu.p, true, s);
-  for (int L = 1; L < D; ++L) lev[L].release();
-  mark("update set");
-  // region = U and its neighbours, sorted by (tile, id).  Every owned free
-  // vertex is in U (level 0, colour <= D - 1) and enters through `self`, so
-  // the expansion skips in-tile free neighbours (the tile_of filter)
-  DBuf<uint64_t> reg;
-  int64_t nreg_all = expand(ukey, nU, m, 1, reg, s, tile_of.p);
-  sort_keys(reg, nreg_all, kbits, idb, s);
-  nreg_all = unique_keys(reg, nreg_all, s);
-  DBuf<int64_t> reg_off(K + 1, s);
-  k_gz_tile_off<<<gsz(K + 1), 256, 0, s>>>(reg.p, nreg_all, K, reg_off.p);
-  LMS_CHECK_LAUNCH();
   DBuf<int64_t> own_off(K + 1, s);
   k_gz_tile_off<<<gsz(K + 1), 256, 0, s>>>(lev[0].p, nlev[0], K, own_off.p);
   LMS_CHECK_LAUNCH();
+  // rings, update set U and region: the per-tile shared-memory walk when every
+  // ghost zone fits its id window, else the sort path
+  int64_t nU = 0, nreg_all = 0;
+  DBuf<uint64_t> ukey, reg;
+  DBuf<uint8_t> ud;
+  DBuf<int64_t> reg_off(K + 1, s);
+  // the sort path: per ring an expansion, sort, unique and set difference
+  auto sort_path = [&](DBuf<uint64_t>& ukey_, DBuf<uint8_t>& ud_, int64_t& nU_, DBuf<uint64_t>& reg_,
+                       DBuf<int64_t>& reg_off_, int64_t& nreg_) {
+    // levels 1..D-1: breadth-first rings through free vertices, per tile
+    for (int L = 1; L < D; ++L) {
+      DBuf<uint64_t> cand;
+      int64_t nc = expand(lev[L - 1], nlev[L - 1], m, 0, cand, s, L == 1 ? tile_of.p : nullptr);
+      sort_keys(cand, nc, kbits, idb, s);
+      nc = unique_keys(cand, nc, s);
+      DBuf<uint8_t> keep(nc > 0 ? nc : 1, s);
+      if (nc > 0) {
+        k_gz_not_in<<<gsz(nc), 256, 0, s>>>(cand.p, nc, lev[L - 1].p, nlev[L - 1], L >= 2 ? lev[L - 2].p : nullptr,
+                                            L >= 2 ? nlev[L - 2] : 0, keep.p);
+        LMS_CHECK_LAUNCH();
+      }
+      lev[L].alloc(nc > 0 ? nc : 1, s);
+      DBuf<int> nsel(1, s);
+      LMS_TRY_CUDA(cudaMemsetAsync(nsel.p, 0, sizeof(int), s));
+      if (nc > 0) {
+        size_t tb = 0;
+        LMS_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, cand.p, keep.p, lev[L].p, nsel.p, nc, s));
+        DBuf<char> tmp(tb, s);
+        LMS_TRY_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, cand.p, keep.p, lev[L].p, nsel.p, nc, s));
+      }
+      nlev[L] = read_i64(nsel.p, false, s);
+    }
+    mark("levels");
+    // update set U: free entries with L + colour <= D - 1
+    int64_t ntot = 0;
+    for (int L = 0; L < D; ++L) ntot += nlev[L];
+    ukey_.alloc(ntot > 0 ? ntot : 1, s);
+    ud_.alloc(ntot > 0 ? ntot : 1, s);
+    DBuf<unsigned long long> nu(1, s);
+    LMS_TRY_CUDA(cudaMemsetAsync(nu.p, 0, sizeof(unsigned long long), s));
+    for (int L = 0; L < D; ++L)
+      if (nlev[L] > 0) {
+        k_gz_collect_u<<<gsz(nlev[L]), 256, 0, s>>>(lev[L].p, nlev[L], L, D, m->fixed.p, m->colour.p, ukey_.p, ud_.p,
+                                                     nu.p);
+        LMS_CHECK_LAUNCH();
+      }
+    nU_ = read_i64(nu.p, true, s);
+    for (int L = 1; L < D; ++L) lev[L].release();
+    mark("update set");
+    // region = U and its neighbours, sorted by (tile, id).  Every owned free
+    // vertex is in U (level 0, colour <= D - 1) and enters through `self`, so
+    // the expansion skips in-tile free neighbours (the tile_of filter)
+    nreg_ = expand(ukey_, nU_, m, 1, reg_, s, tile_of.p);
+    sort_keys(reg_, nreg_, kbits, idb, s);
+    nreg_ = unique_keys(reg_, nreg_, s);
+    k_gz_tile_off<<<gsz(K + 1), 256, 0, s>>>(reg_.p, nreg_, K, reg_off_.p);
+    LMS_CHECK_LAUNCH();
+  };
+  if (!gz_tile_bfs(m, K, D, lev[0], own_off, ukey, ud, nU, reg, reg_off, nreg_all, s)) {
+    sort_path(ukey, ud, nU, reg, reg_off, nreg_all);
+  } else if (getenv("LMS_GZ_TILE_BFS_CHECK")) {
+    // testing: the sort path must give the same U (as a set, with ud) and region
+    DBuf<uint64_t> ukey2, reg2;
+    DBuf<uint8_t> ud2;
+    DBuf<int64_t> reg_off2(K + 1, s);
+    int64_t nU2 = 0, nreg2 = 0;
+    sort_path(ukey2, ud2, nU2, reg2, reg_off2, nreg2);
+    if (!gz_same_sets(ukey, ud, nU, reg, reg_off, nreg_all, ukey2, ud2, nU2, reg2, reg_off2, nreg2, K, s))
+      fail(LMS_E_STATE, "GZ build: the per-tile walk and the sort path disagree (LMS_GZ_TILE_BFS_CHECK)");
+  }
   mark("region");
   // updates sorted by (tile, colour, sweeps needed desc, local index)
   DBuf<uint64_t> ck(nU > 0 ? nU : 1, s), ck2(nU > 0 ? nU : 1, s);
