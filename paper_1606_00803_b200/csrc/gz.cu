@@ -224,7 +224,7 @@ __global__ void k_gz_tile_off(const uint64_t* __restrict__ keys, int64_t n, int6
 
 // ---------------------------------------------------------------- per-tile ghost-zone BFS
 // The fast path of the level, update-set and region phases when every tile's
-// ghost zone lies in a window of GZB_BITS consecutive ids (original / BFS-like
+// ghost zone lies in a window of consecutive ids (original / BFS-like
 // orderings of a grid: a 64 x 64 kd tile of C4 spans ~0.3 M ids): one CTA per
 // tile walks the rings in shared memory, a bit per id for "reached" (vis) and
 // "in the region" (rg), instead of the global expand / sort / unique / set
@@ -237,13 +237,27 @@ __global__ void k_gz_tile_off(const uint64_t* __restrict__ keys, int64_t n, int6
 //     (tile, id) order).
 // Two launches: COUNT gives the per-tile sizes (for the offsets and the
 // allocations), WRITE repeats the walk and stores.  Any id outside the
-// window or a ring longer than GZB_FCAP sets *bad and the caller takes the
+// window or a ring longer than the ring capacity sets *bad and the caller takes the
 // sort path (nothing of this pass is used then).
-constexpr int GZB_THREADS = 1024;
-constexpr int GZB_WORDS = 16384;  // 512 K ids per window
-constexpr int64_t GZB_BITS = 32 * (int64_t)GZB_WORDS;
-constexpr int GZB_FCAP = 6144;    // ring capacity (ring 0 is read from lev0)
-constexpr int GZB_SMEM = 2 * GZB_WORDS * 4 + 2 * GZB_FCAP * 4;
+// The window (words of 32 ids, a multiple of GZB_THREADS) and the ring
+// capacity are launch parameters: a window sized to the tiles' owned id spans
+// lets two CTAs share an SM (C4: 320 K ids, 96 KB), the 512 K-id window with
+// its 176 KB takes one.
+constexpr int GZB_THREADS = 512;
+constexpr int GZB_WORDS_MAX = 16384;  // 512 K ids
+static int gzb_smem(int words, int fcap) { return 2 * words * 4 + 2 * fcap * 4; }
+
+// the largest owned id span of a tile (lev0 is sorted by (tile, id))
+__global__ void k_gz_own_span(const uint64_t* __restrict__ lev0, const int64_t* __restrict__ own_off, int64_t K,
+                              int64_t* span) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = own_off[k], b = own_off[k + 1];
+    if (b > a) {
+      const long long d = (long long)((lev0[b - 1] & 0xffffffffull) - (lev0[a] & 0xffffffffull)) + 1;
+      atomicMax(reinterpret_cast<unsigned long long*>(span), (unsigned long long)d);
+    }
+  }
+}
 
 // set bit p of a shared bitmap, one atomic per distinct word among the active
 // lanes (level 0 marks consecutive ids: ~32 lanes share a word)
@@ -256,36 +270,37 @@ __device__ __forceinline__ void gzb_or_agg(uint32_t* bm, int64_t p) {
 }
 
 template <bool WRITE>
-__global__ void __launch_bounds__(GZB_THREADS, 1)
+__global__ void __launch_bounds__(GZB_THREADS, 2)
     k_gz_bfs_tile(const uint64_t* __restrict__ lev0, const int64_t* __restrict__ own_off, int64_t K, int D,
                   const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const uint8_t* __restrict__ fixed,
                   const int8_t* __restrict__ colour, int64_t* __restrict__ nUk, int64_t* __restrict__ nRk,
                   const int64_t* __restrict__ u_off, const int64_t* __restrict__ r_off, uint64_t* __restrict__ ukey,
-                  uint8_t* __restrict__ ud, uint64_t* __restrict__ reg, int* bad) {
+                  uint8_t* __restrict__ ud, uint64_t* __restrict__ reg, int* bad, int words, int fcap) {
   extern __shared__ __align__(16) unsigned char gzb_sm[];
   uint32_t* vis = reinterpret_cast<uint32_t*>(gzb_sm);
-  uint32_t* rg = vis + GZB_WORDS;
-  int32_t* fr0 = reinterpret_cast<int32_t*>(rg + GZB_WORDS);
-  int32_t* fr1 = fr0 + GZB_FCAP;
+  uint32_t* rg = vis + words;
+  int32_t* fr0 = reinterpret_cast<int32_t*>(rg + words);
+  int32_t* fr1 = fr0 + fcap;
+  const int64_t nbits = 32 * (int64_t)words;
   __shared__ int s_n[2], s_u, s_bad;
   __shared__ int s_wsum[GZB_THREADS / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
     const int64_t a = own_off[k], b = own_off[k + 1];
-    for (int i = t; i < GZB_WORDS / 2; i += GZB_THREADS)  // vis and rg are contiguous
+    for (int i = t; i < words / 2; i += GZB_THREADS)  // vis and rg are contiguous
       reinterpret_cast<uint4*>(vis)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (t == 0) s_n[0] = 0, s_n[1] = 0, s_u = 0, s_bad = 0;
     int64_t lo = 0;
     if (b > a) {
       const int64_t vmin = (int64_t)(lev0[a] & 0xffffffffull), vmax = (int64_t)(lev0[b - 1] & 0xffffffffull);
-      lo = vmin - (GZB_BITS - (vmax - vmin + 1)) / 2;
+      lo = vmin - (nbits - (vmax - vmin + 1)) / 2;
       if (lo < 0) lo = 0;
     }
     __syncthreads();
-    auto inwin = [&](int64_t v) { return v >= lo && v < lo + GZB_BITS; };
+    auto inwin = [&](int64_t v) { return v >= lo && v < lo + nbits; };
     for (int64_t i = a + t; i < b; i += GZB_THREADS) {  // ring 0 (every owned free vertex is in U)
       const int64_t p = (int64_t)(lev0[i] & 0xffffffffull) - lo;
-      if (p < 0 || p >= GZB_BITS) {
+      if (p < 0 || p >= nbits) {
         s_bad = 1;
       } else {
         gzb_or_agg(vis, p);
@@ -295,7 +310,7 @@ __global__ void __launch_bounds__(GZB_THREADS, 1)
     __syncthreads();
     int cur = 0;
     for (int L = 0; L < D; ++L) {  // no early exit: every thread must reach the barriers
-      const int64_t n = L == 0 ? b - a : min(s_n[cur], GZB_FCAP);
+      const int64_t n = L == 0 ? b - a : min(s_n[cur], fcap);
       int32_t* fnext = cur ? fr0 : fr1;
       const int32_t* fcur = cur ? fr1 : fr0;
       for (int64_t i = t; i < n; i += GZB_THREADS) {
@@ -330,7 +345,7 @@ __global__ void __launch_bounds__(GZB_THREADS, 1)
           if (isU && !(rg[p >> 5] & bit)) atomicOr(rg + (p >> 5), bit);
           if (grow && !(vis[p >> 5] & bit) && !fixed[w] && !(atomicOr(vis + (p >> 5), bit) & bit)) {
             const int j = atomicAdd(&s_n[cur ^ 1], 1);
-            if (j < GZB_FCAP) fnext[j] = w;
+            if (j < fcap) fnext[j] = w;
             else s_bad = 1;
           }
         }
@@ -346,9 +361,8 @@ __global__ void __launch_bounds__(GZB_THREADS, 1)
       continue;
     }
     // region size / ids: thread t owns words [t * WPT, (t + 1) * WPT)
-    constexpr int WPT = GZB_WORDS / GZB_THREADS;
+    const int WPT = words / GZB_THREADS;
     int c = 0;
-#pragma unroll
     for (int q = 0; q < WPT; ++q) c += __popc(rg[t * WPT + q]);
     if (!WRITE) {
       for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -369,12 +383,13 @@ __global__ void __launch_bounds__(GZB_THREADS, 1)
       if (lane == 31) s_wsum[warp] = x;
       __syncthreads();
       if (warp == 0) {
-        int y = s_wsum[lane];
+        constexpr int NWARP = GZB_THREADS / 32;
+        int y = lane < NWARP ? s_wsum[lane] : 0;
         for (int o = 1; o < 32; o <<= 1) {
           const int z = __shfl_up_sync(0xffffffffu, y, o);
           if (lane >= o) y += z;
         }
-        s_wsum[lane] = y;
+        if (lane < NWARP) s_wsum[lane] = y;
       }
       __syncthreads();
       int64_t o = r_off[k] + (warp ? s_wsum[warp - 1] : 0) + x - c;
@@ -2227,29 +2242,48 @@ static bool gz_tile_bfs(lms_mesh_s* m, int64_t K, int D, const DBuf<uint64_t>& l
   if (K <= 0 || D > 255) return false;
   int nsm = 0;
   LMS_TRY_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, m->device));
-  const int grid = (int)std::min<int64_t>(K, nsm > 0 ? nsm : 1);
-  LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GZB_SMEM));
-  LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GZB_SMEM));
+  if (nsm <= 0) nsm = 1;
+  // window: 1.25 x the largest owned id span (two CTAs per SM when it fits
+  // 96 KB), else the largest window; a ghost zone outside it -> the next try
+  DBuf<int64_t> span(1, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(span.p, 0, sizeof(int64_t), s));
+  k_gz_own_span<<<gsz(K), 256, 0, s>>>(lev0.p, own_off.p, K, span.p);
+  LMS_CHECK_LAUNCH();
+  const int64_t maxspan = read_i64(span.p, true, s);
+  int w0 = (int)std::min<int64_t>(GZB_WORDS_MAX, ((maxspan * 5 / 4 + 31) / 32 + GZB_THREADS - 1) / GZB_THREADS * GZB_THREADS);
+  if (w0 < 2 * GZB_THREADS) w0 = 2 * GZB_THREADS;
   DBuf<int64_t> nUk(K, s), nRk(K, s), u_off(K + 1, s);
   DBuf<int> bad(1, s);
-  LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
-  k_gz_bfs_tile<false><<<grid, GZB_THREADS, GZB_SMEM, s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p, m->col.p,
-                                                            m->fixed.p, m->colour.p, nUk.p, nRk.p, nullptr, nullptr,
-                                                            nullptr, nullptr, nullptr, bad.p);
-  LMS_CHECK_LAUNCH();
-  int hbad = 0;
-  LMS_TRY_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  LMS_TRY_CUDA(cudaStreamSynchronize(s));
-  if (getenv("LMS_GZ_VERBOSE")) fprintf(stderr, "[gz] rings: %s\n", hbad ? "sort path (a ghost zone leaves its id window)" : "per-tile walk");
+  int words = 0, fcap = 0, grid = 0, hbad = 1;
+  for (int attempt = 0; attempt < 2 && hbad; ++attempt) {
+    words = attempt == 0 ? w0 : GZB_WORDS_MAX;
+    if (attempt == 1 && w0 == GZB_WORDS_MAX) break;
+    fcap = gzb_smem(words, 2048) <= 96 * 1024 ? 2048 : 6144;
+    const int sm = gzb_smem(words, fcap);
+    grid = (int)std::min<int64_t>(K, (int64_t)nsm * (sm <= 100 * 1024 ? 2 : 1));
+    LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    k_gz_bfs_tile<false><<<grid, GZB_THREADS, sm, s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p, m->col.p, m->fixed.p,
+                                                       m->colour.p, nUk.p, nRk.p, nullptr, nullptr, nullptr, nullptr,
+                                                       nullptr, bad.p, words, fcap);
+    LMS_CHECK_LAUNCH();
+    hbad = (int)read_i64(bad.p, false, s);
+  }
+  if (getenv("LMS_GZ_VERBOSE"))
+    fprintf(stderr, "[gz] rings: %s (owned span %lld, window %d ids, %d CTAs)\n",
+            hbad ? "sort path (a ghost zone leaves its id window)" : "per-tile walk", (long long)maxspan, 32 * words,
+            grid);
   if (hbad) return false;
   const int64_t tu = scan_i64(nUk.p, K, u_off.p, s);
   const int64_t tr = scan_i64(nRk.p, K, reg_off.p, s);
   ukey.alloc(tu > 0 ? tu : 1, s);
   ud.alloc(tu > 0 ? tu : 1, s);
   reg.alloc(tr > 0 ? tr : 1, s);
-  k_gz_bfs_tile<true><<<grid, GZB_THREADS, GZB_SMEM, s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p, m->col.p,
-                                                           m->fixed.p, m->colour.p, nullptr, nullptr, u_off.p,
-                                                           reg_off.p, ukey.p, ud.p, reg.p, bad.p);
+  k_gz_bfs_tile<true><<<grid, GZB_THREADS, gzb_smem(words, fcap), s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p,
+                                                                        m->col.p, m->fixed.p, m->colour.p, nullptr,
+                                                                        nullptr, u_off.p, reg_off.p, ukey.p, ud.p,
+                                                                        reg.p, bad.p, words, fcap);
   LMS_CHECK_LAUNCH();
   nU = tu;
   nreg_all = tr;
