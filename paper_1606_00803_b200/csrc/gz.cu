@@ -244,6 +244,7 @@ __global__ void k_gz_tile_off(const uint64_t* __restrict__ keys, int64_t n, int6
 // lets two CTAs share an SM (C4: 320 K ids, 96 KB), the 512 K-id window with
 // its 176 KB takes one.
 constexpr int GZB_THREADS = 512;
+constexpr int GZB_MAXC = 8;  // colours for the in-walk update sort (P = 1)
 constexpr int GZB_WORDS_MAX = 16384;  // 512 K ids
 static int gzb_smem(int words, int fcap) { return 2 * words * 4 + 2 * fcap * 4; }
 
@@ -275,7 +276,8 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
                   const int32_t* __restrict__ rp, const int32_t* __restrict__ col, const uint8_t* __restrict__ fixed,
                   const int8_t* __restrict__ colour, int64_t* __restrict__ nUk, int64_t* __restrict__ nRk,
                   const int64_t* __restrict__ u_off, const int64_t* __restrict__ r_off, uint64_t* __restrict__ ukey,
-                  uint8_t* __restrict__ ud, uint64_t* __restrict__ reg, int* bad, int words, int fcap) {
+                  uint8_t* __restrict__ ud, uint64_t* __restrict__ reg, int* bad, int words, int fcap,
+                  uint64_t* __restrict__ ck2, int32_t* __restrict__ cv2, uint8_t* __restrict__ tag) {
   extern __shared__ __align__(16) unsigned char gzb_sm[];
   uint32_t* vis = reinterpret_cast<uint32_t*>(gzb_sm);
   uint32_t* rg = vis + words;
@@ -284,6 +286,9 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
   const int64_t nbits = 32 * (int64_t)words;
   __shared__ int s_n[2], s_u, s_bad;
   __shared__ int s_wsum[GZB_THREADS / 32];
+  __shared__ int s_cs[GZB_MAXC][GZB_THREADS / 32];  // per colour: warp sums, then warp offsets
+  __shared__ int s_cb[GZB_MAXC];                     // per colour: bucket offset
+  __shared__ int s_run[GZB_MAXC];                    // per colour: slots placed so far
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
     const int64_t a = own_off[k], b = own_off[k + 1];
@@ -392,7 +397,8 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
         if (lane < NWARP) s_wsum[lane] = y;
       }
       __syncthreads();
-      int64_t o = r_off[k] + (warp ? s_wsum[warp - 1] : 0) + x - c;
+      const int rbase = (warp ? s_wsum[warp - 1] : 0) + x - c;  // region rank of the thread's first bit
+      int64_t o = r_off[k] + rbase;
       const uint64_t hi = (uint64_t)k << 32;
       for (int q = 0; q < WPT; ++q) {
         uint32_t wd = rg[t * WPT + q];
@@ -400,6 +406,78 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
           const int bpos = __ffs(wd) - 1;
           wd &= wd - 1;
           reg[o++] = hi | (uint32_t)(lo + 32 * (int64_t)(t * WPT + q) + bpos);
+        }
+      }
+      if (ck2) {
+        // P = 1: the update order (tile, colour, region rank) -- k_gz_ukey's key
+        // with nsw = 1 -- as a stable partition by colour of the region slots:
+        // (A) per-word rank prefix into vis (dead after the walk), (B) every
+        // update tags its slot with colour + 1 (tag: zeroed global scratch,
+        // one byte per region slot) and counts its colour, (C) the slots in
+        // rounds of one per thread: per colour a ballot, warp offsets, and a
+        // running count.
+        __syncthreads();
+        {
+          int run = rbase;
+          for (int q = 0; q < WPT; ++q) {
+            const uint32_t wd = rg[t * WPT + q];
+            vis[t * WPT + q] = (uint32_t)run;
+            run += __popc(wd);
+          }
+        }
+        if (t < GZB_MAXC) s_cb[t] = 0;
+        __syncthreads();
+        const int64_t u0 = u_off[k], nu = u_off[k + 1] - u0, r0 = r_off[k];
+        const int nr = (int)(r_off[k + 1] - r0);
+        for (int64_t i = t; i < nu; i += GZB_THREADS) {
+          const int32_t u = (int32_t)(ukey[u0 + i] & 0xffffffffull);
+          const int64_t p = (int64_t)u - lo;
+          const int w = (int)(p >> 5);
+          const int rank = (int)vis[w] + __popc(rg[w] & ((1u << (p & 31)) - 1u));
+          const int cu = colour[u];
+          tag[r0 + rank] = (uint8_t)(cu + 1);
+          atomicAdd(&s_cb[cu], 1);
+        }
+        __syncthreads();
+        if (t == 0) {
+          int base = 0;
+          for (int cc = 0; cc < GZB_MAXC; ++cc) {
+            const int v = s_cb[cc];
+            s_cb[cc] = base;
+            s_run[cc] = 0;
+            base += v;
+          }
+        }
+        __syncthreads();
+        const unsigned lt = (1u << lane) - 1u;
+        for (int j0 = 0; j0 < nr; j0 += GZB_THREADS) {
+          const int j = j0 + t;
+          const int tg = j < nr ? tag[r0 + j] : 0;
+          int pre = 0;
+#pragma unroll
+          for (int cc = 0; cc < GZB_MAXC; ++cc) {
+            const unsigned bm = __ballot_sync(0xffffffffu, tg == cc + 1);
+            if (tg == cc + 1) pre = __popc(bm & lt);
+            if (lane == 0) s_cs[cc][warp] = __popc(bm);
+          }
+          __syncthreads();
+          if (t < GZB_MAXC) {
+            int acc = s_run[t];
+            for (int w = 0; w < GZB_THREADS / 32; ++w) {
+              const int v = s_cs[t][w];
+              s_cs[t][w] = acc;
+              acc += v;
+            }
+            s_run[t] = acc;
+          }
+          __syncthreads();
+          if (tg) {
+            const int cu = tg - 1;
+            const int64_t dst = u0 + s_cb[cu] + s_cs[cu][warp] + pre;
+            ck2[dst] = ((uint64_t)k << 23) | ((uint64_t)cu << 19) | (uint64_t)j;
+            cv2[dst] = (int32_t)(reg[r0 + j] & 0xffffffffull);
+          }
+          __syncthreads();
         }
       }
     }
@@ -2236,7 +2314,9 @@ static bool gz_same_sets(const DBuf<uint64_t>& ua, const DBuf<uint8_t>& da, int6
 // LMS_GZ_TILE_BFS=0.
 static bool gz_tile_bfs(lms_mesh_s* m, int64_t K, int D, const DBuf<uint64_t>& lev0, const DBuf<int64_t>& own_off,
                         DBuf<uint64_t>& ukey, DBuf<uint8_t>& ud, int64_t& nU, DBuf<uint64_t>& reg,
-                        DBuf<int64_t>& reg_off, int64_t& nreg_all, cudaStream_t s) {
+                        DBuf<int64_t>& reg_off, int64_t& nreg_all, DBuf<uint64_t>* ck2, DBuf<int32_t>* cv2,
+                        bool* presorted, cudaStream_t s) {
+  *presorted = false;
   if (const char* e = getenv("LMS_GZ_TILE_BFS"))
     if (atoi(e) == 0) return false;
   if (K <= 0 || D > 255) return false;
@@ -2266,7 +2346,7 @@ static bool gz_tile_bfs(lms_mesh_s* m, int64_t K, int D, const DBuf<uint64_t>& l
     LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
     k_gz_bfs_tile<false><<<grid, GZB_THREADS, sm, s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p, m->col.p, m->fixed.p,
                                                        m->colour.p, nUk.p, nRk.p, nullptr, nullptr, nullptr, nullptr,
-                                                       nullptr, bad.p, words, fcap);
+                                                       nullptr, bad.p, words, fcap, nullptr, nullptr, nullptr);
     LMS_CHECK_LAUNCH();
     hbad = (int)read_i64(bad.p, false, s);
   }
@@ -2280,10 +2360,20 @@ static bool gz_tile_bfs(lms_mesh_s* m, int64_t K, int D, const DBuf<uint64_t>& l
   ukey.alloc(tu > 0 ? tu : 1, s);
   ud.alloc(tu > 0 ? tu : 1, s);
   reg.alloc(tr > 0 ? tr : 1, s);
+  const bool presort = ck2 != nullptr && !getenv("LMS_GZ_NO_PRESORT");
+  if (presort) {
+    ck2->alloc(tu > 0 ? tu : 1, s);
+    cv2->alloc(tu > 0 ? tu : 1, s);
+  }
+  *presorted = presort;
+  DBuf<uint8_t> tag(presort && tr > 0 ? tr : 1, s);
+  if (presort && tr > 0) LMS_TRY_CUDA(cudaMemsetAsync(tag.p, 0, tr, s));
   k_gz_bfs_tile<true><<<grid, GZB_THREADS, gzb_smem(words, fcap), s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p,
                                                                         m->col.p, m->fixed.p, m->colour.p, nullptr,
                                                                         nullptr, u_off.p, reg_off.p, ukey.p, ud.p,
-                                                                        reg.p, bad.p, words, fcap);
+                                                                        reg.p, bad.p, words, fcap,
+                                                                        presort ? ck2->p : nullptr,
+                                                                        presort ? cv2->p : nullptr, tag.p);
   LMS_CHECK_LAUNCH();
   nU = tu;
   nreg_all = tr;
@@ -2401,7 +2491,14 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
     k_gz_tile_off<<<gsz(K + 1), 256, 0, s>>>(reg_.p, nreg_, K, reg_off_.p);
     LMS_CHECK_LAUNCH();
   };
-  if (!gz_tile_bfs(m, K, D, lev[0], own_off, ukey, ud, nU, reg, reg_off, nreg_all, s)) {
+  // P = 1 with at most GZB_MAXC colours: the walk also emits the updates in
+  // k_gz_ukey's sorted order (ck2, cv2), no global sort
+  DBuf<uint64_t> ck2;
+  DBuf<int32_t> cv2;
+  bool presorted = false;
+  const bool want_presort = P == 1 && C <= GZB_MAXC;
+  if (!gz_tile_bfs(m, K, D, lev[0], own_off, ukey, ud, nU, reg, reg_off, nreg_all, want_presort ? &ck2 : nullptr,
+                   want_presort ? &cv2 : nullptr, &presorted, s)) {
     sort_path(ukey, ud, nU, reg, reg_off, nreg_all);
   } else if (getenv("LMS_GZ_TILE_BFS_CHECK")) {
     // testing: the sort path must give the same U (as a set, with ud) and region
@@ -2415,16 +2512,37 @@ static bool build_gz_once(lms_mesh_s* m, int T, int P, int upl, bool kd, cudaStr
   }
   mark("region");
   // updates sorted by (tile, colour, sweeps needed desc, local index)
-  DBuf<uint64_t> ck(nU > 0 ? nU : 1, s), ck2(nU > 0 ? nU : 1, s);
-  DBuf<int32_t> cv(nU > 0 ? nU : 1, s), cv2(nU > 0 ? nU : 1, s);
-  if (nU > 0) {
-    k_gz_ukey<<<gsz(nU), 256, 0, s>>>(ukey.p, ud.p, nU, reg.p, reg_off.p, m->colour.p, C, P, ck.p, cv.p);
-    LMS_CHECK_LAUNCH();
-    size_t tb = 0;
-    LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ck.p, ck2.p, cv.p, cv2.p, nU, 0, 23 + kbits, s));
-    DBuf<char> tmp(tb, s);
-    LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, ck.p, ck2.p, cv.p, cv2.p, nU, 0, 23 + kbits, s));
+  const bool check_presort = presorted && getenv("LMS_GZ_TILE_BFS_CHECK");
+  DBuf<uint64_t> ck2s;
+  DBuf<int32_t> cv2s;
+  if (!presorted || check_presort) {
+    DBuf<uint64_t> ck(nU > 0 ? nU : 1, s);
+    DBuf<int32_t> cv(nU > 0 ? nU : 1, s);
+    DBuf<uint64_t>& ko = presorted ? ck2s : ck2;
+    DBuf<int32_t>& vo = presorted ? cv2s : cv2;
+    ko.alloc(nU > 0 ? nU : 1, s);
+    vo.alloc(nU > 0 ? nU : 1, s);
+    if (nU > 0) {
+      k_gz_ukey<<<gsz(nU), 256, 0, s>>>(ukey.p, ud.p, nU, reg.p, reg_off.p, m->colour.p, C, P, ck.p, cv.p);
+      LMS_CHECK_LAUNCH();
+      size_t tb = 0;
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, ck.p, ko.p, cv.p, vo.p, nU, 0, 23 + kbits, s));
+      DBuf<char> tmp(tb, s);
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, ck.p, ko.p, cv.p, vo.p, nU, 0, 23 + kbits, s));
+    }
   }
+  if (check_presort && nU > 0) {
+    std::vector<uint64_t> a(nU), b(nU);
+    std::vector<int32_t> va(nU), vb(nU);
+    LMS_TRY_CUDA(cudaMemcpyAsync(a.data(), ck2.p, nU * 8, cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaMemcpyAsync(b.data(), ck2s.p, nU * 8, cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaMemcpyAsync(va.data(), cv2.p, nU * 4, cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaMemcpyAsync(vb.data(), cv2s.p, nU * 4, cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    if (a != b || va != vb) fail(LMS_E_STATE, "GZ build: the walk's update order differs from k_gz_ukey + sort (LMS_GZ_TILE_BFS_CHECK)");
+  }
+  ck2s.release();
+  cv2s.release();
   ukey.release();
   ud.release();
   const int64_t nkc = K * C;
