@@ -244,7 +244,9 @@ __global__ void k_gz_tile_off(const uint64_t* __restrict__ keys, int64_t n, int6
 // lets two CTAs share an SM (C4: 320 K ids, 96 KB), the 512 K-id window with
 // its 176 KB takes one.
 constexpr int GZB_THREADS = 512;
-constexpr int GZB_MAXC = 8;  // colours for the in-walk update sort (P = 1)
+constexpr int GZB_MAXC = 8;
+constexpr int GZB_B = 4;     // vertices per thread per round of the walk
+constexpr int GZB_W = 8;     // neighbours loaded at once  // colours for the in-walk update sort (P = 1)
 constexpr int GZB_WORDS_MAX = 16384;  // 512 K ids
 static int gzb_smem(int words, int fcap) { return 2 * words * 4 + 2 * fcap * 4; }
 
@@ -318,40 +320,68 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
       const int64_t n = L == 0 ? b - a : min(s_n[cur], fcap);
       int32_t* fnext = cur ? fr0 : fr1;
       const int32_t* fcur = cur ? fr1 : fr0;
-      for (int64_t i = t; i < n; i += GZB_THREADS) {
-        const int32_t u = L == 0 ? (int32_t)(lev0[a + i] & 0xffffffffull) : fcur[i];
-        if (!inwin(u)) {
-          s_bad = 1;
-          continue;
-        }
-        const bool isU = L + colour[u] <= D - 1;
-        if (isU) {
-          if (L > 0) {
-            const int64_t p = (int64_t)u - lo;
-            atomicOr(rg + (p >> 5), 1u << (p & 31));
-          }
-          const int j = atomicAdd(&s_u, 1);
-          if (WRITE) {
-            ukey[u_off[k] + j] = ((uint64_t)k << 32) | (uint32_t)u;
-            ud[u_off[k] + j] = (uint8_t)L;
-          }
-        }
-        const bool grow = L + 1 < D;
-        if (!isU && !grow) continue;
-        for (int32_t e = rp[u]; e < rp[u + 1]; ++e) {
-          const int32_t w = col[e];
-          if (!inwin(w)) {
+      // GZB_B vertices per thread per round: their row bounds, colours and
+      // first GZB_W neighbours are loaded together (independent loads in
+      // flight) before the shared-memory marking
+      for (int64_t i0 = t; i0 < n; i0 += GZB_B * GZB_THREADS) {
+        int32_t uu[GZB_B], e0[GZB_B], e1[GZB_B];
+        int cu[GZB_B];
+#pragma unroll
+        for (int j = 0; j < GZB_B; ++j) {
+          const int64_t i = i0 + (int64_t)j * GZB_THREADS;
+          uu[j] = i < n ? (L == 0 ? (int32_t)(lev0[a + i] & 0xffffffffull) : fcur[i]) : -1;
+          if (uu[j] >= 0 && !inwin(uu[j])) {
             s_bad = 1;
-            continue;
+            uu[j] = -1;
           }
-          const int64_t p = (int64_t)w - lo;
-          const uint32_t bit = 1u << (p & 31);
-          // read before the atomic: most neighbours are already marked
-          if (isU && !(rg[p >> 5] & bit)) atomicOr(rg + (p >> 5), bit);
-          if (grow && !(vis[p >> 5] & bit) && !fixed[w] && !(atomicOr(vis + (p >> 5), bit) & bit)) {
-            const int j = atomicAdd(&s_n[cur ^ 1], 1);
-            if (j < fcap) fnext[j] = w;
-            else s_bad = 1;
+        }
+#pragma unroll
+        for (int j = 0; j < GZB_B; ++j)
+          if (uu[j] >= 0) {
+            e0[j] = rp[uu[j]];
+            e1[j] = rp[uu[j] + 1];
+            cu[j] = colour[uu[j]];
+          }
+#pragma unroll
+        for (int j = 0; j < GZB_B; ++j) {
+          const int32_t u = uu[j];
+          if (u < 0) continue;
+          const bool isU = L + cu[j] <= D - 1;
+          if (isU) {
+            if (L > 0) {
+              const int64_t p = (int64_t)u - lo;
+              atomicOr(rg + (p >> 5), 1u << (p & 31));
+            }
+            const int q = atomicAdd(&s_u, 1);
+            if (WRITE) {
+              ukey[u_off[k] + q] = ((uint64_t)k << 32) | (uint32_t)u;
+              ud[u_off[k] + q] = (uint8_t)L;
+            }
+          }
+          const bool grow = L + 1 < D;
+          if (!isU && !grow) continue;
+          for (int32_t eb = e0[j]; eb < e1[j]; eb += GZB_W) {
+            int32_t ww[GZB_W];
+#pragma unroll
+            for (int q = 0; q < GZB_W; ++q) ww[q] = eb + q < e1[j] ? col[eb + q] : -1;
+#pragma unroll
+            for (int q = 0; q < GZB_W; ++q) {
+              const int32_t w = ww[q];
+              if (w < 0) continue;
+              if (!inwin(w)) {
+                s_bad = 1;
+                continue;
+              }
+              const int64_t p = (int64_t)w - lo;
+              const uint32_t bit = 1u << (p & 31);
+              // read before the atomic: most neighbours are already marked
+              if (isU && !(rg[p >> 5] & bit)) atomicOr(rg + (p >> 5), bit);
+              if (grow && !(vis[p >> 5] & bit) && !fixed[w] && !(atomicOr(vis + (p >> 5), bit) & bit)) {
+                const int r = atomicAdd(&s_n[cur ^ 1], 1);
+                if (r < fcap) fnext[r] = w;
+                else s_bad = 1;
+              }
+            }
           }
         }
       }
