@@ -250,7 +250,8 @@ constexpr int GZB_W = 8;     // neighbours loaded at once  // colours for the in
 constexpr int GZB_WORDS_MAX = 16384;  // 512 K ids
 static int gzb_smem(int words, int fcap) { return 2 * words * 4 + 2 * fcap * 4; }
 
-// the largest owned id span of a tile (lev0 is sorted by (tile, id))
+// the largest owned id span of a tile (lev0 is sorted by (tile, id)) and the
+// largest owned count
 __global__ void k_gz_own_span(const uint64_t* __restrict__ lev0, const int64_t* __restrict__ own_off, int64_t K,
                               int64_t* span) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
@@ -258,7 +259,30 @@ __global__ void k_gz_own_span(const uint64_t* __restrict__ lev0, const int64_t* 
     if (b > a) {
       const long long d = (long long)((lev0[b - 1] & 0xffffffffull) - (lev0[a] & 0xffffffffull)) + 1;
       atomicMax(reinterpret_cast<unsigned long long*>(span), (unsigned long long)d);
+      atomicMax(reinterpret_cast<unsigned long long*>(span + 1), (unsigned long long)(b - a));
     }
+  }
+}
+
+// slot mode of the walk: tile k's entries sit at k * cap; copy them to the
+// scanned offsets (one block per tile)
+__global__ void k_gz_compact(int64_t K, int64_t cap, const int64_t* __restrict__ nUk, const int64_t* __restrict__ u_off,
+                             const int64_t* __restrict__ nRk, const int64_t* __restrict__ r_off,
+                             const uint64_t* __restrict__ su, const uint8_t* __restrict__ sd,
+                             const uint64_t* __restrict__ sr, const uint64_t* __restrict__ sck,
+                             const int32_t* __restrict__ scv, uint64_t* __restrict__ ukey, uint8_t* __restrict__ ud,
+                             uint64_t* __restrict__ reg, uint64_t* __restrict__ ck2, int32_t* __restrict__ cv2) {
+  for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
+    const int64_t base = k * cap, nu = nUk[k], nr = nRk[k], uo = u_off[k], ro = r_off[k];
+    for (int64_t i = threadIdx.x; i < nu; i += blockDim.x) {
+      ukey[uo + i] = su[base + i];
+      ud[uo + i] = sd[base + i];
+      if (ck2) {
+        ck2[uo + i] = sck[base + i];
+        cv2[uo + i] = scv[base + i];
+      }
+    }
+    for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) reg[ro + i] = sr[base + i];
   }
 }
 
@@ -279,7 +303,7 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
                   const int8_t* __restrict__ colour, int64_t* __restrict__ nUk, int64_t* __restrict__ nRk,
                   const int64_t* __restrict__ u_off, const int64_t* __restrict__ r_off, uint64_t* __restrict__ ukey,
                   uint8_t* __restrict__ ud, uint64_t* __restrict__ reg, int* bad, int words, int fcap,
-                  uint64_t* __restrict__ ck2, int32_t* __restrict__ cv2, uint8_t* __restrict__ tag) {
+                  uint64_t* __restrict__ ck2, int32_t* __restrict__ cv2, uint8_t* __restrict__ tag, int64_t cap) {
   extern __shared__ __align__(16) unsigned char gzb_sm[];
   uint32_t* vis = reinterpret_cast<uint32_t*>(gzb_sm);
   uint32_t* rg = vis + words;
@@ -354,8 +378,13 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
             }
             const int q = atomicAdd(&s_u, 1);
             if (WRITE) {
-              ukey[u_off[k] + q] = ((uint64_t)k << 32) | (uint32_t)u;
-              ud[u_off[k] + q] = (uint8_t)L;
+              if (cap && q >= cap) {
+                s_bad = 1;
+              } else {
+                const int64_t ub = cap ? k * cap : u_off[k];
+                ukey[ub + q] = ((uint64_t)k << 32) | (uint32_t)u;
+                ud[ub + q] = (uint8_t)L;
+              }
             }
           }
           const bool grow = L + 1 < D;
@@ -427,8 +456,20 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
         if (lane < NWARP) s_wsum[lane] = y;
       }
       __syncthreads();
+      const int nr_tot = s_wsum[GZB_THREADS / 32 - 1];
+      if (cap) {  // slot mode: the counts go out with the data; a tile over its slots -> *bad
+        if (t == 0) {
+          nRk[k] = nr_tot;
+          nUk[k] = s_u;
+          if (nr_tot > cap) atomicOr(bad, 1);
+        }
+        if (nr_tot > cap) {
+          __syncthreads();
+          continue;
+        }
+      }
       const int rbase = (warp ? s_wsum[warp - 1] : 0) + x - c;  // region rank of the thread's first bit
-      int64_t o = r_off[k] + rbase;
+      int64_t o = (cap ? k * cap : r_off[k]) + rbase;
       const uint64_t hi = (uint64_t)k << 32;
       for (int q = 0; q < WPT; ++q) {
         uint32_t wd = rg[t * WPT + q];
@@ -457,8 +498,9 @@ __global__ void __launch_bounds__(GZB_THREADS, 2)
         }
         if (t < GZB_MAXC) s_cb[t] = 0;
         __syncthreads();
-        const int64_t u0 = u_off[k], nu = u_off[k + 1] - u0, r0 = r_off[k];
-        const int nr = (int)(r_off[k + 1] - r0);
+        const int64_t u0 = cap ? k * cap : u_off[k], nu = cap ? s_u : u_off[k + 1] - u0;
+        const int64_t r0 = cap ? k * cap : r_off[k];
+        const int nr = cap ? nr_tot : (int)(r_off[k + 1] - r0);
         for (int64_t i = t; i < nu; i += GZB_THREADS) {
           const int32_t u = (int32_t)(ukey[u0 + i] & 0xffffffffull);
           const int64_t p = (int64_t)u - lo;
@@ -2355,28 +2397,83 @@ static bool gz_tile_bfs(lms_mesh_s* m, int64_t K, int D, const DBuf<uint64_t>& l
   if (nsm <= 0) nsm = 1;
   // window: 1.25 x the largest owned id span (two CTAs per SM when it fits
   // 96 KB), else the largest window; a ghost zone outside it -> the next try
-  DBuf<int64_t> span(1, s);
-  LMS_TRY_CUDA(cudaMemsetAsync(span.p, 0, sizeof(int64_t), s));
+  DBuf<int64_t> span(2, s);
+  LMS_TRY_CUDA(cudaMemsetAsync(span.p, 0, 2 * sizeof(int64_t), s));
   k_gz_own_span<<<gsz(K), 256, 0, s>>>(lev0.p, own_off.p, K, span.p);
   LMS_CHECK_LAUNCH();
-  const int64_t maxspan = read_i64(span.p, true, s);
+  int64_t hs[2] = {0, 0};
+  LMS_TRY_CUDA(cudaMemcpyAsync(hs, span.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  LMS_TRY_CUDA(cudaStreamSynchronize(s));
+  const int64_t maxspan = hs[0], maxown = hs[1];
   int w0 = (int)std::min<int64_t>(GZB_WORDS_MAX, ((maxspan * 5 / 4 + 31) / 32 + GZB_THREADS - 1) / GZB_THREADS * GZB_THREADS);
   if (w0 < 2 * GZB_THREADS) w0 = 2 * GZB_THREADS;
   DBuf<int64_t> nUk(K, s), nRk(K, s), u_off(K + 1, s);
   DBuf<int> bad(1, s);
+  const bool presort = ck2 != nullptr && !getenv("LMS_GZ_NO_PRESORT");
+  auto setup = [&](int words_, int& fcap_, int& grid_) {
+    fcap_ = gzb_smem(words_, 2048) <= 96 * 1024 ? 2048 : 6144;
+    const int sm = gzb_smem(words_, fcap_);
+    grid_ = (int)std::min<int64_t>(K, (int64_t)nsm * (sm <= 100 * 1024 ? 2 : 1));
+    LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    return sm;
+  };
+  // one pass into per-tile slots of cap = 2 x the largest owned count + 1024
+  // entries (the counts come out with the data; a compaction to the scanned
+  // offsets follows), when the slots take under 4 GB; a tile over its slots
+  // or its window -> the two-pass form below (count, then write in place)
+  {
+    const int64_t cap = 2 * maxown + 1024;
+    const bool slots = !(getenv("LMS_GZ_WALK_SLOTS") && atoi(getenv("LMS_GZ_WALK_SLOTS")) == 0) &&
+                       K * cap * (presort ? 30 : 17) < (4ll << 30);
+    if (slots) {
+      int fcap1 = 0, grid1 = 0;
+      const int sm = setup(w0, fcap1, grid1);
+      DBuf<uint64_t> su(K * cap, s), sr(K * cap, s), sck(presort ? K * cap : 1, s);
+      DBuf<uint8_t> sd(K * cap, s), tag(presort ? K * cap : 1, s);
+      DBuf<int32_t> scv(presort ? K * cap : 1, s);
+      if (presort) LMS_TRY_CUDA(cudaMemsetAsync(tag.p, 0, K * cap, s));
+      LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+      k_gz_bfs_tile<true><<<grid1, GZB_THREADS, sm, s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p, m->col.p, m->fixed.p,
+                                                         m->colour.p, nUk.p, nRk.p, nullptr, nullptr, su.p, sd.p, sr.p,
+                                                         bad.p, w0, fcap1, presort ? sck.p : nullptr,
+                                                         presort ? scv.p : nullptr, tag.p, cap);
+      LMS_CHECK_LAUNCH();
+      const int hb = (int)read_i64(bad.p, false, s);
+      if (getenv("LMS_GZ_VERBOSE"))
+        fprintf(stderr, "[gz] rings: %s (owned span %lld, window %d ids, %d CTAs, one pass, %lld slots per tile)\n",
+                hb ? "slots overflow, two passes next" : "per-tile walk", (long long)maxspan, 32 * w0, grid1,
+                (long long)cap);
+      if (!hb) {
+        const int64_t tu = scan_i64(nUk.p, K, u_off.p, s);
+        const int64_t tr = scan_i64(nRk.p, K, reg_off.p, s);
+        ukey.alloc(tu > 0 ? tu : 1, s);
+        ud.alloc(tu > 0 ? tu : 1, s);
+        reg.alloc(tr > 0 ? tr : 1, s);
+        if (presort) {
+          ck2->alloc(tu > 0 ? tu : 1, s);
+          cv2->alloc(tu > 0 ? tu : 1, s);
+        }
+        k_gz_compact<<<(int)std::min<int64_t>(K, 4 * nsm), 256, 0, s>>>(
+            K, cap, nUk.p, u_off.p, nRk.p, reg_off.p, su.p, sd.p, sr.p, presort ? sck.p : nullptr,
+            presort ? scv.p : nullptr, ukey.p, ud.p, reg.p, presort ? ck2->p : nullptr, presort ? cv2->p : nullptr);
+        LMS_CHECK_LAUNCH();
+        *presorted = presort;
+        nU = tu;
+        nreg_all = tr;
+        return true;
+      }
+    }
+  }
   int words = 0, fcap = 0, grid = 0, hbad = 1;
   for (int attempt = 0; attempt < 2 && hbad; ++attempt) {
     words = attempt == 0 ? w0 : GZB_WORDS_MAX;
     if (attempt == 1 && w0 == GZB_WORDS_MAX) break;
-    fcap = gzb_smem(words, 2048) <= 96 * 1024 ? 2048 : 6144;
-    const int sm = gzb_smem(words, fcap);
-    grid = (int)std::min<int64_t>(K, (int64_t)nsm * (sm <= 100 * 1024 ? 2 : 1));
-    LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    LMS_TRY_CUDA(cudaFuncSetAttribute(k_gz_bfs_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    const int sm = setup(words, fcap, grid);
     LMS_TRY_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
     k_gz_bfs_tile<false><<<grid, GZB_THREADS, sm, s>>>(lev0.p, own_off.p, K, D, m->row_ptr.p, m->col.p, m->fixed.p,
                                                        m->colour.p, nUk.p, nRk.p, nullptr, nullptr, nullptr, nullptr,
-                                                       nullptr, bad.p, words, fcap, nullptr, nullptr, nullptr);
+                                                       nullptr, bad.p, words, fcap, nullptr, nullptr, nullptr, 0);
     LMS_CHECK_LAUNCH();
     hbad = (int)read_i64(bad.p, false, s);
   }
@@ -2390,7 +2487,6 @@ static bool gz_tile_bfs(lms_mesh_s* m, int64_t K, int D, const DBuf<uint64_t>& l
   ukey.alloc(tu > 0 ? tu : 1, s);
   ud.alloc(tu > 0 ? tu : 1, s);
   reg.alloc(tr > 0 ? tr : 1, s);
-  const bool presort = ck2 != nullptr && !getenv("LMS_GZ_NO_PRESORT");
   if (presort) {
     ck2->alloc(tu > 0 ? tu : 1, s);
     cv2->alloc(tu > 0 ? tu : 1, s);
@@ -2403,7 +2499,7 @@ static bool gz_tile_bfs(lms_mesh_s* m, int64_t K, int D, const DBuf<uint64_t>& l
                                                                         nullptr, u_off.p, reg_off.p, ukey.p, ud.p,
                                                                         reg.p, bad.p, words, fcap,
                                                                         presort ? ck2->p : nullptr,
-                                                                        presort ? cv2->p : nullptr, tag.p);
+                                                                        presort ? cv2->p : nullptr, tag.p, 0);
   LMS_CHECK_LAUNCH();
   nU = tu;
   nreg_all = tr;

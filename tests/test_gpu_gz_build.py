@@ -81,3 +81,28 @@ def test_tile_walk_full_size_c4(monkeypatch, capfd):
         gm.smooth(1)
         err = capfd.readouterr().err
         assert "per-tile walk" in err, err[-2000:]
+
+
+@pytest.mark.parametrize("slots", ["0", "1"])
+@pytest.mark.parametrize("presort", ["0", "1"])
+def test_tile_walk_forms(slots, presort, monkeypatch, capfd):
+    """Both forms of the walk -- one pass into per-tile slots (default) and
+    count-then-write (LMS_GZ_WALK_SLOTS=0, the fallback when a tile outgrows
+    its slots) -- with and without the in-walk update order
+    (LMS_GZ_NO_PRESORT), against the sort path and the oracle."""
+    monkeypatch.setenv("LMS_GZ_TILE_BFS_CHECK", "1")
+    monkeypatch.setenv("LMS_GZ_VERBOSE", "1")
+    monkeypatch.setenv("LMS_GZ_WALK_SLOTS", slots)
+    if presort == "0":
+        monkeypatch.setenv("LMS_GZ_NO_PRESORT", "1")
+    m = meshgen.grid2d(181, 131, 0.3, seed=51)
+    om = oracle.prepare(m)
+    want = oracle.smooth(om["coords"], om["row_ptr"], om["col"], om["colour"], om["C"], 4)
+    for tile, lag in [(0, 1), (300, 1), (0, 2)]:
+        with gpu_mesh(m) as gm:
+            gm.set_schedule("gz", tile=tile, lag=lag)
+            gm.smooth(4)
+            assert bits_equal(gpu_coords(gm), want), (tile, lag)
+        err = capfd.readouterr().err
+        assert "per-tile walk" in err
+        assert ("one pass" in err) == (slots == "1"), err
