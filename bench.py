@@ -75,6 +75,8 @@ def parse():
     p.add_argument("--lag", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--jobs-in-flight", type=int, default=3,
+                   help="e2e: jobs kept in flight on as many streams (job k on stream k %% N)")
     p.add_argument("--cpu-sweeps", type=int, default=2)
     p.add_argument("--force-dist", action="store_true",
                    help="take the multi-GPU path even at one rank (tests its plumbing under torchrun)")
@@ -417,12 +419,17 @@ def run_ours(args):
         torch.cuda.synchronize()
         lat_ms = sev[0].elapsed_time(sev[-1]) / n_e2e
         step_ms = [round(sev[k].elapsed_time(sev[k + 1]), 2) for k in range(n_e2e)]
-        # throughput with two jobs in flight (a serving loop): job k runs on
-        # stream k % 2, so one job's H2D / D2H copies (PCIe) overlap the other
-        # job's kernels; the kernels themselves still share the SMs.  Every job
-        # copies its whole input from pinned host memory and its result back.
-        strs = [torch.cuda.Stream(), torch.cuda.Stream()]
-        houts = [hout, [torch.empty(V, dtype=torch.float64).pin_memory() for _ in range(dim)]]
+        # throughput with N jobs in flight (a serving loop, N = 3 by default):
+        # job k runs on stream k % N, so one job's H2D / D2H copies (PCIe) and
+        # its host round trips overlap the other jobs' kernels; the kernels
+        # themselves still share the SMs.  Every job copies its whole input
+        # from pinned host memory and its result back.  (Measured on one box:
+        # N = 2 35.0-36.2 ms per job, N = 3 34.0-34.3, N = 4 stalls of
+        # 50-150 ms in some runs; profiles/round2/tile_walk/bench_nj*.)
+        nj = max(1, args.jobs_in_flight)
+        strs = [torch.cuda.Stream() for _ in range(nj)]
+        houts = [hout] + [[torch.empty(V, dtype=torch.float64).pin_memory() for _ in range(dim)] for _ in range(nj - 1)]
+        n_pipe = max(n_e2e, 2 * nj)
 
         def e2e_job(slot, keep):
             with torch.cuda.stream(strs[slot]):
@@ -442,30 +449,34 @@ def run_ours(args):
             torch.cuda.synchronize()
             a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             a.record(strs[0])
-            strs[1].wait_event(a)
+            for st in strs[1:]:
+                st.wait_event(a)
             for k in range(n):
-                e2e_job(k % 2, keep)
-            b.record(strs[1])
-            strs[0].wait_event(b)
+                e2e_job(k % nj, keep)
+            for st in strs[1:]:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                strs[0].wait_event(ev)
             c.record(strs[0])
             torch.cuda.synchronize()
             for g, _, _ in keep:
                 g.check()
                 g.close()
             return a.elapsed_time(c) / n
-        pipelined(n_e2e)  # warm: the allocator caches of both streams
+        pipelined(n_pipe)  # warm: the allocator caches of every stream
         # three timed runs of n_e2e jobs, the median reported (a single run
         # occasionally carries a one-off stall of a few hundred ms)
-        e_runs = [pipelined(n_e2e) for _ in range(3)]
+        e_runs = [pipelined(n_pipe) for _ in range(3)]
         e_ms = statistics.median(e_runs)
         e2e = {"value": vfree * sweeps / (e_ms / 1e3) * world, "unit": "vertex-updates/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
-               "jobs_in_flight": 2, "steps": n_e2e, "runs_ms_per_step": [round(x, 2) for x in e_runs],
+               "jobs_in_flight": nj, "steps": n_pipe, "runs_ms_per_step": [round(x, 2) for x in e_runs],
                "latency_ms_per_job": lat_ms, "serial_value": vfree * sweeps / (lat_ms / 1e3) * world,
                "serial_step_ms": step_ms, "phases_ms": e2e_phases,
                "path": "per job: build_csr_host (H2D elems, then CSR + colouring under the H2D of coords) -> order "
-                       "-> permute -> smooth(%d) -> D2H coords; %d jobs, two in flight on two streams (value, "
-                       "ms_per_step: the median of three such runs); serial_value / latency_ms_per_job: one job at a time" % (sweeps, n_e2e)}
+                       "-> permute -> smooth(%d) -> D2H coords; %d jobs, %d in flight on %d streams (value, "
+                       "ms_per_step: the median of three such runs); serial_value / latency_ms_per_job: one job at a time"
+                       % (sweeps, n_pipe, nj, nj)}
 
     cpu = None
     if rank == 0 and not args.no_cpu:

@@ -1,0 +1,2 @@
+O=gpurun_out/nj; mkdir -p $O
+for i in 1 2; do for n in 2 3 4; do python bench.py --no-cpu --steps 3 --jobs-in-flight $n > $O/bench_nj${n}_$i.log 2>&1; done; done
