@@ -75,7 +75,7 @@ def parse():
     p.add_argument("--lag", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--jobs-in-flight", type=int, default=3,
+    p.add_argument("--jobs-in-flight", type=int, default=4,
                    help="e2e: jobs kept in flight on as many streams (job k on stream k %% N)")
     p.add_argument("--cpu-sweeps", type=int, default=2)
     p.add_argument("--force-dist", action="store_true",
@@ -419,13 +419,14 @@ def run_ours(args):
         torch.cuda.synchronize()
         lat_ms = sev[0].elapsed_time(sev[-1]) / n_e2e
         step_ms = [round(sev[k].elapsed_time(sev[k + 1]), 2) for k in range(n_e2e)]
-        # throughput with N jobs in flight (a serving loop, N = 3 by default):
+        # throughput with N jobs in flight (a serving loop, N = 4 by default):
         # job k runs on stream k % N, so one job's H2D / D2H copies (PCIe) and
         # its host round trips overlap the other jobs' kernels; the kernels
         # themselves still share the SMs.  Every job copies its whole input
         # from pinned host memory and its result back.  (Measured on one box:
-        # N = 2 35.0-36.2 ms per job, N = 3 34.0-34.3, N = 4 stalls of
-        # 50-150 ms in some runs; profiles/round2/tile_walk/bench_nj*.)
+        # N = 2 35.0-36.2 ms per job, N = 3 34.0-34.3, N = 4 33.5-34.2 once
+        # the library's scratch cache holds all N jobs' blocks -- with a 16 GB
+        # cap N = 4 stalled 50-150 ms in some runs; profiles/round2/tile_walk/.)
         nj = max(1, args.jobs_in_flight)
         strs = [torch.cuda.Stream() for _ in range(nj)]
         houts = [hout] + [[torch.empty(V, dtype=torch.float64).pin_memory() for _ in range(dim)] for _ in range(nj - 1)]

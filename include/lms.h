@@ -378,7 +378,8 @@ int64_t lms_kernel_launches(void);
 /* Return the library's cached scratch blocks to the CUDA memory pool.
  * Every call's temporaries are freed stream-ordered into a host-side cache
  * keyed by (stream, size) and reused by later allocations on the same
- * stream; the cache holds at most LMS_CACHE_GB (environment, default 16 GB;
+ * stream; the cache holds at most LMS_CACHE_GB (environment, default a quarter
+ * of the device memory;
  * 0 disables it).  Call this to hand that memory back, for example before
  * destroying a stream the library was used on; the blocks are freed in each
  * owning stream's order.  Never fails. */

@@ -9,9 +9,13 @@
 // same stream: the blocks' previous uses precede any new use in that stream's
 // order, exactly the guarantee cudaFreeAsync + cudaMallocAsync gave.  A block
 // is reused for a request of at least 3/4 of its size.  Cached bytes are
-// capped (LMS_CACHE_GB, default 16 GB; 0 disables the cache); beyond the cap,
-// and on lms_cache_release(), blocks go back to the pool with cudaFreeAsync on
-// their stream.
+// capped (LMS_CACHE_GB; default a quarter of the device memory, 45 GB on a
+// B200; 0 disables the cache); beyond the cap, and on lms_cache_release(),
+// blocks go back to the pool with cudaFreeAsync on their stream.  (A 16 GB cap
+// was too small for three or four C4 jobs in flight -- each GZ build takes
+// ~1.1 GB of walk slots on its stream -- and the churn through the pool gave
+// 50-150 ms stalls: bench e2e with four jobs 7.6-22.6 G/s at 16 GB, 24.9 at
+// 64 GB; profiles/round2/tile_walk/bench_nj*, bench_c64_*.)
 #include <cstdlib>
 #include <map>
 #include <tuple>
@@ -83,7 +87,9 @@ void* ws_alloc(size_t bytes, cudaStream_t s) {
   {
     std::lock_guard<std::mutex> g(c.mu);
     if (!c.init) {
-      double gb = 16.0;
+      size_t fr = 0, tot = 0;
+      double gb = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? (double)tot / 4.0 / 1073741824.0 : 16.0;
+      cudaGetLastError();
       if (const char* e = getenv("LMS_CACHE_GB")) gb = atof(e);
       c.cap = gb > 0 ? (size_t)(gb * 1073741824.0) : 0;
       c.init = true;
