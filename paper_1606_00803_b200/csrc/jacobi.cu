@@ -8,14 +8,14 @@
 // result of lms_smooth's other schedules (reading Z1): it is offered
 // to compare convergence (the paper's loop is in place).
 //
-// Kernel: one CTA of 256 threads per 256 consecutive vertices.  The CTA's
-// column indices (one contiguous CSR range) are staged into shared memory by
-// coalesced 16-byte loads, so the index stream is read once at full width;
-// each thread then gathers its neighbours' (x, y[, z]) from the previous
-// buffer through the read-only path and writes the new value to the other
-// buffer (ping-pong; both buffers hold the fixed vertices).  Bytes per sweep:
-// row_ptr + col read once, coordinates read (gathers mostly hit L1/L2 for
-// banded orderings), free coordinates written once -- B_sweep of SURVEY 8(d).
+// Kernels: k_jacobi_direct (default; see its comment) and k_jacobi, the first
+// version (LMS_JACOBI_STAGED=1): one CTA of 256 threads per 256 consecutive
+// vertices, the CTA's column indices staged into shared memory by coalesced
+// 16-byte loads, a serial gather loop per thread.  Both write the new value
+// to the other buffer (ping-pong; both buffers hold the fixed vertices).
+// Bytes per sweep: row_ptr + col read once, coordinates read (gathers mostly
+// hit L1/L2 for banded orderings), free coordinates written once -- B_sweep
+// of SURVEY 8(d).  C4: 302 us per sweep direct, 452 staged.
 #include <cstdlib>
 
 #include "lms_internal.cuh"
