@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(JB) k_jacobi(const int32_t* __restrict__ rp, c
 }
 
 // The direct form (default): no staging and no CTA barrier.  A thread loads
-// its row bounds, then the first JU column indices of its row in ONE round of
+// its row bounds, then the first JU (8) column indices of its row in ONE round of
 // independent predicated loads (neighbouring threads' rows are adjacent in
 // col, so the warp's loads fall in the same few lines and hit L1 after the
 // first), then all JU x DIM coordinates in one more round, and adds them in
@@ -73,8 +73,7 @@ __global__ void __launch_bounds__(JB) k_jacobi(const int32_t* __restrict__ rp, c
 // rounds per vertex with 8-16 loads in flight in each, against the staged
 // form's five (chunk bounds, staging, barrier, own bounds, a serial gather
 // loop).  Same arithmetic and add order, so the result is bit-identical.
-constexpr int JU = 8;
-template <int DIM>
+template <int DIM, int JU>
 __global__ void __launch_bounds__(JB) k_jacobi_direct(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
                                                       const uint8_t* __restrict__ fixed, int64_t V,
                                                       const double* __restrict__ x0, const double* __restrict__ y0,
@@ -134,6 +133,8 @@ void run_jacobi(lms_mesh_s* m, int sweeps, cudaStream_t s) {
   const unsigned G = (unsigned)(chunks < (int64_t)sms * 8 ? chunks : (int64_t)sms * 8);
   // LMS_JACOBI_STAGED=1: the shared-memory staged form (kept for A/B timing)
   static const bool staged = [] { const char* e = getenv("LMS_JACOBI_STAGED"); return e && atoi(e) != 0; }();
+  // 3D: LMS_JACOBI_JU=16 loads 16 neighbours per round instead of 8 (A/B)
+  static const bool ju16 = [] { const char* e = getenv("LMS_JACOBI_JU"); return e && atoi(e) == 16; }();
   for (int i = 0; i < sweeps; ++i) {
     double* z0 = m->dim == 3 ? m->x[2].p : nullptr;
     double* z1 = m->dim == 3 ? m->xalt[2].p : nullptr;
@@ -142,15 +143,18 @@ void run_jacobi(lms_mesh_s* m, int sweeps, cudaStream_t s) {
         k_jacobi<2><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, z0,
                                      m->xalt[0].p, m->xalt[1].p, z1);
       else
-        k_jacobi_direct<2><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, z0,
+        k_jacobi_direct<2, 8><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, z0,
                                             m->xalt[0].p, m->xalt[1].p, z1);
     } else {
       if (staged)
         k_jacobi<3><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, z0,
                                      m->xalt[0].p, m->xalt[1].p, z1);
+      else if (ju16)
+        k_jacobi_direct<3, 16><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, z0,
+                                                m->xalt[0].p, m->xalt[1].p, z1);
       else
-        k_jacobi_direct<3><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, z0,
-                                            m->xalt[0].p, m->xalt[1].p, z1);
+        k_jacobi_direct<3, 8><<<G, JB, 0, s>>>(m->row_ptr.p, m->col.p, m->fixed.p, V, m->x[0].p, m->x[1].p, z0,
+                                               m->xalt[0].p, m->xalt[1].p, z1);
     }
     LMS_CHECK_LAUNCH();
     for (int a = 0; a < m->dim; ++a) std::swap(m->x[a], m->xalt[a]);
