@@ -144,6 +144,8 @@ struct Schedule {
   DBuf<long long> s2_choff;
   DBuf<int32_t> s2_chw;
   std::vector<int64_t> s2_cstart;  // [C + 1] first chunk of each colour
+  DBuf<int32_t> s2d_cv;            // S2 direct: the free vertices sorted by colour (stable)
+  std::vector<int64_t> s2d_cstart; // [C + 1] first position of each colour in s2d_cv
   DBuf<int32_t> s2_crange;        // [C * (G + 1)] persistent S2: chunk range of each (colour, CTA)
   int s2_G = 0;                    // persistent S2 CTAs (one per SM, at most K)
   int s2_wmax = 16;                // widest item row count (S2 ring slot size)

@@ -21,6 +21,7 @@
 // graph.  The interleaved copy is made at the start of an lms_smooth call and
 // written back to the SoA arrays at its end.
 #include <cooperative_groups.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -550,8 +551,122 @@ static int s2_blocks(lms_mesh_s* m) {
   return nsm * 8;  // 8 CTAs of 256 threads per SM: warps stride the colour's chunks
 }
 
+// ---------------------------------------------------------------- S2 direct
+// The per-colour launch in the form of jacobi.cu's k_jacobi_direct: a thread
+// per free vertex of the colour (cv: the free vertices sorted by colour,
+// ascending label inside a colour), row bounds, then 8 column indices, then
+// 8 x 3 coordinates, each one round of independent loads straight from the
+// relabelled CSR and the SoA coordinates, adds in CSR order (Eq. 1,
+// P:244-251; bit-identical to S1/S2).  No slab, no chunk descriptors, no
+// interleaved copy.  A launch reads only other colours' coordinates and
+// writes only its own colour's, so in-place is the colour-GS order.
+__global__ void k_s2d_keys(const int8_t* __restrict__ colour, const uint8_t* __restrict__ fixed, int64_t V,
+                           uint8_t* __restrict__ key, int32_t* __restrict__ id) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    key[v] = fixed[v] ? (uint8_t)255 : (uint8_t)colour[v];
+    id[v] = (int32_t)v;
+  }
+}
+__global__ void k_s2d_hist(const uint8_t* __restrict__ key, int64_t V, unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int h[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[key[v]], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+constexpr int S2D_JU = 8;
+__global__ void __launch_bounds__(256) k_sweep_s2_direct(const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                         const int32_t* __restrict__ cv, int64_t t0, int64_t t1,
+                                                         double* x, double* y, double* z) {
+  const int64_t t = t0 + (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (t >= t1) return;
+  const int32_t v = __ldg(cv + t);
+  const int32_t b = __ldg(rp + v), e = __ldg(rp + v + 1);
+  const int32_t n = e - b;
+  int32_t u[S2D_JU];
+#pragma unroll
+  for (int i = 0; i < S2D_JU; ++i) u[i] = i < n ? __ldg(col + b + i) : -1;
+  double gx[S2D_JU], gy[S2D_JU], gz[S2D_JU];
+#pragma unroll
+  for (int i = 0; i < S2D_JU; ++i) {
+    gx[i] = gy[i] = gz[i] = 0.0;
+    if (u[i] >= 0) {
+      gx[i] = x[u[i]];
+      gy[i] = y[u[i]];
+      gz[i] = z[u[i]];
+    }
+  }
+  double sx = gx[0], sy = gy[0], sz = gz[0];
+#pragma unroll
+  for (int i = 1; i < S2D_JU; ++i)
+    if (i < n) {
+      sx = __dadd_rn(sx, gx[i]);
+      sy = __dadd_rn(sy, gy[i]);
+      sz = __dadd_rn(sz, gz[i]);
+    }
+  for (int32_t i = S2D_JU; i < n; ++i) {
+    const int32_t w = __ldg(col + b + i);
+    sx = __dadd_rn(sx, x[w]);
+    sy = __dadd_rn(sy, y[w]);
+    sz = __dadd_rn(sz, z[w]);
+  }
+  const double d = (double)n;
+  x[v] = __ddiv_rn(sx, d);
+  y[v] = __ddiv_rn(sy, d);
+  z[v] = __ddiv_rn(sz, d);
+}
+
+static void run_s2_direct(lms_mesh_s* m, int sweeps, cudaStream_t s) {
+  Schedule& S = m->sched;
+  const int64_t V = m->V;
+  const int C = m->C;
+  if (!S.s2d_cv.p) {
+    DBuf<uint8_t> key(V, s), key2(V, s);
+    DBuf<int32_t> id(V, s);
+    DBuf<unsigned long long> hist(256, s);
+    S.s2d_cv.alloc(V, s);
+    const unsigned G = grid_for(V, 256) > 4096 ? 4096 : grid_for(V, 256);
+    k_s2d_keys<<<G, 256, 0, s>>>(m->colour.p, m->fixed.p, V, key.p, id.p);
+    LMS_CHECK_LAUNCH();
+    LMS_TRY_CUDA(cudaMemsetAsync(hist.p, 0, 256 * sizeof(unsigned long long), s));
+    k_s2d_hist<<<G, 256, 0, s>>>(key.p, V, hist.p);
+    LMS_CHECK_LAUNCH();
+    size_t tb = 0;
+    LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, id.p, S.s2d_cv.p, (int)V, 0, 8, s));
+    {
+      DBuf<char> tmp(tb, s);
+      LMS_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key2.p, id.p, S.s2d_cv.p, (int)V, 0, 8, s));
+    }
+    std::vector<unsigned long long> h(256);
+    LMS_TRY_CUDA(cudaMemcpyAsync(h.data(), hist.p, 256 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    LMS_TRY_CUDA(cudaStreamSynchronize(s));
+    S.s2d_cstart.assign(C + 1, 0);
+    for (int c = 0; c < C; ++c) S.s2d_cstart[c + 1] = S.s2d_cstart[c] + (int64_t)h[c];
+  }
+  sync_soa(m, s);
+  soa_changed(m);
+  for (int i = 0; i < sweeps; ++i)
+    for (int c = 0; c < C; ++c) {
+      const int64_t t0 = S.s2d_cstart[c], t1 = S.s2d_cstart[c + 1];
+      if (t1 <= t0) continue;
+      k_sweep_s2_direct<<<(unsigned)((t1 - t0 + 255) / 256), 256, 0, s>>>(m->row_ptr.p, m->col.p, S.s2d_cv.p, t0, t1,
+                                                                         m->x[0].p, m->x[1].p, m->x[2].p);
+      LMS_CHECK_LAUNCH();
+    }
+}
+
 void run_s2(lms_mesh_s* m, int sweeps, cudaStream_t s) {
   if (m->dim != 3) fail(LMS_E_ARG, "the S2 schedule is the 3D kernel (2D meshes use GZ)");
+  {  // LMS_S2_DIRECT=1: per-colour launches of the direct kernel (A/B against the slab forms)
+    static const bool direct = [] { const char* e = getenv("LMS_S2_DIRECT"); return e && atoi(e) != 0; }();
+    if (direct) {
+      run_s2_direct(m, sweeps, s);
+      return;
+    }
+  }
   Schedule& S = m->sched;
   const int64_t V = m->V, K = S.K;
   const int C = m->C;

@@ -504,6 +504,7 @@ void build_schedule(lms_mesh_s* m, cudaStream_t s) {
   S.valid = false;
   S.base_valid = false;
   S.s2_choff.release();  // S2 chunk lists belong to the previous schedule
+  S.s2d_cv.release();
   S.s2_chw.release();
   S.s2_crange.release();
   S.s2_nbptr.release();
